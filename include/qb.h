@@ -1,0 +1,145 @@
+/*
+ * qb.h — C ABI of the B200-native blocked randomized QB factorization
+ *        ("randQB_b" / "randQB_pb") of P.-G. Martinsson and S. Voronin,
+ *        "A randomized blocked algorithm for efficiently computing rank-revealing
+ *        factorizations of matrices", arXiv 1503.07157.
+ *
+ * Citations "P:n" are line numbers of the paper text (reference PAPER.md); readings Rn are
+ * the interpretations listed in DESIGN.md §3.
+ *
+ * Problem: given an m x n matrix A and a tolerance eps, find a
+ * rank k, an m x k matrix Q with orthonormal columns and a k x n matrix B = Q^* A with
+ * ||A - QB||_F <= eps; k is an OUTPUT.  The library runs Fig. 2 (randQB_b) for
+ * q = 0 and Fig. 4 (randQB_pb) with P = q power steps for q >= 1, block by block:
+ *   Omega_i = randn(n, b)                       (counter-based)
+ *   Q_i = orth(A Omega_i); q x {Q_i = orth(A^* Q_i); Q_i = orth(A Q_i)}
+ *   Q_i = orth(Q_i - Qbar Qbar^* Q_i)           (re-projection, line (3') / (8))
+ *   B_i = Q_i^* A;  A = A - Q_i B_i;  stop once ||A||_F <= eps   (R1, R4)
+ *
+ * Conventions for every entry point:
+ *   - All matrices are dense, FP64 (QB_F64) or FP32 (QB_F32) as chosen at qb_create.
+ *   - "device" pointers are CUDA device pointers on the context's device; the caller owns
+ *     everything it passes in; the context owns everything it hands out.
+ *   - Column-major means element (i, j) at ptr[i + j*ld]; row-major means ptr[i*ld + j].
+ *   - Calls are blocking with respect to the context stream unless stated otherwise and
+ *     return a qb_status; nothing is thrown across the ABI.  After QB_ERR_CUDA the context
+ *     must be destroyed.  qb_last_error() describes the last failure.
+ *   - A context is not thread-safe; use one per host thread.
+ */
+#ifndef QB_H_
+#define QB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qb_ctx_s* qb_ctx;
+
+typedef enum {
+  QB_OK = 0,                  /* converged: ||A - QB||_F <= eps (or k = 0)                    */
+  QB_NOT_CONVERGED = 1,       /* reached kmax with ||A - QB||_F > eps; outputs valid (R5)     */
+  QB_ERR_INVALID_ARG = 2,     /* bad dims / ld / b < 1 / q < 0 / eps < 0 or NaN / NaN-Inf in A */
+  QB_ERR_OOM = 3,             /* device allocation failed                                      */
+  QB_ERR_CUDA = 4,            /* CUDA runtime error (sticky; destroy the context)              */
+  QB_ERR_NCCL = 5,            /* NCCL error (distributed contexts)                             */
+  QB_ERR_ORTH_BREAKDOWN = 6,  /* CholeskyQR failed even after the shifted fallback (R8)        */
+  QB_ERR_UNSUPPORTED = 7      /* valid request this build does not implement (see message)     */
+} qb_status;
+
+typedef enum { QB_F64 = 0, QB_F32 = 1 } qb_dtype;
+
+/* qb_factor flags */
+enum {
+  QB_OVERWRITE_A = 1u,  /* A may be used as the residual workspace and is destroyed (P:112:
+                           "A^(j) can overwrite A^(j-1)"); requires lda even and A 16-byte
+                           aligned, otherwise an internal copy is made anyway.              */
+  QB_NO_REPROJ = 2u     /* skip line (3')/(8) — for demonstrating P:684-696 only            */
+};
+
+/* Per-block record (qb_stats).  r2 is the directly computed ||A^(i)||_F^2 (the stop test,
+ * R1); ei is the error indicator ||A||_F^2 - sum_j ||B_j||_F^2 (the Frobenius
+ * identity) recorded beside it.  fallback counts shifted-CholeskyQR retries in the block.  */
+typedef struct {
+  int64_t ell;        /* columns accepted after this block (= k so far)                     */
+  int64_t w;          /* width of this block (b, or less for the last block when capped)   */
+  double r2;          /* ||A^(i)||_F^2                                                      */
+  double ei;          /* ||A||_F^2 - sum_{j<=i} ||B_j||_F^2                                 */
+  double ms;          /* device time of the block (CUDA events), milliseconds               */
+  int32_t fallback;   /* number of shifted-CholeskyQR fallbacks taken in this block         */
+  int32_t reserved;
+} qb_block_stats;
+
+/* Create a context on CUDA device `device` computing in `dtype`.  `cuda_stream` is a
+ * cudaStream_t to run on, or NULL for a context-owned non-blocking stream.
+ * Errors: QB_ERR_INVALID_ARG (bad device / dtype), QB_ERR_CUDA.                           */
+qb_status qb_create(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream);
+
+/* Distributed context (column sharding): this process is rank `rank` of
+ * `nranks`, one GPU each; `nccl_unique_id` points to the 128-byte ncclUniqueId that rank 0
+ * created (qb_nccl_unique_id) and the caller broadcast.  Each rank passes its column shard
+ * A(:, col_offset : col_offset + n_local) to qb_factor with n = n_local and the global
+ * column count in `n_global`; Omega rows are drawn for the same global indices, so every P
+ * sees the same Omega.  Collective: all ranks call it.  Errors: QB_ERR_NCCL when NCCL is
+ * unavailable or fails, plus those of qb_create.                                           */
+qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream,
+                         int rank, int nranks, const void* nccl_unique_id,
+                         int64_t col_offset, int64_t n_global);
+
+/* Write a fresh ncclUniqueId (128 bytes) to `out128`.  QB_ERR_NCCL if NCCL is absent.      */
+qb_status qb_nccl_unique_id(void* out128);
+
+/* The factorization (Fig. 2 / Fig. 4).
+ *   A      device, column-major m x n, leading dimension lda >= m (the local column shard
+ *          for a distributed context).  Read-only unless QB_OVERWRITE_A.
+ *   eps    absolute Frobenius tolerance (R2), eps >= 0.  The loop stops after the first
+ *          block with ||A^(i)||_F^2 <= eps^2 (R4); ||A||_F <= eps returns k = 0 (R3).
+ *   b      block size >= 1 (b <= 512 in this build); q >= 0 power steps; seed selects Omega.
+ *   kmax   rank cap; <= 0 means min(m, n_global).  The last block is narrowed to hit it (R5).
+ * Outputs (all optional except k):
+ *   *k     rank found.   *resid = ||A^(k)||_F (direct, R1).
+ *   *Q     device, column-major m x k, leading dimension *ldq (context-owned, replicated on
+ *          every rank).  *B: device, ROW-major k x n (row i = B(i, :)), leading dimension
+ *          *ldb (context-owned; the local column shard on a distributed context).  Both stay
+ *          valid until the next qb_factor or qb_destroy.
+ * Returns QB_OK, QB_NOT_CONVERGED (outputs valid), or an error.                           */
+qb_status qb_factor(qb_ctx ctx, void* A, int64_t m, int64_t n, int64_t lda, double eps,
+                    int64_t b, int q, uint64_t seed, int64_t kmax, unsigned flags,
+                    int64_t* k, const void** Q, int64_t* ldq, const void** B, int64_t* ldb,
+                    double* resid);
+
+/* Per-block records of the last qb_factor: copies min(cap, nblocks) records to `out`
+ * (may be NULL when cap = 0) and the total count to *nblocks.                              */
+qb_status qb_stats(qb_ctx ctx, qb_block_stats* out, int64_t cap, int64_t* nblocks);
+
+/* Omega(row0:row1, col0:col0+w) of the generator of DESIGN.md §3.3 ("randn(n,b)",
+ * eq. (OmegaBlock)) written ROW-major to device memory `out` (element (r, c) at
+ * out[(r - row0)*ldo + (c - col0)], ldo >= w), in the context dtype (FP32 = RN32 of the
+ * FP64 draw).  Asynchronous on the context stream.                                        */
+qb_status qb_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_t col0,
+                   int64_t w, void* out, int64_t ldo);
+
+/* orth(X) by CholeskyQR2 with the shifted-CholeskyQR3 fallback (R8): X is
+ * device, column-major m x w (ldx), overwritten by Q with orthonormal columns spanning
+ * ran(X); diag(R) > 0.  w <= 512.  Returns QB_ERR_ORTH_BREAKDOWN if even the shifted
+ * variant fails.  Blocking.                                                               */
+qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx);
+
+/* Partial SVD from the last factorization: B = Uhat D V^*, U = Q Uhat.
+ * NEXT-1 row; returns QB_ERR_UNSUPPORTED in this build.                                   */
+qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U, int64_t* ldu, const void** S,
+                  const void** V, int64_t* ldv);
+
+/* Number of the library's own kernel launches since the context was created.              */
+int64_t qb_kernel_launches(qb_ctx ctx);
+
+void qb_destroy(qb_ctx ctx);
+const char* qb_status_string(qb_status s);
+const char* qb_last_error(qb_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QB_H_ */

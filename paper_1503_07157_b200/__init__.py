@@ -1,0 +1,209 @@
+"""B200-native blocked randomized QB factorization (Martinsson & Voronin, arXiv 1503.07157).
+
+Thin Python binding over the C ABI in include/qb.h (libqb.so, built in-tree for sm_100a by
+``python -m paper_1503_07157_b200.build``).  This module only marshals arguments: every
+arithmetic step of the factorization runs in the library's CUDA kernels.  There is no CPU
+fallback — if libqb.so is missing or no B200 is visible, calls raise.
+
+Function names mirror the C entry points: qb_create, qb_factor, qb_stats, qb_omega, qb_orth,
+qb_destroy, qb_status_string, qb_last_error, qb_kernel_launches.  ``factor()`` is a
+convenience wrapper for torch CUDA tensors (torch supplies device memory only).
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqb.so")
+
+QB_OK = 0
+QB_NOT_CONVERGED = 1
+QB_ERR_INVALID_ARG = 2
+QB_ERR_OOM = 3
+QB_ERR_CUDA = 4
+QB_ERR_NCCL = 5
+QB_ERR_ORTH_BREAKDOWN = 6
+QB_ERR_UNSUPPORTED = 7
+
+QB_F64 = 0
+QB_F32 = 1
+
+QB_OVERWRITE_A = 1
+QB_NO_REPROJ = 2
+
+
+class QBError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_status_name(status)}: {msg}")
+        self.status = status
+
+
+class BlockStats(ctypes.Structure):
+    _fields_ = [("ell", ctypes.c_int64), ("w", ctypes.c_int64), ("r2", ctypes.c_double),
+                ("ei", ctypes.c_double), ("ms", ctypes.c_double), ("fallback", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded libqb.so (raises loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1503_07157_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        c_ctx = ctypes.c_void_p
+        i64, u64, dbl, vp = ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+        P = ctypes.POINTER
+        L.qb_create.argtypes = [P(c_ctx), ctypes.c_int, ctypes.c_int, vp]
+        L.qb_create_dist.argtypes = [P(c_ctx), ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
+                                     i64, i64]
+        L.qb_nccl_unique_id.argtypes = [vp]
+        L.qb_factor.argtypes = [c_ctx, vp, i64, i64, i64, dbl, i64, ctypes.c_int, u64, i64, ctypes.c_uint,
+                                P(i64), P(vp), P(i64), P(vp), P(i64), P(dbl)]
+        L.qb_stats.argtypes = [c_ctx, vp, i64, P(i64)]
+        L.qb_omega.argtypes = [c_ctx, u64, i64, i64, i64, i64, vp, i64]
+        L.qb_orth.argtypes = [c_ctx, vp, i64, i64, i64]
+        L.rqb_svd.argtypes = [c_ctx, i64, P(vp), P(i64), P(vp), P(vp), P(i64)]
+        L.qb_kernel_launches.argtypes = [c_ctx]
+        L.qb_kernel_launches.restype = i64
+        L.qb_destroy.argtypes = [c_ctx]
+        L.qb_destroy.restype = None
+        L.qb_status_string.argtypes = [ctypes.c_int]
+        L.qb_status_string.restype = ctypes.c_char_p
+        L.qb_last_error.argtypes = [c_ctx]
+        L.qb_last_error.restype = ctypes.c_char_p
+        for f in ("qb_create", "qb_create_dist", "qb_nccl_unique_id", "qb_factor", "qb_stats", "qb_omega",
+                  "qb_orth", "rqb_svd"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _status_name(s):
+    try:
+        return lib().qb_status_string(int(s)).decode()
+    except Exception:  # pragma: no cover
+        return f"status {s}"
+
+
+def qb_status_string(s):
+    return lib().qb_status_string(int(s)).decode()
+
+
+def qb_last_error(ctx):
+    return lib().qb_last_error(ctx).decode()
+
+
+def _check(ctx, s, ok=(QB_OK,)):
+    if s not in ok:
+        raise QBError(s, qb_last_error(ctx) if ctx else "")
+    return s
+
+
+def qb_create(device=0, dtype=QB_F64, stream=None):
+    ctx = ctypes.c_void_p()
+    s = lib().qb_create(ctypes.byref(ctx), int(device), int(dtype), stream)
+    if s != QB_OK:
+        msg = qb_last_error(ctx) if ctx.value else ""
+        if ctx.value:
+            lib().qb_destroy(ctx)
+        raise QBError(s, msg)
+    return ctx
+
+
+def qb_destroy(ctx):
+    if ctx is not None and ctx.value:
+        lib().qb_destroy(ctx)
+
+
+def qb_kernel_launches(ctx):
+    return int(lib().qb_kernel_launches(ctx))
+
+
+def qb_factor(ctx, A_ptr, m, n, lda, eps, b, q=0, seed=1, kmax=0, flags=0):
+    """Raw call: returns dict(status, k, Q, ldq, B, ldb, resid) with device pointers."""
+    k = ctypes.c_int64()
+    Q = ctypes.c_void_p()
+    ldq = ctypes.c_int64()
+    B = ctypes.c_void_p()
+    ldb = ctypes.c_int64()
+    resid = ctypes.c_double()
+    s = lib().qb_factor(ctx, ctypes.c_void_p(A_ptr), m, n, lda, float(eps), b, q, seed, kmax, flags,
+                        ctypes.byref(k), ctypes.byref(Q), ctypes.byref(ldq), ctypes.byref(B), ctypes.byref(ldb),
+                        ctypes.byref(resid))
+    _check(ctx, s, ok=(QB_OK, QB_NOT_CONVERGED))
+    return dict(status=s, k=k.value, Q=Q.value, ldq=ldq.value, B=B.value, ldb=ldb.value, resid=resid.value)
+
+
+def qb_stats(ctx):
+    n = ctypes.c_int64()
+    _check(ctx, lib().qb_stats(ctx, None, 0, ctypes.byref(n)))
+    arr = (BlockStats * max(n.value, 1))()
+    _check(ctx, lib().qb_stats(ctx, ctypes.cast(arr, ctypes.c_void_p), n.value, ctypes.byref(n)))
+    return [dict(ell=a.ell, w=a.w, r2=a.r2, ei=a.ei, ms=a.ms, fallback=a.fallback) for a in arr[:n.value]]
+
+
+def qb_omega(ctx, seed, row0, row1, col0, w, out_ptr, ldo):
+    _check(ctx, lib().qb_omega(ctx, seed, row0, row1, col0, w, ctypes.c_void_p(out_ptr), ldo))
+
+
+def qb_orth(ctx, X_ptr, m, w, ldx):
+    _check(ctx, lib().qb_orth(ctx, ctypes.c_void_p(X_ptr), m, w, ldx))
+
+
+# ------------------------------------------------------------------ torch convenience layer
+class _CAI:
+    """Expose a device pointer as a strided array to torch (no copy)."""
+
+    def __init__(self, ptr, shape, strides_bytes, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "strides": tuple(strides_bytes),
+                                         "typestr": typestr, "data": (int(ptr), False), "version": 3}
+
+
+def view_colmajor(ptr, rows, cols, ld, typestr="<f8"):
+    import torch
+    es = 8 if typestr.endswith("8") else 4
+    return torch.as_tensor(_CAI(ptr, (rows, cols), (es, es * ld), typestr), device="cuda")
+
+
+def view_rowmajor(ptr, rows, cols, ld, typestr="<f8"):
+    import torch
+    es = 8 if typestr.endswith("8") else 4
+    return torch.as_tensor(_CAI(ptr, (rows, cols), (es * ld, es), typestr), device="cuda")
+
+
+class QB:
+    """Owns one context.  ``factor(A, eps, b, q, seed)`` with A a CUDA float64 tensor whose
+    columns are contiguous (``A.stride(0) == 1``)."""
+
+    def __init__(self, device=0, dtype=QB_F64, stream=None):
+        self.ctx = qb_create(device, dtype, stream)
+
+    def close(self):
+        qb_destroy(self.ctx)
+        self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def factor(self, A, eps, b, q=0, seed=1, kmax=0, overwrite=False, copy_out=True):
+        import torch
+        assert A.is_cuda and A.dtype == torch.float64 and A.dim() == 2 and A.stride(0) == 1
+        m, n = A.shape
+        r = qb_factor(self.ctx, A.data_ptr(), m, n, A.stride(1) if n > 1 else m, eps, b, q, seed, kmax,
+                      QB_OVERWRITE_A if overwrite else 0)
+        k = r["k"]
+        Q = view_colmajor(r["Q"], m, k, r["ldq"]) if k > 0 else torch.zeros(m, 0, dtype=A.dtype, device=A.device)
+        B = view_rowmajor(r["B"], k, n, r["ldb"]) if k > 0 else torch.zeros(0, n, dtype=A.dtype, device=A.device)
+        if copy_out:
+            Q, B = Q.clone(), B.clone()
+        return dict(status=r["status"], k=k, Q=Q, B=B, resid=r["resid"], stats=qb_stats(self.ctx))
+
+    def launches(self):
+        return qb_kernel_launches(self.ctx)

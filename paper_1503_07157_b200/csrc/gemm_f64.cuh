@@ -1,0 +1,250 @@
+// FP64 GEMM for sm_100a (K2/K3/K4-Gram/K5/K6/K7 of DESIGN.md §5): TMA -> 128B-swizzled
+// shared memory -> DMMA (mma.sync m8n8k4 f64) with register accumulators.
+//
+// tcgen05.mma has no FP64 kind on sm_100a (ptxas rejects .kind::f64), so the FP64
+// contractions of the paper — Y = A Ω, B = Q^* A (:710), A -= Q B (:712),
+// the power steps A^* Q / A Z (:868-870), the CholeskyQR Gram and Q = Y R^-1, and the
+// re-projection Q - Q̄(Q̄^*Q) (:708) — run on the FP64 tensor pipe (SASS DMMA.8x8x4,
+// 37.2 TFLOP/s measured, profiles/MEASURED_FP64.json) fed by TMA through an mbarrier ring.
+//
+// C(M x N) = sum_k opA(i, k) opB(k, j) with two operand layouts:
+//   NN: opA(i,k) = A[i + k*lda] (M-contiguous), opB(k,j) = B[j + k*ldb] (N-contiguous)
+//   TN: opA(i,k) = A[k + i*lda] (K-contiguous), opB(k,j) = B[k + j*ldb] (K-contiguous)
+// CTA tile 128 x BN, k-tile 16; warp tile 64 x 32 = 8 x 4 DMMA 8x8 sub-tiles.
+//
+// Bank-conflict-free fragment loads: every operand stage is a set of TMA boxes whose 128-byte
+// rows are XOR-swizzled (CU_TENSOR_MAP_SWIZZLE_128B).  For K-contiguous boxes (rows = m or
+// n, 16 k per row) the 4 k of one DMMA are consecutive; for MN-contiguous boxes (rows = k,
+// 16 m or n per row) the 4 k of one DMMA are {kq, kq+4, kq+8, kq+12}.  Either way a warp's
+// 32 LDS.64 touch 16 distinct bank pairs twice: 2 wavefronts, the minimum for 256 bytes.
+// The k permutation inside a 16-wide k-tile does not change the sum's terms.
+#pragma once
+#include "common.cuh"
+
+namespace qbk {
+
+enum GemmLayout { GEMM_NN = 0, GEMM_TN = 1 };
+enum GemmEpi { EPI_STORE_COL = 0, EPI_STORE_ROW = 1, EPI_SUB_COL = 2 };
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 16;
+
+struct GemmParams {
+  int M, N, K;
+  int tiles_m, tiles_n;
+  int nkt;             // ceil(K / 16)
+  int kt_per_split;    // k-tiles per split (gridDim.y splits)
+  int raster_m_fast;   // 1: consecutive CTAs walk M first (they share the B panel)
+  double* C;
+  int64_t ldc;
+  int64_t split_stride;  // elements between split partial outputs
+  double* norm_partials; // EPI_SUB_COL: per-CTA sum of squares of the new C
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int WARPS = (GEMM_BM / 64) * (BN / 32);
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int STAGES = BN == 64 ? 4 : 5;
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 8;
+  static constexpr int B_BYTES = BN * GEMM_BK * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * STAGES * 8 + WARPS * 8;
+  static constexpr int MIN_BLOCKS = BN == 64 ? 2 : 1;
+};
+
+template <int LAYOUT, int BN>
+__device__ __forceinline__ void gemm_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, uint8_t* sA,
+                                                 uint8_t* sB, uint64_t* bar, int m0, int n0, int k0) {
+  using Cfg = GemmCfg<BN>;
+  mbar_arrive_expect_tx(bar, Cfg::STAGE_BYTES);
+  if (LAYOUT == GEMM_NN) {
+#pragma unroll
+    for (int c = 0; c < GEMM_BM / 16; ++c) tma_load_2d(sA + c * 2048, tA, bar, m0 + 16 * c, k0);
+#pragma unroll
+    for (int c = 0; c < BN / 16; ++c) tma_load_2d(sB + c * 2048, tB, bar, n0 + 16 * c, k0);
+  } else {
+    tma_load_2d(sA, tA, bar, k0, m0);
+    tma_load_2d(sB, tB, bar, k0, n0);
+  }
+}
+
+template <int LAYOUT, int BN, int EPI>
+__global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
+    gemm_f64_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                    const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  double* red = reinterpret_cast<double*>(empty + STAGES);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+
+  int tm, tn;
+  if (p.raster_m_fast) {
+    tm = blockIdx.x % p.tiles_m;
+    tn = blockIdx.x / p.tiles_m;
+  } else {
+    tn = blockIdx.x % p.tiles_n;
+    tm = blockIdx.x / p.tiles_n;
+  }
+  const int m0 = tm * GEMM_BM, n0 = tn * BN;
+  const int kt0 = blockIdx.y * p.kt_per_split;
+  const int kt1 = min(p.nkt, kt0 + p.kt_per_split);
+  const int nk = max(kt1 - kt0, 0);
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tA);
+    tma_prefetch_desc(&tB);
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::WARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES && s < nk; ++s)
+      gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + s * Cfg::STAGE_BYTES, smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES,
+                                   &full[s], m0, n0, (kt0 + s) * GEMM_BK);
+  }
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Per-lane fragment offsets inside a stage (bytes), see the header comment.
+  uint32_t offA[4][2], offB[4][2];
+  if (LAYOUT == GEMM_NN) {
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      const int k = kq + 4 * (lane & 3);
+      const int rsw = k & 7;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t o = k * 128 + ((((h * 4) + (lane >> 3)) ^ rsw) << 4) + (((lane >> 2) & 1) << 3);
+        offA[kq][h] = o;
+        offB[kq][h] = o;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      const int k = kq * 4 + (lane & 3);
+      const uint32_t o = (lane >> 2) * 128 + ((((k >> 1) ^ (lane >> 2))) << 4) + ((k & 1) << 3);
+      offA[kq][0] = offA[kq][1] = o;
+      offB[kq][0] = offB[kq][1] = o;
+    }
+  }
+
+  for (int i = 0; i < nk; ++i) {
+    const int slot = i % STAGES;
+    const uint32_t par = (i / STAGES) & 1;
+    mbar_wait(&full[slot], par);
+    __syncwarp();
+    const uint8_t* aS = smem + slot * Cfg::STAGE_BYTES;
+    const uint8_t* bS = aS + Cfg::A_BYTES;
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      double a[8], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) {
+        const uint32_t off = LAYOUT == GEMM_NN ? (wm * 4 + (mi >> 1)) * 2048 + offA[kq][mi & 1]
+                                               : (wm * 64 + mi * 8) * 128 + offA[kq][0];
+        a[mi] = *reinterpret_cast<const double*>(aS + off);
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const uint32_t off = LAYOUT == GEMM_NN ? (wn * 2 + (ni >> 1)) * 2048 + offB[kq][ni & 1]
+                                               : (wn * 32 + ni * 8) * 128 + offB[kq][0];
+        b[ni] = *reinterpret_cast<const double*>(bS + off);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (tid == 0 && i + STAGES < nk) {
+      mbar_wait(&empty[slot], par);
+      gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + slot * Cfg::STAGE_BYTES,
+                                   smem + slot * Cfg::STAGE_BYTES + Cfg::A_BYTES, &full[slot], m0, n0,
+                                   (kt0 + i + STAGES) * GEMM_BK);
+    }
+  }
+
+  // ------------------------------------------------------------ epilogue
+  const int mb = m0 + wm * 64 + (lane >> 2);
+  const int nb = n0 + wn * 32 + 2 * (lane & 3);
+  if (EPI == EPI_STORE_COL) {
+    double* C = p.C + static_cast<int64_t>(blockIdx.y) * p.split_stride;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int m = mb + mi * 8;
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = nb + ni * 8 + e;
+          if (n < p.N) C[m + static_cast<int64_t>(n) * p.ldc] = acc[mi][ni][e];
+        }
+    }
+  } else if (EPI == EPI_STORE_ROW) {
+    double* C = p.C + static_cast<int64_t>(blockIdx.y) * p.split_stride;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int m = mb + mi * 8;
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int n = nb + ni * 8;
+        double* dst = C + static_cast<int64_t>(m) * p.ldc + n;
+        if (n + 1 < p.N) {
+          *reinterpret_cast<double2*>(dst) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        } else if (n < p.N) {
+          dst[0] = acc[mi][ni][0];
+        }
+      }
+    }
+  } else {  // EPI_SUB_COL: C -= acc, sum of squares of the result
+    double sq = 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int m = mb + mi * 8;
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = nb + ni * 8 + e;
+          if (n < p.N) {
+            double* c = p.C + m + static_cast<int64_t>(n) * p.ldc;
+            const double v = *c - acc[mi][ni][e];
+            *c = v;
+            sq = fma(v, v, sq);
+          }
+        }
+    }
+    if (p.norm_partials != nullptr) {
+      sq = warp_sum(sq);
+      if (lane == 0) red[warp] = sq;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < Cfg::WARPS; ++w) t += red[w];
+        p.norm_partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+      }
+    }
+  }
+}
+
+}  // namespace qbk

@@ -1,0 +1,655 @@
+// qb.cu — host driver and C ABI (include/qb.h) of the B200-native blocked randomized QB
+// factorization (randQB_b; randQB_pb).
+//
+// One context owns a CUDA stream, the residual workspace, Q̄ / B̄ and all scratch.  The
+// block loop below is the paper's loop; every arithmetic step runs in this library's
+// kernels (omega.cuh, gemm_f64.cuh, small.cuh).  The host only sequences launches and
+// reads two scalars per block (the stop test) plus the CholeskyQR status words.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "../../include/qb.h"
+#include "common.cuh"
+#include "gemm_f64.cuh"
+#include "omega.cuh"
+#include "small.cuh"
+
+namespace {
+
+using namespace qbk;
+
+constexpr int64_t kMaxB = CHOL_MAXW;
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  double* d() const { return static_cast<double*>(p); }
+};
+
+}  // namespace
+
+struct qb_ctx_s {
+  int device = 0;
+  qb_dtype dtype = QB_F64;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 148;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  OmegaConsts omega_consts{};
+
+  // distributed (column sharding); nranks == 1 on a plain context
+  int rank = 0, nranks = 1;
+  int64_t col_offset = 0, n_global = 0;
+
+  DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status;
+  int64_t kcap = 0, ldq = 0, ldb = 0, qbar_rows = 0, bbar_cols = 0;
+  double* h_scal = nullptr;  // pinned: [0] r2, [1] sum B^2, [2..3] spare
+  int* h_status = nullptr;   // pinned
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<qb_block_stats> stats;
+  int block_fallbacks = 0;
+  const double* outQ = nullptr;
+  const double* outB = nullptr;
+};
+
+namespace {
+
+qb_status fail(qb_ctx c, qb_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define QB_CUDA(call)                                                                             \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? QB_ERR_OOM : QB_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+  } while (0)
+
+#define QB_TRY(expr)                 \
+  do {                               \
+    qb_status s_ = (expr);           \
+    if (s_ != QB_OK) return s_;      \
+  } while (0)
+
+qb_status ensure(qb_ctx ctx, DevBuf& b, size_t bytes) {
+  if (b.bytes >= bytes) return QB_OK;
+  if (b.p) QB_CUDA(cudaFree(b.p));
+  b.p = nullptr;
+  b.bytes = 0;
+  QB_CUDA(cudaMalloc(&b.p, std::max<size_t>(bytes, 256)));
+  b.bytes = std::max<size_t>(bytes, 256);
+  return QB_OK;
+}
+
+qb_status check_launch(qb_ctx ctx, const char* what) {
+  ++ctx->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, QB_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  return QB_OK;
+}
+
+// ---------------------------------------------------------------- tensor maps
+qb_status make_map(qb_ctx ctx, CUtensorMap* map, const double* ptr, uint64_t inner, uint64_t outer, int64_t ld,
+                   uint32_t box_inner, uint32_t box_outer) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * 8) & 15) != 0)
+    return fail(ctx, QB_ERR_INVALID_ARG, "TMA operand not 16-byte aligned (ptr %p, ld %lld)", (const void*)ptr,
+                (long long)ld);
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return QB_OK;
+}
+
+// ---------------------------------------------------------------- GEMM launcher
+template <int LAYOUT, int BN, int EPI>
+qb_status launch_gemm_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_f64_kernel<LAYOUT, BN, EPI>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_done = true;
+  }
+  dim3 grid(p.tiles_m * p.tiles_n, splits);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, p);
+  return check_launch(ctx, "gemm_f64");
+}
+
+constexpr int kBN = 64;
+
+int choose_splits(int tiles, int nkt, int slots, int max_splits) {
+  int best = 1;
+  double best_t = 1e300;
+  for (int s = 1; s <= max_splits; ++s) {
+    const int per = (nkt + s - 1) / s;
+    if (s > 1 && per < 4) break;
+    const int units = tiles * s;
+    const int waves = (units + slots - 1) / slots;
+    const double t = waves * (per + 3.0) * (s > 1 ? 1.0 + 0.003 * s : 1.0);
+    if (t < best_t * 0.995) {
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
+}
+
+// C = opA * opB.  epi: EPI_STORE_COL (C[i + j*ldc]), EPI_STORE_ROW (C[i*ldc + j]) or
+// EPI_SUB_COL (C[i + j*ldc] -= ..., per-CTA sum of squares into ctx->parts when
+// want_norm; *nparts receives the number of partials).  For the STORE epilogues the
+// K dimension may be split; then partials land in ctx->P and are reduced in a fixed order
+// (with the sum of squares of C into ctx->parts when want_norm).
+qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const double* A, int64_t lda, const double* B,
+               int64_t ldb, double* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true) {
+  if (nparts) *nparts = 0;
+  if (M <= 0 || N <= 0) return QB_OK;
+  CUtensorMap ta, tb;
+  if (layout == GEMM_NN) {
+    QB_TRY(make_map(ctx, &ta, A, M, K, lda, 16, GEMM_BK));
+    QB_TRY(make_map(ctx, &tb, B, N, K, ldb, 16, GEMM_BK));
+  } else {
+    QB_TRY(make_map(ctx, &ta, A, K, M, lda, 16, GEMM_BM));
+    QB_TRY(make_map(ctx, &tb, B, K, N, ldb, 16, kBN));
+  }
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  p.tiles_n = (N + kBN - 1) / kBN;
+  p.nkt = (K + GEMM_BK - 1) / GEMM_BK;
+  p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int slots = ctx->num_sms * GemmCfg<kBN>::MIN_BLOCKS;
+  int splits = 1;
+  if (epi != EPI_SUB_COL && allow_split) splits = choose_splits(tiles, p.nkt, slots, 64);
+  p.kt_per_split = (p.nkt + splits - 1) / splits;
+  splits = (p.nkt + p.kt_per_split - 1) / p.kt_per_split;
+  if (splits < 1) splits = 1;
+
+  if (epi == EPI_SUB_COL) {
+    p.C = C;
+    p.ldc = ldc;
+    p.split_stride = 0;
+    if (want_norm) {
+      QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)tiles));
+      p.norm_partials = ctx->parts.d();
+      if (nparts) *nparts = tiles;
+    }
+    if (layout == GEMM_NN) return launch_gemm_t<GEMM_NN, kBN, EPI_SUB_COL>(ctx, ta, tb, p, 1);
+    return launch_gemm_t<GEMM_TN, kBN, EPI_SUB_COL>(ctx, ta, tb, p, 1);
+  }
+
+  if (splits == 1) {
+    p.C = C;
+    p.ldc = ldc;
+    if (layout == GEMM_NN) {
+      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, 1)));
+      else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, 1)));
+    } else {
+      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, 1)));
+      else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, 1)));
+    }
+    if (want_norm) {
+      // sum of squares of the stored result (rows x cols in "strided-row" form)
+      const int64_t rows = epi == EPI_STORE_ROW ? M : N, cols = epi == EPI_STORE_ROW ? N : M;
+      const int grid = (int)std::min<int64_t>(rows, 4 * ctx->num_sms);
+      QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
+      sumsq_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(C, cols, rows, ldc, ctx->parts.d());
+      QB_TRY(check_launch(ctx, "sumsq"));
+      if (nparts) *nparts = grid;
+    }
+    return QB_OK;
+  }
+
+  // split-K: partials in the output layout, then a fixed-order reduction
+  const int64_t rows = epi == EPI_STORE_ROW ? M : N, cols = epi == EPI_STORE_ROW ? N : M;
+  const int64_t ldp = round_up(cols, 2);
+  const int64_t stride = rows * ldp;
+  QB_TRY(ensure(ctx, ctx->P, sizeof(double) * (size_t)(stride * splits)));
+  p.C = ctx->P.d();
+  p.ldc = ldp;
+  p.split_stride = stride;
+  if (layout == GEMM_NN) {
+    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, splits)));
+    else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, splits)));
+  } else {
+    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, splits)));
+    else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, splits)));
+  }
+  const int64_t total = rows * cols;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
+  double* sq = nullptr;
+  if (want_norm) {
+    QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
+    sq = ctx->parts.d();
+    if (nparts) *nparts = grid;
+  }
+  splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp, C, ldc, sq);
+  return check_launch(ctx, "splitk_reduce");
+}
+
+qb_status reduce_to_scal(qb_ctx ctx, int64_t nparts, int slot) {
+  reduce_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->parts.d(), nparts, ctx->scal.d(), slot);
+  return check_launch(ctx, "reduce");
+}
+
+// ---------------------------------------------------------------- CholeskyQR2
+qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, int* status_out) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    QB_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CHOL_SMEM));
+    attr_done = true;
+  }
+  const int64_t ld = round_up(kMaxB, 16);
+  chol_inv_kernel<<<1, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(ctx->G.d(), ld, w, m_rows, ctx->L.d(), ld,
+                                                               ctx->Rinv.d(), ld, static_cast<int*>(ctx->status.p),
+                                                               1e-13);
+  QB_TRY(check_launch(ctx, "chol_inv"));
+  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *status_out = ctx->h_status[0];
+  return QB_OK;
+}
+
+// One CholeskyQR pass: dst = src R^-1 with R^T R = src^T src (+ shift on breakdown).
+qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
+                      int* shifted) {
+  const int64_t ldgb = round_up(kMaxB, 16);
+  QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr));
+  int st = 0;
+  QB_TRY(chol_inv(ctx, w, m, &st));
+  if (st == 2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR breakdown even with the shift (w=%d)", w);
+  if (st == 1) *shifted = 1;
+  return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr);
+}
+
+// orth(src) -> dst by CholeskyQR2 (shifted CholeskyQR3 when the first pass breaks down).
+// src and dst may alias; ctx->T1 (rows x kMaxB, ld ldt) is the scratch.
+qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w, int* fallbacks) {
+  const int64_t ldt = round_up(m, 16);
+  double* T = ctx->T1.d();
+  int shifted = 0;
+  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, &shifted));
+  int again = 0;
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, &again));
+  if (shifted || again) {
+    ++*fallbacks;
+    int again2 = 0;
+    QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, &again2));
+    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, &again2));
+    if (again2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR3 did not converge (w=%d)", w);
+  }
+  return QB_OK;
+}
+
+qb_status launch_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_t col0, int64_t w, void* out,
+                       int64_t ldo) {
+  const int64_t npairs = ((row1 - 1) >> 1) - (row0 >> 1) + 1;
+  const int64_t total = npairs * w;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 32 * ctx->num_sms));
+  if (ctx->dtype == QB_F64)
+    omega_kernel<double><<<grid, 256, 0, ctx->stream>>>(seed, row0, row1, col0, w, static_cast<double*>(out), ldo,
+                                                        ctx->omega_consts);
+  else
+    omega_kernel<float><<<grid, 256, 0, ctx->stream>>>(seed, row0, row1, col0, w, static_cast<float*>(out), ldo,
+                                                       ctx->omega_consts);
+  return check_launch(ctx, "omega");
+}
+
+qb_status grow_factors(qb_ctx ctx, int64_t m, int64_t n, int64_t need, int64_t kmax) {
+  if (need <= ctx->kcap && ctx->qbar_rows == m && ctx->bbar_cols == n) return QB_OK;
+  int64_t cap = std::max<int64_t>(need, std::min<int64_t>(kmax, std::max<int64_t>(2 * ctx->kcap, 1024)));
+  cap = std::min<int64_t>(std::max<int64_t>(cap, need), std::max<int64_t>(kmax, need));
+  const int64_t ldq = round_up(m, 16), ldb = round_up(n, 16);
+  DevBuf nq, nb;
+  QB_CUDA(cudaMalloc(&nq.p, sizeof(double) * (size_t)(ldq * cap)));
+  nq.bytes = sizeof(double) * (size_t)(ldq * cap);
+  QB_CUDA(cudaMalloc(&nb.p, sizeof(double) * (size_t)(ldb * cap)));
+  nb.bytes = sizeof(double) * (size_t)(ldb * cap);
+  if (ctx->Qbar.p && ctx->qbar_rows == m && ctx->bbar_cols == n && ctx->kcap > 0) {
+    QB_CUDA(cudaMemcpyAsync(nq.p, ctx->Qbar.p, sizeof(double) * (size_t)(ldq * ctx->kcap), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    QB_CUDA(cudaMemcpyAsync(nb.p, ctx->Bbar.p, sizeof(double) * (size_t)(ldb * ctx->kcap), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  if (ctx->Qbar.p) QB_CUDA(cudaFree(ctx->Qbar.p));
+  if (ctx->Bbar.p) QB_CUDA(cudaFree(ctx->Bbar.p));
+  ctx->Qbar = nq;
+  ctx->Bbar = nb;
+  ctx->kcap = cap;
+  ctx->ldq = ldq;
+  ctx->ldb = ldb;
+  ctx->qbar_rows = m;
+  ctx->bbar_cols = n;
+  return QB_OK;
+}
+
+qb_status init_ctx(qb_ctx ctx, int device, qb_dtype dtype, void* stream) {
+  if (dtype != QB_F64 && dtype != QB_F32) return fail(ctx, QB_ERR_INVALID_ARG, "bad dtype %d", (int)dtype);
+  int ndev = 0;
+  QB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ctx, QB_ERR_INVALID_ARG, "bad device %d of %d", device, ndev);
+  ctx->device = device;
+  ctx->dtype = dtype;
+  QB_CUDA(cudaSetDevice(device));
+  int major = 0, minor = 0;
+  QB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  QB_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  if (major != 10 || minor != 0)
+    return fail(ctx, QB_ERR_UNSUPPORTED, "this build targets sm_100a (B200); device is sm_%d%d", major, minor);
+  QB_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+  if (stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    QB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  QB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(ctx, QB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  for (int k = 1; k <= 11; ++k) ctx->omega_consts.log_c[k] = 2.0 / (2.0 * k + 1.0);  // IEEE RN quotient
+  ctx->omega_consts.log_c12 = 2.0 / 25.0;
+  QB_CUDA(cudaMallocHost(&ctx->h_scal, 8 * sizeof(double)));
+  QB_CUDA(cudaMallocHost(&ctx->h_status, 8 * sizeof(int)));
+  QB_TRY(ensure(ctx, ctx->scal, 8 * sizeof(double)));
+  QB_TRY(ensure(ctx, ctx->status, 8 * sizeof(int)));
+  QB_CUDA(cudaEventCreate(&ctx->ev0));
+  QB_CUDA(cudaEventCreate(&ctx->ev1));
+  return QB_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char* qb_status_string(qb_status s) {
+  switch (s) {
+    case QB_OK: return "QB_OK";
+    case QB_NOT_CONVERGED: return "QB_NOT_CONVERGED";
+    case QB_ERR_INVALID_ARG: return "QB_ERR_INVALID_ARG";
+    case QB_ERR_OOM: return "QB_ERR_OOM";
+    case QB_ERR_CUDA: return "QB_ERR_CUDA";
+    case QB_ERR_NCCL: return "QB_ERR_NCCL";
+    case QB_ERR_ORTH_BREAKDOWN: return "QB_ERR_ORTH_BREAKDOWN";
+    case QB_ERR_UNSUPPORTED: return "QB_ERR_UNSUPPORTED";
+  }
+  return "QB_UNKNOWN";
+}
+
+const char* qb_last_error(qb_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t qb_kernel_launches(qb_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+qb_status qb_create(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream) {
+  if (!out) return QB_ERR_INVALID_ARG;
+  *out = nullptr;
+  qb_ctx ctx = new qb_ctx_s();
+  qb_status s = init_ctx(ctx, device, dtype, cuda_stream);
+  *out = ctx;  // returned even on failure so qb_last_error can explain; caller destroys
+  return s;
+}
+
+qb_status qb_nccl_unique_id(void* out128) {
+  (void)out128;
+  return QB_ERR_NCCL;
+}
+
+qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, int rank, int nranks,
+                         const void* nccl_unique_id, int64_t col_offset, int64_t n_global) {
+  (void)nccl_unique_id;
+  qb_status s = qb_create(out, device, dtype, cuda_stream);
+  if (s != QB_OK) return s;
+  qb_ctx ctx = *out;
+  if (nranks < 1 || rank < 0 || rank >= nranks || col_offset < 0 || n_global < 1)
+    return fail(ctx, QB_ERR_INVALID_ARG, "bad distributed arguments");
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  ctx->col_offset = col_offset;
+  ctx->n_global = n_global;
+  if (nranks > 1) return fail(ctx, QB_ERR_NCCL, "NCCL transport not built in this library version");
+  return QB_OK;
+}
+
+void qb_destroy(qb_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  DevBuf* bufs[] = {&ctx->Awork, &ctx->Qbar, &ctx->Bbar, &ctx->Om, &ctx->Y,     &ctx->T1,    &ctx->Z,   &ctx->Zt,
+                    &ctx->G,     &ctx->L,    &ctx->Rinv, &ctx->W,  &ctx->P,     &ctx->parts, &ctx->scal, &ctx->status};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+qb_status qb_stats(qb_ctx ctx, qb_block_stats* out, int64_t cap, int64_t* nblocks) {
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  const int64_t n = static_cast<int64_t>(ctx->stats.size());
+  if (nblocks) *nblocks = n;
+  if (out && cap > 0) std::memcpy(out, ctx->stats.data(), sizeof(qb_block_stats) * (size_t)std::min(cap, n));
+  return QB_OK;
+}
+
+qb_status qb_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_t col0, int64_t w, void* out,
+                   int64_t ldo) {
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  if (row0 < 0 || row1 < row0 || col0 < 0 || w < 0 || (w > 0 && ldo < w) || (!out && row1 > row0 && w > 0))
+    return fail(ctx, QB_ERR_INVALID_ARG, "qb_omega: bad arguments");
+  if (row1 == row0 || w == 0) return QB_OK;
+  QB_CUDA(cudaSetDevice(ctx->device));
+  return launch_omega(ctx, seed, row0, row1, col0, w, out, ldo);
+}
+
+qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  if (ctx->dtype != QB_F64) return fail(ctx, QB_ERR_UNSUPPORTED, "qb_orth: FP32 not built yet");
+  if (!X || m < 1 || w < 1 || w > kMaxB || w > m || ldx < m || m > INT32_MAX)
+    return fail(ctx, QB_ERR_INVALID_ARG, "qb_orth: bad arguments (m=%lld w=%lld ldx=%lld)", (long long)m,
+                (long long)w, (long long)ldx);
+  QB_CUDA(cudaSetDevice(ctx->device));
+  const int64_t ldgb = round_up(kMaxB, 16);
+  QB_TRY(ensure(ctx, ctx->G, sizeof(double) * ldgb * ldgb));
+  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * ldgb * ldgb));
+  QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * ldgb * ldgb));
+  QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(m, 16) * kMaxB)));
+  int fb = 0;
+  const bool aligned = (ldx % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  if (aligned) {
+    QB_TRY(cholqr2(ctx, static_cast<double*>(X), ldx, static_cast<double*>(X), ldx, m, (int)w, &fb));
+  } else {  // TMA needs 16-byte aligned columns: stage through an aligned copy
+    const int64_t ldy = round_up(m, 16);
+    QB_TRY(ensure(ctx, ctx->Y, sizeof(double) * (size_t)(ldy * w)));
+    QB_CUDA(cudaMemcpy2DAsync(ctx->Y.p, ldy * 8, X, ldx * 8, m * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
+    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldy, ctx->Y.d(), ldy, m, (int)w, &fb));
+    QB_CUDA(cudaMemcpy2DAsync(X, ldx * 8, ctx->Y.p, ldy * 8, m * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QB_OK;
+}
+
+qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U, int64_t* ldu, const void** S, const void** V,
+                  int64_t* ldv) {
+  (void)kkeep; (void)U; (void)ldu; (void)S; (void)V; (void)ldv;
+  return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd is the NEXT-1 row; not built yet");
+}
+
+qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, double eps, int64_t b, int q,
+                    uint64_t seed, int64_t kmax, unsigned flags, int64_t* k_out, const void** Q_out,
+                    int64_t* ldq_out, const void** B_out, int64_t* ldb_out, double* resid_out) {
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  ctx->stats.clear();
+  if (!k_out) return fail(ctx, QB_ERR_INVALID_ARG, "k must not be NULL");
+  *k_out = 0;
+  if (ctx->dtype != QB_F64) return fail(ctx, QB_ERR_UNSUPPORTED, "the FP32 path is not built yet");
+  if (!Ain || m < 1 || n < 1 || lda < m || m > INT32_MAX || n > INT32_MAX)
+    return fail(ctx, QB_ERR_INVALID_ARG, "bad matrix arguments (m=%lld n=%lld lda=%lld)", (long long)m, (long long)n,
+                (long long)lda);
+  if (b < 1 || b > kMaxB) return fail(ctx, QB_ERR_INVALID_ARG, "block size b=%lld outside [1, %lld]", (long long)b, (long long)kMaxB);
+  if (q < 0) return fail(ctx, QB_ERR_INVALID_ARG, "q=%d < 0", q);
+  if (!(eps >= 0.0)) return fail(ctx, QB_ERR_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
+  const int64_t n_glob = ctx->nranks > 1 ? ctx->n_global : n;
+  const int64_t kmax_eff = (kmax <= 0) ? std::min(m, n_glob) : std::min(kmax, std::min(m, n_glob));
+  QB_CUDA(cudaSetDevice(ctx->device));
+
+  // ---- residual workspace A^(0) = A (A^(j) overwrites A^(j-1), :112)
+  double* A = static_cast<double*>(Ain);
+  int64_t ldA = lda;
+  const bool inplace_ok = (flags & QB_OVERWRITE_A) && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(Ain) & 15) == 0);
+  if (!inplace_ok) {
+    ldA = round_up(m, 16);
+    QB_TRY(ensure(ctx, ctx->Awork, sizeof(double) * (size_t)(ldA * n)));
+    QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * 8, Ain, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    A = ctx->Awork.d();
+  }
+
+  // ---- scratch
+  const int64_t ldm = round_up(m, 16), ldn = round_up(n, 16), bp = round_up(kMaxB, 16);
+  QB_TRY(ensure(ctx, ctx->Om, sizeof(double) * (size_t)(n * bp)));
+  QB_TRY(ensure(ctx, ctx->Y, sizeof(double) * (size_t)(ldm * b)));
+  QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(std::max(m, n), 16) * kMaxB)));
+  QB_TRY(ensure(ctx, ctx->G, sizeof(double) * bp * bp));
+  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * bp * bp));
+  QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * bp * bp));
+  if (q > 0) {
+    QB_TRY(ensure(ctx, ctx->Z, sizeof(double) * (size_t)(ldn * b)));
+    QB_TRY(ensure(ctx, ctx->Zt, sizeof(double) * (size_t)(n * bp)));
+  }
+
+  // ---- a0: r0^2 = ||A||_F^2; trivial exit (Algorithm 1 line (2), reading R3)
+  {
+    const int grid = (int)std::min<int64_t>(n, 8 * ctx->num_sms);
+    QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
+    sumsq_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(A, m, n, ldA, ctx->parts.d());
+    QB_TRY(check_launch(ctx, "sumsq"));
+    QB_TRY(reduce_to_scal(ctx, grid, 0));
+    QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  const double r2_0 = ctx->h_scal[0];
+  if (!std::isfinite(r2_0)) return fail(ctx, QB_ERR_INVALID_ARG, "A contains NaN or Inf");
+  const double eps2 = eps * eps;
+  double r2 = r2_0, ei = r2_0;
+  ctx->outQ = nullptr;
+  ctx->outB = nullptr;
+  if (resid_out) *resid_out = std::sqrt(r2_0);
+  if (r2_0 <= eps2) {
+    QB_TRY(grow_factors(ctx, m, n, 1, std::max<int64_t>(kmax_eff, 1)));
+    if (Q_out) *Q_out = ctx->Qbar.p;
+    if (ldq_out) *ldq_out = ctx->ldq;
+    if (B_out) *B_out = ctx->Bbar.p;
+    if (ldb_out) *ldb_out = ctx->ldb;
+    return QB_OK;
+  }
+
+  int64_t ell = 0;
+  while (ell < kmax_eff) {
+    const int64_t w = std::min<int64_t>(b, kmax_eff - ell);
+    QB_TRY(grow_factors(ctx, m, n, ell + w, kmax_eff));
+    QB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    ctx->block_fallbacks = 0;
+    double* Qbar = ctx->Qbar.d();
+    double* Qi = Qbar + ell * ctx->ldq;
+    double* Bi = ctx->Bbar.d() + ell * ctx->ldb;
+
+    // line (2): Ω_i = randn(n, w), global columns ell .. ell+w-1, row-major (ld bp)
+    QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp));
+    // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
+    QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Om.d(), bp, ctx->Y.d(), ldm, false,
+                nullptr));
+    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, &ctx->block_fallbacks));
+    // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
+    for (int j = 0; j < q; ++j) {
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, Qi, ctx->ldq, ctx->Z.d(), ldn, false,
+                  nullptr));
+      QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, &ctx->block_fallbacks));
+      {
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w + 31) / 32));
+        transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w, ctx->Zt.d(), bp);
+        QB_TRY(check_launch(ctx, "transpose"));
+      }
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Zt.d(), bp, ctx->Y.d(), ldm,
+                  false, nullptr));
+      QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, &ctx->block_fallbacks));
+    }
+    // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
+    if (ell > 0 && !(flags & QB_NO_REPROJ)) {
+      QB_TRY(ensure(ctx, ctx->W, sizeof(double) * (size_t)(ell * bp)));
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)ell, (int)w, (int)m, Qbar, ctx->ldq, Qi, ctx->ldq, ctx->W.d(), bp,
+                  false, nullptr));
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)ell, Qbar, ctx->ldq, ctx->W.d(), bp, Qi, ctx->ldq,
+                  false, nullptr));
+      QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, &ctx->block_fallbacks));
+    }
+    // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
+    int64_t nb_parts = 0;
+    QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)w, (int)n, (int)m, Qi, ctx->ldq, A, ldA, Bi, ctx->ldb, true,
+                &nb_parts));
+    QB_TRY(reduce_to_scal(ctx, nb_parts, 1));
+    // line (10): A^(i) = A^(i-1) - Q_i B_i, with sum A^(i)^2 in the epilogue (the stop test, R1)
+    int64_t na_parts = 0;
+    QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)n, (int)w, Qi, ctx->ldq, Bi, ctx->ldb, A, ldA, true,
+                &na_parts));
+    QB_TRY(reduce_to_scal(ctx, na_parts, 0));
+    QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    r2 = ctx->h_scal[0];
+    ei -= ctx->h_scal[1];
+    ell += w;
+    qb_block_stats st{};
+    st.ell = ell;
+    st.w = w;
+    st.r2 = r2;
+    st.ei = ei;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    st.ms = ms;
+    st.fallback = ctx->block_fallbacks;
+    ctx->stats.push_back(st);
+    if (!std::isfinite(r2)) return fail(ctx, QB_ERR_CUDA, "non-finite residual after block ending at %lld", (long long)ell);
+    if (r2 <= eps2) break;  // line (11): stop test (R1, R4)
+  }
+  *k_out = ell;
+  if (Q_out) *Q_out = ctx->Qbar.p;
+  if (ldq_out) *ldq_out = ctx->ldq;
+  if (B_out) *B_out = ctx->Bbar.p;
+  if (ldb_out) *ldb_out = ctx->ldb;
+  if (resid_out) *resid_out = std::sqrt(r2);
+  return r2 <= eps2 ? QB_OK : QB_NOT_CONVERGED;
+}
+
+}  // extern "C"

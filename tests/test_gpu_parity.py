@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Tolerances are the north_star's (BASELINE.json), FP64: identical k outside the tie zone
+(reading R19), ||Q^*Q - I||_max <= 1e-12, ||Q_g B_g - Q_o B_o||_F / ||A||_F <= 1e-10 (one
+GEMM [Q_g Q_o][B_g; -B_o], reading in DESIGN.md §6), ||A - Q_g B_g||_F <= eps (1 + 1e-8).
+Ω is compared bit for bit."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import omega as oomega
+from oracle import qb as oqb
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def qbmod():
+    import paper_1503_07157_b200 as qbp
+    from paper_1503_07157_b200 import build
+    build.build()
+    return qbp
+
+
+@pytest.fixture(scope="module")
+def ctx(qbmod):
+    c = qbmod.QB(0)
+    yield c
+    c.close()
+
+
+def to_dev(A):
+    return torch.from_numpy(np.asfortranarray(A)).cuda()  # Fortran order -> stride(0) == 1
+
+
+def in_tie_zone(res_o, eps, rel=1e-8):
+    return any(abs(np.sqrt(h[2]) - eps) <= rel * eps for h in res_o.hist)
+
+
+def check_parity(A, g, o, eps, tol_orth=1e-12, tol_qb=1e-10):
+    nA = np.linalg.norm(A)
+    Qg = g["Q"].cpu().numpy()
+    Bg = g["B"].cpu().numpy()
+    if not in_tie_zone(o, eps):
+        assert g["k"] == o.k, (g["k"], o.k)
+        assert g["status"] == o.status
+    k = g["k"]
+    if k > 0:
+        assert np.abs(Qg.T @ Qg - np.eye(k)).max() <= tol_orth
+    if g["k"] == o.k and k > 0:
+        diff = np.hstack([Qg, o.Q]) @ np.vstack([Bg, -o.B])
+        assert np.linalg.norm(diff) / nA <= tol_qb
+    true = np.linalg.norm(A - Qg @ Bg)
+    if g["status"] == 0:
+        assert true <= eps * (1 + 1e-8)
+    # direct residual reported by the library = true residual of the returned factors
+    assert abs(g["resid"] - true) <= 1e-12 * nA + 1e-8 * true
+    return true
+
+
+# ------------------------------------------------------------------------- Ω generator
+@pytest.mark.parametrize("seed,n,row0,row1,col0,w", [
+    (1, 300, 0, 300, 0, 10), (1, 1001, 0, 1001, 37, 64), (7, 1001, 1, 1000, 3, 5),
+    (123456789012345, 50_001, 17, 49_999, 1000, 3), (2**64 - 1, 64, 0, 64, 2**33, 2)])
+def test_omega_bitwise(qbmod, ctx, seed, n, row0, row1, col0, w):
+    ldo = w + 3
+    out = torch.full((row1 - row0, ldo), float("nan"), dtype=torch.float64, device="cuda")
+    qbmod.qb_omega(ctx.ctx, seed, row0, row1, col0, w, out.data_ptr(), ldo)
+    torch.cuda.synchronize()
+    got = out[:, :w].cpu().numpy()
+    ref = oomega.omega_panel(seed, n, col0, w, row0, row1)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    assert np.isnan(out[:, w:].cpu().numpy()).all()  # ldo padding untouched
+
+
+# ------------------------------------------------------------------------- orth
+@pytest.mark.parametrize("m,w", [(1000, 1), (1000, 7), (333, 64), (5000, 256), (2048, 128)])
+def test_orth_parity(qbmod, ctx, m, w):
+    X = np.random.default_rng(m + w).standard_normal((m, w))
+    Xd = to_dev(X)
+    qbmod.qb_orth(ctx.ctx, Xd.data_ptr(), m, w, m)
+    Q = Xd.cpu().numpy()
+    Qo = oqb.orth(X)
+    assert np.abs(Q.T @ Q - np.eye(w)).max() <= 1e-13
+    assert np.abs(Q - Qo).max() <= 1e-11
+
+
+def test_orth_rank_deficient_fallback(qbmod, ctx):
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((500, 12)) @ rng.standard_normal((12, 20))   # rank 12 < w = 20
+    Xd = to_dev(X)
+    qbmod.qb_orth(ctx.ctx, Xd.data_ptr(), 500, 20, 500)
+    Q = Xd.cpu().numpy()
+    assert np.abs(Q.T @ Q - np.eye(20)).max() <= 1e-12
+    assert np.linalg.norm(X - Q @ (Q.T @ X)) <= 1e-12 * np.linalg.norm(X)
+
+
+# ------------------------------------------------------------------------- full loop
+CASES = [
+    # name, m, n, spectrum, eps, b, q
+    ("C1", 400, 300, "exp10_20", 1e-6, 10, 0),
+    ("C1q1", 400, 300, "exp10_20", 1e-6, 10, 1),
+    ("ragged", 333, 517, "exp10_25", 1e-7, 17, 0),
+    ("tall_q2", 1000, 260, "poly2", 1e-5, 64, 2),
+    ("wide", 260, 1000, "exp_100", 1e-4, 32, 1),
+    ("b1", 120, 90, "exp10_20", 1e-3, 1, 0),
+    ("bigb", 700, 650, "exp10_25", 1e-6, 256, 0),
+]
+
+
+def make(m, n, kind, seed):
+    r = min(m, n)
+    if kind == "exp10_25":
+        sig = 10.0 ** (-np.arange(1, r + 1) / 25.0)
+    else:
+        sig = synth.sigma(kind, r)
+    return synth.make_matrix_np(m, n, sig, seed), sig
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_factor_parity(qbmod, ctx, case):
+    name, m, n, kind, eps, b, q = case
+    A, sig = make(m, n, kind, 1000 + m)
+    o = oqb.randqb_pb(A, eps, b, q, seed=1)
+    g = ctx.factor(to_dev(A), eps, b, q, seed=1)
+    check_parity(A, g, o, eps)
+    # per-block residual history and the error indicator
+    assert len(g["stats"]) == len(o.hist)
+    nA2 = np.linalg.norm(A) ** 2
+    for sg, ho in zip(g["stats"], o.hist):
+        assert sg["ell"] == ho[0] and sg["w"] == ho[1]
+        assert abs(sg["r2"] - ho[2]) <= 1e-12 * nA2
+        assert abs(sg["ei"] - sg["r2"]) <= 6 * 2.0 ** -53 * nA2 * 4
+
+
+def test_config_C2_parity(qbmod, ctx):
+    cfg = synth.CONFIGS["C2"]
+    sig = synth.config_sigma(cfg)
+    Ad = synth.make_matrix_torch(cfg.m, cfg.n, sig, cfg.seed_matrix)
+    A = Ad.cpu().numpy()
+    o = oqb.randqb_pb(A, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega)
+    g = ctx.factor(Ad, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega)
+    check_parity(A, g, o, cfg.eps)
+    assert g["k"] >= synth.eps_rank(sig, cfg.eps)
+
+
+def test_degenerate_inputs(qbmod, ctx):
+    A = np.zeros((50, 40))
+    g = ctx.factor(to_dev(A), 1e-8, 8)
+    assert (g["status"], g["k"]) == (0, 0)
+    A = np.random.default_rng(0).standard_normal((50, 40))
+    g = ctx.factor(to_dev(A), 10 * np.linalg.norm(A), 8)       # reading R3
+    assert (g["status"], g["k"]) == (0, 0)
+    g = ctx.factor(to_dev(A), 0.0, 8, kmax=20)                 # reading R5
+    assert (g["status"], g["k"]) == (qbmod.QB_NOT_CONVERGED, 20)
+    assert [s["w"] for s in g["stats"]] == [8, 8, 4]
+    o = oqb.randqb_pb(A, 0.0, 8, kmax=20)
+    check_parity(A, g, o, 0.0)
+    g = ctx.factor(to_dev(A), 1e-9, 8)                         # exhausts at min(m, n)
+    assert g["k"] == 40 and g["resid"] < 1e-9
+
+
+def test_rank_exhaustion_inside_block(qbmod, ctx):
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((120, 25)) @ rng.standard_normal((25, 90))
+    eps = 1e-9 * np.linalg.norm(A)
+    g = ctx.factor(to_dev(A), eps, 10, q=0, seed=3)
+    o = oqb.randqb_pb(A, eps, 10, q=0, seed=3)
+    assert g["k"] == o.k == 30
+    Qg = g["Q"].cpu().numpy()
+    assert np.abs(Qg.T @ Qg - np.eye(30)).max() <= 1e-12
+    assert np.linalg.norm(A - Qg @ g["B"].cpu().numpy()) <= 1e-12 * np.linalg.norm(A)
+    assert sum(s["fallback"] for s in g["stats"]) >= 1
+
+
+def test_invalid_arguments(qbmod, ctx):
+    A = to_dev(np.ones((10, 10)))
+    with pytest.raises(qbmod.QBError):
+        ctx.factor(A, 1e-3, 0)
+    with pytest.raises(qbmod.QBError):
+        ctx.factor(A, -1.0, 4)
+    An = np.ones((10, 10))
+    An[3, 4] = np.nan
+    with pytest.raises(qbmod.QBError) as e:
+        ctx.factor(to_dev(An), 1e-3, 4)
+    assert e.value.status == qbmod.QB_ERR_INVALID_ARG
+
+
+def test_overwrite_a_leaves_residual(qbmod, ctx):
+    A, _ = make(300, 200, "exp10_25", 5)
+    Ad = to_dev(A)
+    g = ctx.factor(Ad, 1e-6, 16, overwrite=True)
+    R = Ad.cpu().numpy()
+    Qg, Bg = g["Q"].cpu().numpy(), g["B"].cpu().numpy()
+    assert np.linalg.norm(R - (A - Qg @ Bg)) <= 1e-12 * np.linalg.norm(A)
+    g2 = ctx.factor(to_dev(A), 1e-6, 16)
+    assert g2["k"] == g["k"]
+    assert np.array_equal(g2["Q"].cpu().numpy(), Qg)   # bitwise reproducible
+
+
+def test_no_reproj_loses_orthogonality(qbmod, ctx):
+    """without line (3') the blocks drift into the earlier span."""
+    A, _ = make(1000, 800, "exp10_25", 3)
+    g = ctx.factor(to_dev(A), 1e-13, 20, q=0, seed=1)
+    r = qbmod.qb_factor(ctx.ctx, to_dev(A).data_ptr(), 1000, 800, 1000, 1e-13, 20, 0, 1, 0, qbmod.QB_NO_REPROJ)
+    Q = g["Q"].cpu().numpy()
+    Qn = qbmod.view_colmajor(r["Q"], 1000, r["k"], r["ldq"]).cpu().numpy()
+    o_with = np.abs(Q.T @ Q - np.eye(Q.shape[1])).max()
+    o_without = np.abs(Qn.T @ Qn - np.eye(Qn.shape[1])).max()
+    assert o_with <= 1e-12 and o_without > 1e3 * o_with
+
+
+def test_target_config_properties(qbmod, ctx):
+    """The bench workload (T: 20000^2, b = 256, q = 0) at full size, in the launch configuration
+    bench.py times: properties that hold at any size + sampled Ω entries vs the oracle."""
+    cfg = synth.CONFIGS["T"]
+    sig = synth.config_sigma(cfg)
+    Ad = synth.make_matrix_torch(cfg.m, cfg.n, sig, cfg.seed_matrix)
+    nA = float(torch.linalg.norm(Ad))
+    g = ctx.factor(Ad, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=False)
+    Q, B, k = g["Q"], g["B"], g["k"]
+    assert g["status"] == 0 and k % cfg.b == 0
+    kq = synth.eps_rank(sig, cfg.eps)
+    assert k >= kq
+    orth = (Q.T @ Q - torch.eye(k, dtype=torch.float64, device="cuda")).abs().max().item()
+    assert orth <= 1e-12
+    true = torch.linalg.norm(torch.addmm(Ad, Q, B, alpha=-1.0)).item()
+    assert true <= cfg.eps * (1 + 1e-8)
+    assert true >= synth.optimal_error(sig, k) * (1 - 1e-6)
+    st = g["stats"]
+    assert st[-1]["r2"] <= cfg.eps ** 2 < st[-2]["r2"]
+    for s in st:
+        assert abs(s["ei"] - s["r2"]) <= 6 * 2.0 ** -53 * nA ** 2 * 4
+    # sampled Ω(rows, cols) at the full size against the oracle generator
+    rng = np.random.default_rng(0)
+    for c0 in (0, k - cfg.b):
+        rows = rng.integers(0, cfg.n, 64)
+        out = torch.empty((cfg.n, cfg.b), dtype=torch.float64, device="cuda")
+        qbmod.qb_omega(ctx.ctx, cfg.seed_omega, 0, cfg.n, c0, cfg.b, out.data_ptr(), cfg.b)
+        got = out.cpu().numpy()[rows]
+        ref = np.vstack([oomega.omega_panel(cfg.seed_omega, cfg.n, c0, cfg.b, r, r + 1) for r in rows])
+        assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
