@@ -67,7 +67,10 @@ typedef struct {
   int64_t w;          /* width of this block (b, or less for the last block when capped)   */
   double r2;          /* ||A^(i)||_F^2                                                      */
   double ei;          /* ||A||_F^2 - sum_{j<=i} ||B_j||_F^2                                 */
-  double ms;          /* device time of the block (CUDA events), milliseconds               */
+  double ms;          /* device time of the whole block (CUDA events), milliseconds         */
+  double ms_sketch;   /* Omega_i + Y_i = A Omega_i (line (3) product)                       */
+  double ms_bmat;     /* B_i = Q_i^* A (line (9)) incl. its split-K reduction               */
+  double ms_down;     /* A -= Q_i B_i with the fused ||A^(i)||_F^2 epilogue (line (10))     */
   int32_t fallback;   /* number of shifted-CholeskyQR fallbacks taken in this block         */
   int32_t reserved;
 } qb_block_stats;
@@ -96,7 +99,7 @@ qb_status qb_nccl_unique_id(void* out128);
  *          for a distributed context).  Read-only unless QB_OVERWRITE_A.
  *   eps    absolute Frobenius tolerance (R2), eps >= 0.  The loop stops after the first
  *          block with ||A^(i)||_F^2 <= eps^2 (R4); ||A||_F <= eps returns k = 0 (R3).
- *   b      block size >= 1 (b <= 512 in this build); q >= 0 power steps; seed selects Omega.
+ *   b      block size, 1 <= b <= 256 in this build; q >= 0 power steps; seed selects Omega.
  *   kmax   rank cap; <= 0 means min(m, n_global).  The last block is narrowed to hit it (R5).
  * Outputs (all optional except k):
  *   *k     rank found.   *resid = ||A^(k)||_F (direct, R1).
@@ -109,6 +112,16 @@ qb_status qb_factor(qb_ctx ctx, void* A, int64_t m, int64_t n, int64_t lda, doub
                     int64_t b, int q, uint64_t seed, int64_t kmax, unsigned flags,
                     int64_t* k, const void** Q, int64_t* ldq, const void** B, int64_t* ldb,
                     double* resid);
+
+/* qb_factor with HOST buffers (end-to-end entry point): A_host (column-major, lda_host) is
+ * copied to the device on the context stream (pinned memory makes this a DMA at full PCIe /
+ * C2C rate), factored with the device path, and Q (column-major m x k, ldq_host) and B
+ * (row-major k x n, ldb_host) are copied back into caller buffers with room for kcap_host
+ * columns / rows (only min(k, kcap_host) are written; *k is the true rank).               */
+qb_status qb_factor_host(qb_ctx ctx, const void* A_host, int64_t m, int64_t n, int64_t lda_host,
+                         double eps, int64_t b, int q, uint64_t seed, int64_t kmax, int64_t* k,
+                         void* Q_host, int64_t ldq_host, void* B_host, int64_t ldb_host,
+                         int64_t kcap_host, double* resid);
 
 /* Per-block records of the last qb_factor: copies min(cap, nblocks) records to `out`
  * (may be NULL when cap = 0) and the total count to *nblocks.                              */
@@ -123,7 +136,7 @@ qb_status qb_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_
 
 /* orth(X) by CholeskyQR2 with the shifted-CholeskyQR3 fallback (R8): X is
  * device, column-major m x w (ldx), overwritten by Q with orthonormal columns spanning
- * ran(X); diag(R) > 0.  w <= 512.  Returns QB_ERR_ORTH_BREAKDOWN if even the shifted
+ * ran(X); diag(R) > 0.  w <= 256.  Returns QB_ERR_ORTH_BREAKDOWN if even the shifted
  * variant fails.  Blocking.                                                               */
 qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx);
 

@@ -39,7 +39,8 @@ class QBError(RuntimeError):
 
 class BlockStats(ctypes.Structure):
     _fields_ = [("ell", ctypes.c_int64), ("w", ctypes.c_int64), ("r2", ctypes.c_double),
-                ("ei", ctypes.c_double), ("ms", ctypes.c_double), ("fallback", ctypes.c_int32),
+                ("ei", ctypes.c_double), ("ms", ctypes.c_double), ("ms_sketch", ctypes.c_double),
+                ("ms_bmat", ctypes.c_double), ("ms_down", ctypes.c_double), ("fallback", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
 
 
@@ -63,6 +64,8 @@ def lib():
         L.qb_nccl_unique_id.argtypes = [vp]
         L.qb_factor.argtypes = [c_ctx, vp, i64, i64, i64, dbl, i64, ctypes.c_int, u64, i64, ctypes.c_uint,
                                 P(i64), P(vp), P(i64), P(vp), P(i64), P(dbl)]
+        L.qb_factor_host.argtypes = [c_ctx, vp, i64, i64, i64, dbl, i64, ctypes.c_int, u64, i64, P(i64), vp, i64,
+                                     vp, i64, i64, P(dbl)]
         L.qb_stats.argtypes = [c_ctx, vp, i64, P(i64)]
         L.qb_omega.argtypes = [c_ctx, u64, i64, i64, i64, i64, vp, i64]
         L.qb_orth.argtypes = [c_ctx, vp, i64, i64, i64]
@@ -75,7 +78,7 @@ def lib():
         L.qb_status_string.restype = ctypes.c_char_p
         L.qb_last_error.argtypes = [c_ctx]
         L.qb_last_error.restype = ctypes.c_char_p
-        for f in ("qb_create", "qb_create_dist", "qb_nccl_unique_id", "qb_factor", "qb_stats", "qb_omega",
+        for f in ("qb_create", "qb_create_dist", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_stats", "qb_omega",
                   "qb_orth", "rqb_svd"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -138,12 +141,24 @@ def qb_factor(ctx, A_ptr, m, n, lda, eps, b, q=0, seed=1, kmax=0, flags=0):
     return dict(status=s, k=k.value, Q=Q.value, ldq=ldq.value, B=B.value, ldb=ldb.value, resid=resid.value)
 
 
+def qb_factor_host(ctx, A_host_ptr, m, n, lda, eps, b, q, seed, kmax, Q_host_ptr, ldq, B_host_ptr, ldb, kcap):
+    """End-to-end call with host buffers (see include/qb.h).  Returns dict(status, k, resid)."""
+    k = ctypes.c_int64()
+    resid = ctypes.c_double()
+    s = lib().qb_factor_host(ctx, ctypes.c_void_p(A_host_ptr), m, n, lda, float(eps), b, q, seed, kmax,
+                             ctypes.byref(k), ctypes.c_void_p(Q_host_ptr), ldq, ctypes.c_void_p(B_host_ptr), ldb,
+                             kcap, ctypes.byref(resid))
+    _check(ctx, s, ok=(QB_OK, QB_NOT_CONVERGED))
+    return dict(status=s, k=k.value, resid=resid.value)
+
+
 def qb_stats(ctx):
     n = ctypes.c_int64()
     _check(ctx, lib().qb_stats(ctx, None, 0, ctypes.byref(n)))
     arr = (BlockStats * max(n.value, 1))()
     _check(ctx, lib().qb_stats(ctx, ctypes.cast(arr, ctypes.c_void_p), n.value, ctypes.byref(n)))
-    return [dict(ell=a.ell, w=a.w, r2=a.r2, ei=a.ei, ms=a.ms, fallback=a.fallback) for a in arr[:n.value]]
+    return [dict(ell=a.ell, w=a.w, r2=a.r2, ei=a.ei, ms=a.ms, ms_sketch=a.ms_sketch, ms_bmat=a.ms_bmat,
+                 ms_down=a.ms_down, fallback=a.fallback) for a in arr[:n.value]]
 
 
 def qb_omega(ctx, seed, row0, row1, col0, w, out_ptr, ldo):

@@ -59,6 +59,7 @@ struct qb_ctx_s {
   double* h_scal = nullptr;  // pinned: [0] r2, [1] sum B^2, [2..3] spare
   int* h_status = nullptr;   // pinned
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evp[6] = {};  // phase events: sketch, B, downdate (begin/end)
   std::vector<qb_block_stats> stats;
   int block_fallbacks = 0;
   const double* outQ = nullptr;
@@ -384,6 +385,7 @@ qb_status init_ctx(qb_ctx ctx, int device, qb_dtype dtype, void* stream) {
   QB_TRY(ensure(ctx, ctx->status, 8 * sizeof(int)));
   QB_CUDA(cudaEventCreate(&ctx->ev0));
   QB_CUDA(cudaEventCreate(&ctx->ev1));
+  for (auto& e : ctx->evp) QB_CUDA(cudaEventCreate(&e));
   return QB_OK;
 }
 
@@ -452,6 +454,8 @@ void qb_destroy(qb_ctx ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (auto& e : ctx->evp)
+    if (e) cudaEventDestroy(e);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -586,10 +590,12 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     double* Bi = ctx->Bbar.d() + ell * ctx->ldb;
 
     // line (2): Ω_i = randn(n, w), global columns ell .. ell+w-1, row-major (ld bp)
+    QB_CUDA(cudaEventRecord(ctx->evp[0], ctx->stream));
     QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp));
     // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
     QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Om.d(), bp, ctx->Y.d(), ldm, false,
                 nullptr));
+    QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
     QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, &ctx->block_fallbacks));
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     for (int j = 0; j < q; ++j) {
@@ -616,13 +622,17 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     }
     // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
     int64_t nb_parts = 0;
+    QB_CUDA(cudaEventRecord(ctx->evp[2], ctx->stream));
     QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)w, (int)n, (int)m, Qi, ctx->ldq, A, ldA, Bi, ctx->ldb, true,
                 &nb_parts));
+    QB_CUDA(cudaEventRecord(ctx->evp[3], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, nb_parts, 1));
     // line (10): A^(i) = A^(i-1) - Q_i B_i, with sum A^(i)^2 in the epilogue (the stop test, R1)
     int64_t na_parts = 0;
+    QB_CUDA(cudaEventRecord(ctx->evp[4], ctx->stream));
     QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)n, (int)w, Qi, ctx->ldq, Bi, ctx->ldb, A, ldA, true,
                 &na_parts));
+    QB_CUDA(cudaEventRecord(ctx->evp[5], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
@@ -638,6 +648,12 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     st.ms = ms;
+    cudaEventElapsedTime(&ms, ctx->evp[0], ctx->evp[1]);
+    st.ms_sketch = ms;
+    cudaEventElapsedTime(&ms, ctx->evp[2], ctx->evp[3]);
+    st.ms_bmat = ms;
+    cudaEventElapsedTime(&ms, ctx->evp[4], ctx->evp[5]);
+    st.ms_down = ms;
     st.fallback = ctx->block_fallbacks;
     ctx->stats.push_back(st);
     if (!std::isfinite(r2)) return fail(ctx, QB_ERR_CUDA, "non-finite residual after block ending at %lld", (long long)ell);
@@ -650,6 +666,32 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   if (ldb_out) *ldb_out = ctx->ldb;
   if (resid_out) *resid_out = std::sqrt(r2);
   return r2 <= eps2 ? QB_OK : QB_NOT_CONVERGED;
+}
+
+qb_status qb_factor_host(qb_ctx ctx, const void* A_host, int64_t m, int64_t n, int64_t lda_host, double eps,
+                         int64_t b, int q, uint64_t seed, int64_t kmax, int64_t* k, void* Q_host, int64_t ldq_host,
+                         void* B_host, int64_t ldb_host, int64_t kcap_host, double* resid) {
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  if (!A_host || !k || m < 1 || n < 1 || lda_host < m || kcap_host < 0 || (kcap_host > 0 && (!Q_host || !B_host)) ||
+      (Q_host && ldq_host < m) || (B_host && ldb_host < n))
+    return fail(ctx, QB_ERR_INVALID_ARG, "qb_factor_host: bad arguments");
+  QB_CUDA(cudaSetDevice(ctx->device));
+  const int64_t ldA = round_up(m, 16);
+  QB_TRY(ensure(ctx, ctx->Awork, sizeof(double) * (size_t)(ldA * n)));
+  QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * 8, A_host, lda_host * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream));
+  const void* Qd = nullptr;
+  const void* Bd = nullptr;
+  int64_t ldq = 0, ldb = 0;
+  qb_status s = qb_factor(ctx, ctx->Awork.p, m, n, ldA, eps, b, q, seed, kmax, QB_OVERWRITE_A, k, &Qd, &ldq, &Bd,
+                          &ldb, resid);
+  if (s != QB_OK && s != QB_NOT_CONVERGED) return s;
+  const int64_t kc = std::min(*k, kcap_host);
+  if (kc > 0) {
+    QB_CUDA(cudaMemcpy2DAsync(Q_host, ldq_host * 8, Qd, ldq * 8, m * 8, kc, cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaMemcpy2DAsync(B_host, ldb_host * 8, Bd, ldb * 8, n * 8, kc, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return s;
 }
 
 }  // extern "C"
