@@ -295,7 +295,7 @@ def run_ours(args, cfg):
 
 def ctypes_stream(stream):
     import ctypes
-    return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(stream.cuda_stream or 1)   # 0 (legacy default) -> cudaStreamLegacy
 
 
 def main():

@@ -76,7 +76,8 @@ typedef struct {
 } qb_block_stats;
 
 /* Create a context on CUDA device `device` computing in `dtype`.  `cuda_stream` is a
- * cudaStream_t to run on, or NULL for a context-owned non-blocking stream.
+ * cudaStream_t to run on (cudaStreamLegacy = (void*)1 for the legacy default stream), or
+ * NULL for a context-owned blocking stream (ordered after legacy-default-stream work).
  * Errors: QB_ERR_INVALID_ARG (bad device / dtype), QB_ERR_CUDA.                           */
 qb_status qb_create(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream);
 
@@ -139,6 +140,24 @@ qb_status qb_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_
  * ran(X); diag(R) > 0.  w <= 256.  Returns QB_ERR_ORTH_BREAKDOWN if even the shifted
  * variant fails.  Blocking.                                                               */
 qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx);
+
+/* Test hook: one product with the library's FP64 GEMM (the kernel behind every contraction of
+ * the loop).  layout 0 (NN): C = A B with A[i + k*lda] (m x k) and B[j + k*ldb] (k x n, i.e.
+ * B row-major); layout 1 (TN): C = A^T B with A[k + i*lda] and B[k + j*ldb].  epi 0: C
+ * column-major = result; 1: C row-major (C[i*ldc + j]) = result; 2: C column-major -= result
+ * (then *sumsq = ||C||_F^2 of the updated C, else *sumsq = ||result||_F^2 when sumsq != NULL).
+ * split != 0 lets the library split K (fixed-order reduction).  FP64 contexts only.  Blocking.
+ * Pointers must be 16-byte aligned with even leading dimensions (TMA).                       */
+qb_status qb_gemm(qb_ctx ctx, int layout, int epi, int64_t M, int64_t N, int64_t K,
+                  const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                  int split, double* sumsq);
+
+/* Test hook: the CholeskyQR core on a w x w Gram matrix G (device, column-major, ldg):
+ * Rinv (device, ROW-major, ldr) = R^-1 with R^T R = G (+ the shifted-CholeskyQR shift of
+ * reading R8 on breakdown, computed for an m_rows-row X); *shifted = 0 / 1.  w <= 256.
+ * Returns QB_ERR_ORTH_BREAKDOWN if the shifted factorization fails too.  Blocking.          */
+qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_t m_rows,
+                       void* Rinv, int64_t ldr, int* shifted);
 
 /* Partial SVD from the last factorization: B = Uhat D V^*, U = Q Uhat.
  * NEXT-1 row; returns QB_ERR_UNSUPPORTED in this build.                                   */

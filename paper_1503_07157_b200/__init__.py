@@ -66,6 +66,9 @@ def lib():
                                 P(i64), P(vp), P(i64), P(vp), P(i64), P(dbl)]
         L.qb_factor_host.argtypes = [c_ctx, vp, i64, i64, i64, dbl, i64, ctypes.c_int, u64, i64, P(i64), vp, i64,
                                      vp, i64, i64, P(dbl)]
+        L.qb_gemm.argtypes = [c_ctx, ctypes.c_int, ctypes.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64,
+                              ctypes.c_int, P(dbl)]
+        L.qb_chol_rinv.argtypes = [c_ctx, vp, i64, i64, i64, vp, i64, P(ctypes.c_int)]
         L.qb_stats.argtypes = [c_ctx, vp, i64, P(i64)]
         L.qb_omega.argtypes = [c_ctx, u64, i64, i64, i64, i64, vp, i64]
         L.qb_orth.argtypes = [c_ctx, vp, i64, i64, i64]
@@ -78,7 +81,7 @@ def lib():
         L.qb_status_string.restype = ctypes.c_char_p
         L.qb_last_error.argtypes = [c_ctx]
         L.qb_last_error.restype = ctypes.c_char_p
-        for f in ("qb_create", "qb_create_dist", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_stats", "qb_omega",
+        for f in ("qb_create", "qb_create_dist", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_gemm", "qb_chol_rinv", "qb_stats", "qb_omega",
                   "qb_orth", "rqb_svd"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -165,6 +168,23 @@ def qb_omega(ctx, seed, row0, row1, col0, w, out_ptr, ldo):
     _check(ctx, lib().qb_omega(ctx, seed, row0, row1, col0, w, ctypes.c_void_p(out_ptr), ldo))
 
 
+def qb_gemm(ctx, layout, epi, M, N, K, A_ptr, lda, B_ptr, ldb, C_ptr, ldc, split=True, want_sumsq=False):
+    """Test hook over the library GEMM (see include/qb.h).  Returns ||.||_F^2 or None."""
+    ss = ctypes.c_double()
+    _check(ctx, lib().qb_gemm(ctx, layout, epi, M, N, K, ctypes.c_void_p(A_ptr), lda, ctypes.c_void_p(B_ptr), ldb,
+                              ctypes.c_void_p(C_ptr), ldc, 1 if split else 0,
+                              ctypes.byref(ss) if want_sumsq else None))
+    return ss.value if want_sumsq else None
+
+
+def qb_chol_rinv(ctx, G_ptr, ldg, w, m_rows, R_ptr, ldr):
+    """Test hook: R^-1 (row-major) of the Cholesky factor of a Gram matrix.  Returns shifted flag."""
+    sh = ctypes.c_int()
+    _check(ctx, lib().qb_chol_rinv(ctx, ctypes.c_void_p(G_ptr), ldg, w, m_rows, ctypes.c_void_p(R_ptr), ldr,
+                                   ctypes.byref(sh)))
+    return sh.value
+
+
 def qb_orth(ctx, X_ptr, m, w, ldx):
     _check(ctx, lib().qb_orth(ctx, ctypes.c_void_p(X_ptr), m, w, ldx))
 
@@ -191,10 +211,17 @@ def view_rowmajor(ptr, rows, cols, ld, typestr="<f8"):
 
 
 class QB:
-    """Owns one context.  ``factor(A, eps, b, q, seed)`` with A a CUDA float64 tensor whose
-    columns are contiguous (``A.stride(0) == 1``)."""
+    """Owns one context (on torch's current stream of `device` unless `stream` is given).
+    ``factor(A, eps, b, q, seed)`` with A a CUDA float64 tensor whose columns are contiguous
+    (``A.stride(0) == 1``)."""
 
     def __init__(self, device=0, dtype=QB_F64, stream=None):
+        # Default to torch's current stream on `device` so that the library's kernels are
+        # stream-ordered after the torch work that produced their inputs.
+        if stream is None:
+            import torch
+            h = torch.cuda.current_stream(device).cuda_stream
+            stream = ctypes.c_void_p(h if h else 1)   # 0 (torch's default) -> cudaStreamLegacy
         self.ctx = qb_create(device, dtype, stream)
 
     def close(self):

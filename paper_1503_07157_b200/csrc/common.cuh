@@ -60,12 +60,6 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-  return v;
-}
-
 // Deterministic warp sum (fixed xor tree).
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -75,8 +75,10 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
                     const GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the 128B-swizzle atoms, by pointer arithmetic on the __shared__
+  // array so that the compiler keeps the shared address space (LDS, not generic LD).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   double* red = reinterpret_cast<double*>(empty + STAGES);
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
   }
   __syncthreads();
   if (tid == 0) {
-    for (int s = 0; s < STAGES && s < nk; ++s)
+      for (int s = 0; s < STAGES && s < nk; ++s)
       gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + s * Cfg::STAGE_BYTES, smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES,
                                    &full[s], m0, n0, (kt0 + s) * GEMM_BK);
   }
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
           if (n < p.N) C[m + static_cast<int64_t>(n) * p.ldc] = acc[mi][ni][e];
         }
     }
-  } else if (EPI == EPI_STORE_ROW) {
+    } else if (EPI == EPI_STORE_ROW) {
     double* C = p.C + static_cast<int64_t>(blockIdx.y) * p.split_stride;
 #pragma unroll
     for (int mi = 0; mi < 8; ++mi) {
@@ -215,26 +217,40 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
         }
       }
     }
-  } else {  // EPI_SUB_COL: C -= acc, sum of squares of the result
+    } else {  // EPI_SUB_COL: C -= acc, sum of squares of the result
+    // 16 loads of C in flight per thread before the first dependent store (two m8 rows).
     double sq = 0.0;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
-      const int m = mb + mi * 8;
-      if (m >= p.M) continue;
+    for (int mp = 0; mp < 8; mp += 2) {
+      double cv[2][4][2];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int h = 0; h < 2; ++h) {
+        const int m = mb + (mp + h) * 8;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = nb + ni * 8 + e;
-          if (n < p.N) {
-            double* c = p.C + m + static_cast<int64_t>(n) * p.ldc;
-            const double v = *c - acc[mi][ni][e];
-            *c = v;
-            sq = fma(v, v, sq);
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = nb + ni * 8 + e;
+            cv[h][ni][e] = (m < p.M && n < p.N) ? __ldcg(p.C + m + static_cast<int64_t>(n) * p.ldc) : 0.0;
           }
-        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = mb + (mp + h) * 8;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = nb + ni * 8 + e;
+            if (m < p.M && n < p.N) {
+              const double v = cv[h][ni][e] - acc[mp + h][ni][e];
+              __stcg(p.C + m + static_cast<int64_t>(n) * p.ldc, v);
+              sq = fma(v, v, sq);
+            }
+          }
+      }
     }
-    if (p.norm_partials != nullptr) {
+      if (p.norm_partials != nullptr) {
       sq = warp_sum(sq);
       if (lane == 0) red[warp] = sq;
       __syncthreads();

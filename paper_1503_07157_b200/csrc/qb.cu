@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -92,8 +93,15 @@ qb_status fail(qb_ctx c, qb_status s, const char* fmt, ...) {
     if (s_ != QB_OK) return s_;      \
   } while (0)
 
+int debug_env(const char* name) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : 0;
+}
+
 qb_status ensure(qb_ctx ctx, DevBuf& b, size_t bytes) {
   if (b.bytes >= bytes) return QB_OK;
+  // kernels already queued on the context stream may still read the old buffer
+  if (b.p && ctx->stream) QB_CUDA(cudaStreamSynchronize(ctx->stream));
   if (b.p) QB_CUDA(cudaFree(b.p));
   b.p = nullptr;
   b.bytes = 0;
@@ -106,6 +114,12 @@ qb_status check_launch(qb_ctx ctx, const char* what) {
   ++ctx->launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, QB_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  // QB_DEBUG_SYNC=1: synchronize after every launch (localises asynchronous faults)
+  static const int sync_each = debug_env("QB_DEBUG_SYNC");
+  if (sync_each) {
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, QB_ERR_CUDA, "after %s: %s", what, cudaGetErrorString(e));
+  }
   return QB_OK;
 }
 
@@ -264,14 +278,18 @@ qb_status reduce_to_scal(qb_ctx ctx, int64_t nparts, int slot) {
 qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, int* status_out) {
   static bool attr_done = false;
   if (!attr_done) {
-    QB_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CHOL_SMEM));
+    QB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CHOL_SMEM));
+    QB_CUDA(cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRINV_SMEM));
     attr_done = true;
   }
   const int64_t ld = round_up(kMaxB, 16);
-  chol_inv_kernel<<<1, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(ctx->G.d(), ld, w, m_rows, ctx->L.d(), ld,
-                                                               ctx->Rinv.d(), ld, static_cast<int*>(ctx->status.p),
-                                                               1e-13);
-  QB_TRY(check_launch(ctx, "chol_inv"));
+  double* Dinv = ctx->L.d() + ld * ld;
+  chol_kernel<<<1, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(ctx->G.d(), ld, w, m_rows, ctx->L.d(), ld, Dinv,
+                                                           static_cast<int*>(ctx->status.p), 1e-13);
+  QB_TRY(check_launch(ctx, "chol"));
+  trinv_kernel<<<(w + CHOL_NB - 1) / CHOL_NB, TRINV_THREADS, TRINV_SMEM, ctx->stream>>>(
+      w, ctx->L.d(), ld, Dinv, static_cast<int*>(ctx->status.p), ctx->Rinv.d(), ld);
+  QB_TRY(check_launch(ctx, "trinv"));
   QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
   *status_out = ctx->h_status[0];
@@ -287,7 +305,8 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
   QB_TRY(chol_inv(ctx, w, m, &st));
   if (st == 2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR breakdown even with the shift (w=%d)", w);
   if (st == 1) *shifted = 1;
-  return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr);
+  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr));
+  return QB_OK;
 }
 
 // orth(src) -> dst by CholeskyQR2 (shifted CholeskyQR3 when the first pass breaks down).
@@ -345,6 +364,8 @@ qb_status grow_factors(qb_ctx ctx, int64_t m, int64_t n, int64_t need, int64_t k
   ctx->Qbar = nq;
   ctx->Bbar = nb;
   ctx->kcap = cap;
+  // re-projection coefficients W = Q̄^T Q_i (up to kcap x b, row-major), sized with Q̄
+  QB_TRY(ensure(ctx, ctx->W, sizeof(double) * (size_t)(cap * round_up(kMaxB, 16))));
   ctx->ldq = ldq;
   ctx->ldb = ldb;
   ctx->qbar_rows = m;
@@ -369,7 +390,8 @@ qb_status init_ctx(qb_ctx ctx, int device, qb_dtype dtype, void* stream) {
   if (stream) {
     ctx->stream = static_cast<cudaStream_t>(stream);
   } else {
-    QB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    // blocking stream: implicitly ordered after work on the legacy default stream
+    QB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault));
     ctx->own_stream = true;
   }
   void* fn = nullptr;
@@ -487,7 +509,7 @@ qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
   QB_CUDA(cudaSetDevice(ctx->device));
   const int64_t ldgb = round_up(kMaxB, 16);
   QB_TRY(ensure(ctx, ctx->G, sizeof(double) * ldgb * ldgb));
-  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * ldgb * ldgb));
+  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (ldgb * ldgb + 8 * 32 * 32)));
   QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * ldgb * ldgb));
   QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(m, 16) * kMaxB)));
   int fb = 0;
@@ -501,6 +523,49 @@ qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
     QB_TRY(cholqr2(ctx, ctx->Y.d(), ldy, ctx->Y.d(), ldy, m, (int)w, &fb));
     QB_CUDA(cudaMemcpy2DAsync(X, ldx * 8, ctx->Y.p, ldy * 8, m * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QB_OK;
+}
+
+qb_status qb_gemm(qb_ctx ctx, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, void* C, int64_t ldc, int split, double* sumsq) {
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  if (ctx->dtype != QB_F64) return fail(ctx, QB_ERR_UNSUPPORTED, "qb_gemm: FP64 contexts only");
+  if ((layout != GEMM_NN && layout != GEMM_TN) || epi < 0 || epi > 2 || M < 0 || N < 0 || K < 1 || M > INT32_MAX ||
+      N > INT32_MAX || K > INT32_MAX || !A || !B || !C)
+    return fail(ctx, QB_ERR_INVALID_ARG, "qb_gemm: bad arguments");
+  QB_CUDA(cudaSetDevice(ctx->device));
+  QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)std::max<int64_t>(
+                                     ((M + GEMM_BM - 1) / GEMM_BM) * ((N + kBN - 1) / kBN), 16 * ctx->num_sms)));
+  int64_t np = 0;
+  QB_TRY(gemm(ctx, layout, epi, (int)M, (int)N, (int)K, static_cast<const double*>(A), lda,
+              static_cast<const double*>(B), ldb, static_cast<double*>(C), ldc, sumsq != nullptr, &np, split != 0));
+  if (sumsq) {
+    QB_TRY(reduce_to_scal(ctx, np, 2));
+    QB_CUDA(cudaMemcpyAsync(ctx->h_scal + 2, ctx->scal.d() + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (sumsq) *sumsq = ctx->h_scal[2];
+  return QB_OK;
+}
+
+qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_t m_rows, void* Rinv, int64_t ldr,
+                       int* shifted) {
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  if (!G || !Rinv || w < 1 || w > kMaxB || ldg < w || ldr < w || m_rows < 1)
+    return fail(ctx, QB_ERR_INVALID_ARG, "qb_chol_rinv: bad arguments");
+  QB_CUDA(cudaSetDevice(ctx->device));
+  const int64_t ld = round_up(kMaxB, 16);
+  QB_TRY(ensure(ctx, ctx->G, sizeof(double) * ld * ld));
+  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (ld * ld + 8 * 32 * 32)));
+  QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * ld * ld));
+  QB_CUDA(cudaMemcpy2DAsync(ctx->G.p, ld * 8, G, ldg * 8, w * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
+  int st = 0;
+  QB_TRY(chol_inv(ctx, (int)w, m_rows, &st));
+  if (shifted) *shifted = st;
+  if (st >= 2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "qb_chol_rinv: shifted Cholesky failed");
+  // ctx->Rinv holds L^-1 column-major == R^-1 row-major (ld); copy rows out
+  QB_CUDA(cudaMemcpy2DAsync(Rinv, ldr * 8, ctx->Rinv.p, ld * 8, w * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
   return QB_OK;
 }
@@ -546,12 +611,16 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   QB_TRY(ensure(ctx, ctx->Y, sizeof(double) * (size_t)(ldm * b)));
   QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(std::max(m, n), 16) * kMaxB)));
   QB_TRY(ensure(ctx, ctx->G, sizeof(double) * bp * bp));
-  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * bp * bp));
+  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (bp * bp + 8 * 32 * 32)));
   QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * bp * bp));
   if (q > 0) {
     QB_TRY(ensure(ctx, ctx->Z, sizeof(double) * (size_t)(ldn * b)));
     QB_TRY(ensure(ctx, ctx->Zt, sizeof(double) * (size_t)(n * bp)));
   }
+
+  // per-CTA partials of the largest reduction (the downdate GEMM grid), sized once up front
+  QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)std::max<int64_t>(
+                                     ((m + GEMM_BM - 1) / GEMM_BM) * ((n + kBN - 1) / kBN), 16 * ctx->num_sms)));
 
   // ---- a0: r0^2 = ||A||_F^2; trivial exit (Algorithm 1 line (2), reading R3)
   {

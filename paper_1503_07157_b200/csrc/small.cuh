@@ -3,8 +3,9 @@
 //   reduce_kernel      K8: fixed-order sum of per-CTA partials -> one FP64 scalar
 //   splitk_reduce      fixed-order sum of split-K partials (+ sum of squares, the EI term)
 //   transpose_kernel   column-major <-> row-major copy of a tall-skinny panel
-//   chol_inv_kernel    K4 core: R^-1 of the Cholesky factor of a w x w Gram matrix,
-//                      with the shifted-CholeskyQR fallback (reading R8)
+//   chol_kernel        K4 core: Cholesky factor of a w x w Gram matrix (one CTA) with the
+//                      shifted-CholeskyQR fallback (reading R8)
+//   trinv_kernel       K4 core: R^-1 = L^-T by blocked forward substitution (w/32 CTAs)
 // All reductions run in a fixed order, so results are bitwise reproducible.
 #pragma once
 #include "common.cuh"
@@ -95,43 +96,42 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
 }
 
 // ---------------------------------------------------------------------------------------
-// chol_inv_kernel: one CTA, w <= CHOL_MAXW.
-//   G (w x w, column-major, symmetric positive semi-definite Gram matrix X^T X)
-//   -> L with L L^T = G + shift I (lower, column-major scratch `L`, ld ldl)
-//   -> Rinv = L^-T written ROW-major (Rinv[i*ldr + j] = (L^-1)(j, i)), upper triangular,
-//      so that Q = X Rinv is the CholeskyQR orthonormal factor.
-// Attempt 0 uses shift 0.  A pivot that is not > tol * G_jj (or NaN) is a breakdown
-// (reading R8); the kernel then restarts once with the shifted-CholeskyQR shift
-// s = 11 (m w + w (w + 1)) u trace(G) (trace(G) = ||X||_F^2 >= ||X||_2^2) and reports it.
-// status[0] = 0 ok / 1 shifted / 2 failed even with the shift.
+// K4 core, step 1 — chol_kernel: one CTA, w <= CHOL_MAXW.
+//   G (w x w, column-major, the Gram matrix X^T X)  ->  L with L L^T = G + shift I
+//   (lower, column-major `L`, ld ldl) and the inverses of its 32 x 32 diagonal blocks
+//   (`Dinv`, block J at Dinv + J*32*32, row-major 32 x 32).
+// Left-looking by 32-column panels; every operand is staged in shared memory (no dependent
+// global loads).  A pivot that is not > tol * G_jj (or NaN) is a breakdown (reading R8): the
+// kernel restarts once with the shifted-CholeskyQR shift s = 11 (m w + w (w+1)) u trace(G)
+// (trace(G) = ||X||_F^2 >= ||X||_2^2).  status[0] = 0 ok / 1 shifted / 2 failed.
 constexpr int CHOL_MAXW = 256;
 constexpr int CHOL_NB = 32;
 constexpr int CHOL_THREADS = 512;
-constexpr int CHOL_SMEM = (CHOL_MAXW * (CHOL_NB + 1) + CHOL_NB * (CHOL_MAXW + 1) + CHOL_MAXW) * 8 + 64;
+constexpr int CHOL_PLD = CHOL_NB + 1;
+constexpr int CHOL_SMEM = (2 * CHOL_MAXW * CHOL_PLD + 2 * CHOL_NB * CHOL_PLD + CHOL_MAXW) * 8;
 
-__global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int w,
-                                                                int64_t m_rows, double* __restrict__ L,
-                                                                int64_t ldl, double* __restrict__ Rinv,
-                                                                int64_t ldr, int* __restrict__ status,
-                                                                double tol) {
+__global__ void __launch_bounds__(CHOL_THREADS) chol_kernel(const double* __restrict__ G, int64_t ldg, int w,
+                                                            int64_t m_rows, double* __restrict__ L, int64_t ldl,
+                                                            double* __restrict__ Dinv, int* __restrict__ status,
+                                                            double tol) {
   extern __shared__ double sm[];
-  double* P = sm;                                   // [CHOL_MAXW][CHOL_NB + 1]
-  double* LR = P + CHOL_MAXW * (CHOL_NB + 1);       // [CHOL_NB][CHOL_MAXW + 1]
-  double* dg = LR + CHOL_NB * (CHOL_MAXW + 1);      // original diagonal of G
+  double* P = sm;                          // [CHOL_MAXW][PLD] current panel (rows p..w-1)
+  double* Lc = P + CHOL_MAXW * CHOL_PLD;   // [CHOL_MAXW][PLD] staged L(p.., kc..kc+32)
+  double* Dl = Lc + CHOL_MAXW * CHOL_PLD;  // [32][PLD] L11 of the panel
+  double* Di = Dl + CHOL_NB * CHOL_PLD;    // [32][PLD] L11^-1
+  double* dg = Di + CHOL_NB * CHOL_PLD;    // original diagonal of G
+  constexpr int PLD = CHOL_PLD;
   __shared__ int s_fail;
   __shared__ double s_shift;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int PLD = CHOL_NB + 1, LRLD = CHOL_MAXW + 1;
 
-  for (int j = tid; j < w; j += CHOL_THREADS) dg[j] = G[j + j * ldg];
+  for (int j = tid; j < w; j += CHOL_THREADS) dg[j] = __ldcg(G + j + j * ldg);
   __syncthreads();
   if (tid == 0) {
     double tr = 0.0;
     for (int j = 0; j < w; ++j) tr += dg[j];
-    const double u = 0x1p-53;
-    s_shift = 11.0 * (static_cast<double>(m_rows) * w + static_cast<double>(w) * (w + 1)) * u * tr;
+    s_shift = 11.0 * (static_cast<double>(m_rows) * w + static_cast<double>(w) * (w + 1)) * 0x1p-53 * tr;
   }
-
   int attempt = 0;
   for (; attempt < 2; ++attempt) {
     const double shift = attempt == 0 ? 0.0 : s_shift;
@@ -139,136 +139,181 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const double* __
     __syncthreads();
     for (int p = 0; p < w; p += CHOL_NB) {
       const int nb = min(CHOL_NB, w - p), rows = w - p;
-      // stage L(p + j, 0:p) and the panel G(p:w, p:p+nb)
-      for (int idx = tid; idx < nb * p; idx += CHOL_THREADS) {
-        const int j = idx % nb, k = idx / nb;
-        LR[j * LRLD + k] = L[(p + j) + static_cast<int64_t>(k) * ldl];
-      }
       for (int idx = tid; idx < rows * nb; idx += CHOL_THREADS) {
         const int i = idx % rows, j = idx / rows;
-        double v = G[(p + i) + static_cast<int64_t>(p + j) * ldg];
+        double v = __ldcg(G + (p + i) + static_cast<int64_t>(p + j) * ldg);
         if (i == j) v += shift;
         P[i * PLD + j] = v;
       }
-      __syncthreads();
-      // left-looking update: P(i, j) -= sum_{k<p} L(p+i, k) L(p+j, k)
-      if (p > 0) {
-        const int half = tid >> 8, i = tid & 255;
-        if (i < rows) {
-          double acc[16];
+      // left-looking update P -= L(p:w, 0:p) L(p:p+nb, 0:p)^T, 32 columns of L at a time
+      const int j = lane, i0 = warp;  // thread owns P(i0 + 16 r, j), r < 16
+      double acc[16];
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) acc[jj] = 0.0;
-          for (int k = 0; k < p; ++k) {
-            const double l = L[(p + i) + static_cast<int64_t>(k) * ldl];
+      for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+      for (int kc = 0; kc < p; kc += CHOL_NB) {
+        __syncthreads();
+        for (int idx = tid; idx < rows * CHOL_NB; idx += CHOL_THREADS) {
+          const int i = idx % rows, kk = idx / rows;
+          Lc[i * PLD + kk] = __ldcg(L + (p + i) + static_cast<int64_t>(kc + kk) * ldl);
+        }
+        __syncthreads();
+        if (j < nb) {
+#pragma unroll 4
+          for (int kk = 0; kk < CHOL_NB; ++kk) {
+            const double lj = Lc[j * PLD + kk];
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) acc[jj] = fma(l, LR[(half * 16 + jj) * LRLD + k], acc[jj]);
+            for (int r = 0; r < 16; ++r) {
+              const int i = i0 + 16 * r;
+              if (i < rows) acc[r] = fma(Lc[i * PLD + kk], lj, acc[r]);
+            }
           }
+        }
+      }
+      __syncthreads();
+      if (j < nb) {
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj)
-            if (half * 16 + jj < nb) P[i * PLD + half * 16 + jj] -= acc[jj];
+        for (int r = 0; r < 16; ++r) {
+          const int i = i0 + 16 * r;
+          if (i < rows) P[i * PLD + j] -= acc[r];
         }
       }
       __syncthreads();
       // unblocked Cholesky of the nb x nb diagonal block (warp 0, lane = row)
       if (warp == 0) {
-        for (int j = 0; j < nb; ++j) {
-          const double d = P[j * PLD + j];
-          const bool bad = !(d > tol * dg[p + j]) || !(d > 0.0);
-          if (bad) {
+        for (int jj = 0; jj < nb; ++jj) {
+          const double d = P[jj * PLD + jj];
+          if (!(d > tol * dg[p + jj]) || !(d > 0.0)) {
             if (lane == 0) s_fail = 1;
             break;
           }
           const double r = sqrt(d);
           __syncwarp();
-          if (lane == j) P[j * PLD + j] = r;
-          if (lane > j && lane < nb) P[lane * PLD + j] /= r;
+          if (lane == jj) P[jj * PLD + jj] = r;
+          if (lane > jj && lane < nb) P[lane * PLD + jj] /= r;
           __syncwarp();
-          if (lane > j && lane < nb) {
-            const double lij = P[lane * PLD + j];
-            for (int c = j + 1; c <= lane; ++c) P[lane * PLD + c] -= lij * P[c * PLD + j];
+          if (lane > jj && lane < nb) {
+            const double lij = P[lane * PLD + jj];
+            for (int c = jj + 1; c <= lane; ++c) P[lane * PLD + c] -= lij * P[c * PLD + jj];
           }
           __syncwarp();
+        }
+        // L11 (lower) -> Dl, zero above; L11^-1 by forward substitution, lane = column
+        if (!s_fail) {
+          for (int r = 0; r < CHOL_NB; ++r) Dl[r * PLD + lane] = (r < nb && lane < nb && lane <= r) ? P[r * PLD + lane] : (r == lane ? 1.0 : 0.0);
+          __syncwarp();
+          for (int r = 0; r < CHOL_NB; ++r) {
+            double v = (r == lane) ? 1.0 : 0.0;
+            for (int k = lane; k < r; ++k) v -= Dl[r * PLD + k] * Di[k * PLD + lane];
+            Di[r * PLD + lane] = (r >= lane) ? v / Dl[r * PLD + r] : 0.0;
+            __syncwarp();
+          }
         }
       }
       __syncthreads();
       if (s_fail) break;
-      // panel below the diagonal block: x L11^T = P(i, :), forward substitution per row
-      for (int i = nb + tid; i < rows; i += CHOL_THREADS) {
-        for (int j = 0; j < nb; ++j) {
-          double v = P[i * PLD + j];
-          for (int c = 0; c < j; ++c) v -= P[i * PLD + c] * P[j * PLD + c];
-          P[i * PLD + j] = v / P[j * PLD + j];
+      // panel below the diagonal block: L21 = P21 L11^-T, L21(i, j) = sum_{c<=j} P(i, c) Di(j, c)
+      {
+        double out[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int i = nb + i0 + 16 * r;
+          double v = 0.0;
+          if (i < rows && j < nb)
+            for (int c = 0; c <= j; ++c) v = fma(P[i * PLD + c], Di[j * PLD + c], v);
+          out[r] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int i = nb + i0 + 16 * r;
+          if (i < rows && j < nb) P[i * PLD + j] = out[r];
         }
       }
       __syncthreads();
       for (int idx = tid; idx < rows * nb; idx += CHOL_THREADS) {
-        const int i = idx % rows, j = idx / rows;
-        if (i >= j) L[(p + i) + static_cast<int64_t>(p + j) * ldl] = P[i * PLD + j];
+        const int i = idx % rows, jj = idx / rows;
+        L[(p + i) + static_cast<int64_t>(p + jj) * ldl] = (i >= jj) ? P[i * PLD + jj] : 0.0;
       }
+      for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
+        Dinv[(p / CHOL_NB) * CHOL_NB * CHOL_NB + idx] = Di[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)];
       __syncthreads();
     }
     if (!s_fail) break;
   }
-  if (attempt == 2) {
-    if (tid == 0) status[0] = 2;
-    return;
-  }
-  if (tid == 0) status[0] = attempt;
-  __syncthreads();
+  if (tid == 0) status[0] = attempt;  // 0, 1, or 2 (= failed twice)
+}
 
-  // ---- Linv = L^-1 (lower), stored column-major in Rinv (=> Rinv row-major = L^-T).
-  // zero the strictly upper part
-  for (int64_t idx = tid; idx < static_cast<int64_t>(w) * w; idx += CHOL_THREADS) {
-    const int r = static_cast<int>(idx % w), c = static_cast<int>(idx / w);
-    if (r < c) Rinv[r + static_cast<int64_t>(c) * ldr] = 0.0;
-  }
+// K4 core, step 2 — trinv_kernel: grid = ceil(w/32) CTAs, CTA J computes block column J of
+// L^-1 (rows >= 32J) by blocked forward substitution
+//   X_JJ = Dinv_J,  X_IJ = -Dinv_I sum_{K=J}^{I-1} L_IK X_KJ  (I > J)
+// and writes it column-major into Rinv (ld ldr), zero above the diagonal, so that Rinv read
+// ROW-major is R^-1 = L^-T, upper triangular: Q = X Rinv is the CholeskyQR factor.
+constexpr int TRINV_THREADS = 256;
+constexpr int TRINV_LRLD = CHOL_MAXW + 1;
+constexpr int TRINV_SMEM = (CHOL_MAXW * CHOL_PLD + CHOL_NB * TRINV_LRLD + 2 * CHOL_NB * CHOL_PLD) * 8;
+
+__global__ void __launch_bounds__(TRINV_THREADS) trinv_kernel(int w, const double* __restrict__ L, int64_t ldl,
+                                                              const double* __restrict__ Dinv,
+                                                              const int* __restrict__ status,
+                                                              double* __restrict__ Rinv, int64_t ldr) {
+  if (__ldcg(status) >= 2) return;
+  extern __shared__ double sm[];
+  constexpr int PLD = CHOL_PLD;
+  double* X = sm;                             // [CHOL_MAXW][PLD] rows oJ.. of block column J
+  double* Lr = X + CHOL_MAXW * PLD;           // [32][TRINV_LRLD] L(oI.., oJ..oI)
+  double* Tb = Lr + CHOL_NB * TRINV_LRLD;     // [32][PLD]
+  double* Db = Tb + CHOL_NB * PLD;            // [32][PLD]
+  const int tid = threadIdx.x;
+  const int J = blockIdx.x, oJ = J * CHOL_NB, bsJ = min(CHOL_NB, w - oJ);
   const int nbk = (w + CHOL_NB - 1) / CHOL_NB;
-  // (a) diagonal blocks: warp jb inverts L_jb,jb by forward substitution, lane = column
-  for (int jb = warp; jb < nbk; jb += CHOL_THREADS / 32) {
-    const int o = jb * CHOL_NB, bs = min(CHOL_NB, w - o);
-    double* X = P + jb * CHOL_NB * PLD;  // bs x bs scratch rows (fits: nbk*32 <= CHOL_MAXW rows)
-    if (lane < bs) {
-      for (int r = 0; r < bs; ++r) {
-        double v = (r == lane) ? 1.0 : 0.0;
-        if (r > lane) {
-          for (int k = lane; k < r; ++k) v -= L[(o + r) + static_cast<int64_t>(o + k) * ldl] * X[k * PLD + lane];
-        } else if (r < lane) {
-          v = 0.0;
-        }
-        X[r * PLD + lane] = (r >= lane) ? v / L[(o + r) + static_cast<int64_t>(o + r) * ldl] : 0.0;
-      }
-      for (int r = 0; r < bs; ++r) Rinv[(o + r) + static_cast<int64_t>(o + lane) * ldr] = X[r * PLD + lane];
+  for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += TRINV_THREADS)
+    X[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = __ldcg(Dinv + J * CHOL_NB * CHOL_NB + idx);
+  const int r = tid >> 3, c0 = (tid & 7) * 4;  // thread owns T(r, c0..c0+3)
+  for (int I = J + 1; I < nbk; ++I) {
+    const int oI = I * CHOL_NB, bsI = min(CHOL_NB, w - oI), kl = oI - oJ;
+    __syncthreads();
+    for (int idx = tid; idx < CHOL_NB * kl; idx += TRINV_THREADS) {
+      const int rr = idx % CHOL_NB, kk = idx / CHOL_NB;
+      Lr[rr * TRINV_LRLD + kk] = rr < bsI ? __ldcg(L + (oI + rr) + static_cast<int64_t>(oJ + kk) * ldl) : 0.0;
     }
+    for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += TRINV_THREADS)
+      Db[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = __ldcg(Dinv + I * CHOL_NB * CHOL_NB + idx);
+    __syncthreads();
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    for (int kk = 0; kk < kl; ++kk) {
+      const double l = Lr[r * TRINV_LRLD + kk];
+      const double* x = X + kk * PLD + c0;
+      t0 = fma(l, x[0], t0);
+      t1 = fma(l, x[1], t1);
+      t2 = fma(l, x[2], t2);
+      t3 = fma(l, x[3], t3);
+    }
+    Tb[r * PLD + c0] = t0;
+    Tb[r * PLD + c0 + 1] = t1;
+    Tb[r * PLD + c0 + 2] = t2;
+    Tb[r * PLD + c0 + 3] = t3;
+    __syncthreads();
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    for (int t = 0; t <= r; ++t) {
+      const double d = Db[r * PLD + t];
+      v0 = fma(d, Tb[t * PLD + c0], v0);
+      v1 = fma(d, Tb[t * PLD + c0 + 1], v1);
+      v2 = fma(d, Tb[t * PLD + c0 + 2], v2);
+      v3 = fma(d, Tb[t * PLD + c0 + 3], v3);
+    }
+    double* xo = X + (kl + r) * PLD + c0;
+    xo[0] = -v0;
+    xo[1] = -v1;
+    xo[2] = -v2;
+    xo[3] = -v3;
   }
   __syncthreads();
-  // (b) block rows I = 1..nbk-1: X_IJ = -X_II * sum_{K=J}^{I-1} L_IK X_KJ  for J < I
-  double* T = LR;  // [I*CHOL_NB][CHOL_NB+1] scratch (I*32 <= CHOL_MAXW - 32 rows)
-  for (int I = 1; I < nbk; ++I) {
-    const int oI = I * CHOL_NB, bsI = min(CHOL_NB, w - oI);
-    const int nel = I * CHOL_NB * CHOL_NB;
-    for (int idx = tid; idx < nel; idx += CHOL_THREADS) {
-      const int J = idx / (CHOL_NB * CHOL_NB), rem = idx % (CHOL_NB * CHOL_NB);
-      const int r = rem / CHOL_NB, c = rem % CHOL_NB;
-      double v = 0.0;
-      if (r < bsI) {
-        const int col = J * CHOL_NB + c;
-        for (int k = J * CHOL_NB + c; k < oI; ++k)  // X(k, col) = 0 for k < col
-          v += L[(oI + r) + static_cast<int64_t>(k) * ldl] * Rinv[k + static_cast<int64_t>(col) * ldr];
-      }
-      T[(J * CHOL_NB + r) * PLD + c] = v;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nel; idx += CHOL_THREADS) {
-      const int J = idx / (CHOL_NB * CHOL_NB), rem = idx % (CHOL_NB * CHOL_NB);
-      const int r = rem / CHOL_NB, c = rem % CHOL_NB;
-      if (r < bsI) {
-        double v = 0.0;
-        for (int t = 0; t <= r; ++t)
-          v += Rinv[(oI + r) + static_cast<int64_t>(oI + t) * ldr] * T[(J * CHOL_NB + t) * PLD + c];
-        Rinv[(oI + r) + static_cast<int64_t>(J * CHOL_NB + c) * ldr] = -v;
-      }
-    }
-    __syncthreads();
+  // write block column J of L^-1 (column-major, zeros above the diagonal block)
+  for (int idx = tid; idx < w * bsJ; idx += TRINV_THREADS) {
+    const int row = idx % w, c = idx / w;
+    double v = 0.0;
+    if (row >= oJ) v = X[(row - oJ) * PLD + c];
+    Rinv[row + static_cast<int64_t>(oJ + c) * ldr] = v;
   }
 }
 

@@ -242,3 +242,17 @@ def test_target_config_properties(qbmod, ctx):
         got = out.cpu().numpy()[rows]
         ref = np.vstack([oomega.omega_panel(cfg.seed_omega, cfg.n, c0, cfg.b, r, r + 1) for r in rows])
         assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+
+
+def test_fresh_context_reproducible_across_growth(qbmod):
+    """k > 1024 forces the Q̄/B̄ capacity to grow inside the first call; a fresh context and a
+    reused one must give bitwise identical factors (fixed-order reductions)."""
+    sig = np.exp(-np.arange(1, 3001) / 100.0)
+    Ad = synth.make_matrix_torch(3000, 3000, sig, 77)
+    c = qbmod.QB(0)
+    g1 = c.factor(Ad, 1e-4, 64, 0, seed=5)
+    g2 = c.factor(Ad, 1e-4, 64, 0, seed=5)
+    c.close()
+    assert g1["k"] == g2["k"] and g1["k"] > 1024
+    assert torch.equal(g1["Q"], g2["Q"]) and torch.equal(g1["B"], g2["B"])
+    assert [s["r2"] for s in g1["stats"]] == [s["r2"] for s in g2["stats"]]
