@@ -39,6 +39,7 @@ struct GemmParams {
   int64_t ldc;
   int64_t split_stride;  // elements between split partial outputs
   double* norm_partials; // EPI_SUB_COL: per-CTA sum of squares of the new C
+  const int* gate;       // optional: the kernel does nothing unless *gate != 0
 };
 
 template <int BN>
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
                     const GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
+  if (p.gate != nullptr && __ldcg(p.gate) == 0) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms, by pointer arithmetic on the __shared__
   // array so that the compiler keeps the shared address space (LDS, not generic LD).

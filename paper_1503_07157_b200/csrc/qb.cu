@@ -180,7 +180,8 @@ int choose_splits(int tiles, int nkt, int slots, int max_splits) {
 // K dimension may be split; then partials land in ctx->P and are reduced in a fixed order
 // (with the sum of squares of C into ctx->parts when want_norm).
 qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const double* A, int64_t lda, const double* B,
-               int64_t ldb, double* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true) {
+               int64_t ldb, double* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true,
+               const int* gate = nullptr) {
   if (nparts) *nparts = 0;
   if (M <= 0 || N <= 0) return QB_OK;
   CUtensorMap ta, tb;
@@ -199,6 +200,7 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   p.tiles_n = (N + kBN - 1) / kBN;
   p.nkt = (K + GEMM_BK - 1) / GEMM_BK;
   p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
+  p.gate = gate;
   const int tiles = p.tiles_m * p.tiles_n;
   const int slots = ctx->num_sms * GemmCfg<kBN>::MIN_BLOCKS;
   int splits = 1;
@@ -265,7 +267,8 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
     sq = ctx->parts.d();
     if (nparts) *nparts = grid;
   }
-  splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp, C, ldc, sq);
+  splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp, C, ldc, sq,
+                                                               gate);
   return check_launch(ctx, "splitk_reduce");
 }
 
@@ -275,7 +278,11 @@ qb_status reduce_to_scal(qb_ctx ctx, int64_t nparts, int slot) {
 }
 
 // ---------------------------------------------------------------- CholeskyQR2
-qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, int* status_out) {
+int* status_dev(qb_ctx ctx) { return static_cast<int*>(ctx->status.p); }
+
+// T for one CholeskyQR pass from the Gram matrix in ctx->G (no host synchronisation):
+// Newton-Schulz T = I - (G - I)/2 when ||G - I||_F <= 1e-8 (ns), else T = R^-1.
+qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) {
   static bool attr_done = false;
   if (!attr_done) {
     QB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CHOL_SMEM));
@@ -285,46 +292,43 @@ qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, int* status_out) {
   const int64_t ld = round_up(kMaxB, 16);
   double* Dinv = ctx->L.d() + ld * ld;
   chol_kernel<<<1, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(ctx->G.d(), ld, w, m_rows, ctx->L.d(), ld, Dinv,
-                                                           static_cast<int*>(ctx->status.p), 1e-13);
+                                                           ctx->Rinv.d(), ld, status_dev(ctx), 1e-13,
+                                                           ns ? 1e-16 : -1.0, gate);
   QB_TRY(check_launch(ctx, "chol"));
   trinv_kernel<<<(w + CHOL_NB - 1) / CHOL_NB, TRINV_THREADS, TRINV_SMEM, ctx->stream>>>(
-      w, ctx->L.d(), ld, Dinv, static_cast<int*>(ctx->status.p), ctx->Rinv.d(), ld);
-  QB_TRY(check_launch(ctx, "trinv"));
-  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  QB_CUDA(cudaStreamSynchronize(ctx->stream));
-  *status_out = ctx->h_status[0];
-  return QB_OK;
+      w, ctx->L.d(), ld, Dinv, status_dev(ctx), ctx->Rinv.d(), ld, gate);
+  return check_launch(ctx, "trinv");
 }
 
-// One CholeskyQR pass: dst = src R^-1 with R^T R = src^T src (+ shift on breakdown).
+// One CholeskyQR pass: dst = src T, with T from chol_inv (all on the device; gated).
 qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
-                      int* shifted) {
+                      const int* gate) {
   const int64_t ldgb = round_up(kMaxB, 16);
-  QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr));
-  int st = 0;
-  QB_TRY(chol_inv(ctx, w, m, &st));
-  if (st == 2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR breakdown even with the shift (w=%d)", w);
-  if (st == 1) *shifted = 1;
-  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr));
-  return QB_OK;
+  QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr, true,
+              gate));
+  QB_TRY(chol_inv(ctx, w, m, true, gate));
+  return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr, true,
+              gate);
 }
 
-// orth(src) -> dst by CholeskyQR2 (shifted CholeskyQR3 when the first pass breaks down).
-// src and dst may alias; ctx->T1 (rows x kMaxB, ld ldt) is the scratch.
-qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w, int* fallbacks) {
+// orth(src) -> dst: CholeskyQR2, where a pass whose Gram is already within 1e-8 of I takes
+// the Newton-Schulz step instead of a factorization; a shifted first factorization (reading
+// R8) triggers two more passes (shifted CholeskyQR3), gated on the device flag status[1].
+// src and dst may alias; ctx->T1 is the scratch.  Nothing here synchronises with the host;
+// failures surface in status[3], read at the end of the block.
+qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w) {
   const int64_t ldt = round_up(m, 16);
   double* T = ctx->T1.d();
-  int shifted = 0;
-  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, &shifted));
-  int again = 0;
-  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, &again));
-  if (shifted || again) {
-    ++*fallbacks;
-    int again2 = 0;
-    QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, &again2));
-    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, &again2));
-    if (again2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR3 did not converge (w=%d)", w);
-  }
+  QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, sizeof(int), ctx->stream));
+  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr));
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, nullptr));
+  QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1));
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1));
+  return QB_OK;
+}
+
+qb_status reset_flags(qb_ctx ctx) {
+  QB_CUDA(cudaMemsetAsync(status_dev(ctx), 0, 4 * sizeof(int), ctx->stream));
   return QB_OK;
 }
 
@@ -512,18 +516,20 @@ qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
   QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (ldgb * ldgb + 8 * 32 * 32)));
   QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * ldgb * ldgb));
   QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(m, 16) * kMaxB)));
-  int fb = 0;
+  QB_TRY(reset_flags(ctx));
   const bool aligned = (ldx % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
   if (aligned) {
-    QB_TRY(cholqr2(ctx, static_cast<double*>(X), ldx, static_cast<double*>(X), ldx, m, (int)w, &fb));
+    QB_TRY(cholqr2(ctx, static_cast<double*>(X), ldx, static_cast<double*>(X), ldx, m, (int)w));
   } else {  // TMA needs 16-byte aligned columns: stage through an aligned copy
     const int64_t ldy = round_up(m, 16);
     QB_TRY(ensure(ctx, ctx->Y, sizeof(double) * (size_t)(ldy * w)));
     QB_CUDA(cudaMemcpy2DAsync(ctx->Y.p, ldy * 8, X, ldx * 8, m * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
-    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldy, ctx->Y.d(), ldy, m, (int)w, &fb));
+    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldy, ctx->Y.d(), ldy, m, (int)w));
     QB_CUDA(cudaMemcpy2DAsync(X, ldx * 8, ctx->Y.p, ldy * 8, m * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->h_status[3]) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift (w=%lld)", (long long)w);
   return QB_OK;
 }
 
@@ -560,10 +566,13 @@ qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_
   QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (ld * ld + 8 * 32 * 32)));
   QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * ld * ld));
   QB_CUDA(cudaMemcpy2DAsync(ctx->G.p, ld * 8, G, ldg * 8, w * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
-  int st = 0;
-  QB_TRY(chol_inv(ctx, (int)w, m_rows, &st));
+  QB_TRY(reset_flags(ctx));
+  QB_TRY(chol_inv(ctx, (int)w, m_rows, false, nullptr));
+  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int st = ctx->h_status[0];
   if (shifted) *shifted = st;
-  if (st >= 2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "qb_chol_rinv: shifted Cholesky failed");
+  if (st == 2) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "qb_chol_rinv: shifted Cholesky failed");
   // ctx->Rinv holds L^-1 column-major == R^-1 row-major (ld); copy rows out
   QB_CUDA(cudaMemcpy2DAsync(Rinv, ldr * 8, ctx->Rinv.p, ld * 8, w * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -653,7 +662,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     const int64_t w = std::min<int64_t>(b, kmax_eff - ell);
     QB_TRY(grow_factors(ctx, m, n, ell + w, kmax_eff));
     QB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    ctx->block_fallbacks = 0;
+    QB_TRY(reset_flags(ctx));
     double* Qbar = ctx->Qbar.d();
     double* Qi = Qbar + ell * ctx->ldq;
     double* Bi = ctx->Bbar.d() + ell * ctx->ldb;
@@ -665,12 +674,12 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Om.d(), bp, ctx->Y.d(), ldm, false,
                 nullptr));
     QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
-    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, &ctx->block_fallbacks));
+    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     for (int j = 0; j < q; ++j) {
       QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, Qi, ctx->ldq, ctx->Z.d(), ldn, false,
                   nullptr));
-      QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, &ctx->block_fallbacks));
+      QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w));
       {
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w + 31) / 32));
         transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w, ctx->Zt.d(), bp);
@@ -678,7 +687,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       }
       QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Zt.d(), bp, ctx->Y.d(), ldm,
                   false, nullptr));
-      QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, &ctx->block_fallbacks));
+      QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
     if (ell > 0 && !(flags & QB_NO_REPROJ)) {
@@ -687,7 +696,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
                   false, nullptr));
       QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)ell, Qbar, ctx->ldq, ctx->W.d(), bp, Qi, ctx->ldq,
                   false, nullptr));
-      QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, &ctx->block_fallbacks));
+      QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w));
     }
     // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
     int64_t nb_parts = 0;
@@ -704,8 +713,13 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_CUDA(cudaEventRecord(ctx->evp[5], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_status[3])
+      return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift in the block ending at %lld",
+                  (long long)(ell + w));
+    ctx->block_fallbacks = ctx->h_status[2];
     r2 = ctx->h_scal[0];
     ei -= ctx->h_scal[1];
     ell += w;

@@ -54,7 +54,9 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_kernel(const double* __res
 __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double* __restrict__ P, int S, int64_t stride,
                                                                     int64_t rows, int64_t cols, int64_t ldp,
                                                                     double* __restrict__ out, int64_t ldo,
-                                                                    double* __restrict__ sq_partials) {
+                                                                    double* __restrict__ sq_partials,
+                                                                    const int* __restrict__ gate) {
+  if (gate != nullptr && __ldcg(gate) == 0) return;
   __shared__ double red[RED_THREADS / 32];
   double sq = 0.0;
   const int64_t total = rows * cols;
@@ -96,24 +98,33 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
 }
 
 // ---------------------------------------------------------------------------------------
-// K4 core, step 1 — chol_kernel: one CTA, w <= CHOL_MAXW.
-//   G (w x w, column-major, the Gram matrix X^T X)  ->  L with L L^T = G + shift I
-//   (lower, column-major `L`, ld ldl) and the inverses of its 32 x 32 diagonal blocks
-//   (`Dinv`, block J at Dinv + J*32*32, row-major 32 x 32).
-// Left-looking by 32-column panels; every operand is staged in shared memory (no dependent
-// global loads).  A pivot that is not > tol * G_jj (or NaN) is a breakdown (reading R8): the
-// kernel restarts once with the shifted-CholeskyQR shift s = 11 (m w + w (w+1)) u trace(G)
-// (trace(G) = ||X||_F^2 >= ||X||_2^2).  status[0] = 0 ok / 1 shifted / 2 failed.
+// K4 core, step 1 — chol_kernel: one CTA, w <= CHOL_MAXW.  Given the w x w Gram matrix
+// G = X^T X (column-major), produce T (row-major, in `Rinv`) such that X T is orthonormal:
+//   * Newton-Schulz path: if ||G - I||_F <= ns_tol, X is already orthonormal to first order
+//     and T = I - (G - I)/2 (one Newton-Schulz step towards the polar factor; the error is
+//     (3/4)||G - I||^2, below u for ns_tol = 1e-8).  No factorization.   status[0] = 3.
+//   * Cholesky path: L L^T = G (+ shift), written column-major to `L` with the inverses of its
+//     32 x 32 diagonal blocks in `Dinv` (block J at Dinv + J*32*32, row-major); trinv_kernel
+//     then writes T = R^-1 = L^-T.  Left-looking by 32-column panels, operands staged in
+//     shared memory.  A pivot that is not > tol * G_jj (or NaN) is a breakdown (reading R8):
+//     the kernel restarts once with the shifted-CholeskyQR shift s = 11 (m w + w (w+1)) u
+//     trace(G) (trace(G) = ||X||_F^2 >= ||X||_2^2).  status[0] = 0 ok / 1 shifted / 2 failed.
+// Block-level flags: status[1] = 1 when the shift was used (gates the extra CholeskyQR3
+// passes), status[2] += 1 per shifted factorization, status[3] = 1 on failure.
+// `gate` (may be null): the kernel does nothing unless *gate != 0.
 constexpr int CHOL_MAXW = 256;
 constexpr int CHOL_NB = 32;
 constexpr int CHOL_THREADS = 512;
 constexpr int CHOL_PLD = CHOL_NB + 1;
 constexpr int CHOL_SMEM = (2 * CHOL_MAXW * CHOL_PLD + 2 * CHOL_NB * CHOL_PLD + CHOL_MAXW) * 8;
+constexpr int CHOL_ST_NS = 3;
 
 __global__ void __launch_bounds__(CHOL_THREADS) chol_kernel(const double* __restrict__ G, int64_t ldg, int w,
                                                             int64_t m_rows, double* __restrict__ L, int64_t ldl,
-                                                            double* __restrict__ Dinv, int* __restrict__ status,
-                                                            double tol) {
+                                                            double* __restrict__ Dinv, double* __restrict__ Rinv,
+                                                            int64_t ldr, int* __restrict__ status, double tol,
+                                                            double ns_tol2, const int* __restrict__ gate) {
+  if (gate != nullptr && __ldcg(gate) == 0) return;
   extern __shared__ double sm[];
   double* P = sm;                          // [CHOL_MAXW][PLD] current panel (rows p..w-1)
   double* Lc = P + CHOL_MAXW * CHOL_PLD;   // [CHOL_MAXW][PLD] staged L(p.., kc..kc+32)
@@ -122,8 +133,37 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_kernel(const double* __rest
   double* dg = Di + CHOL_NB * CHOL_PLD;    // original diagonal of G
   constexpr int PLD = CHOL_PLD;
   __shared__ int s_fail;
-  __shared__ double s_shift;
+  __shared__ double s_shift, s_e2;
+  __shared__ double red[CHOL_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- Newton-Schulz test: e2 = ||G - I||_F^2 (fixed-order reduction)
+  if (ns_tol2 >= 0.0) {
+    double e2 = 0.0;
+    for (int idx = tid; idx < w * w; idx += CHOL_THREADS) {
+      const int i = idx % w, j = idx / w;
+      const double d = __ldcg(G + i + static_cast<int64_t>(j) * ldg) - (i == j ? 1.0 : 0.0);
+      e2 = fma(d, d, e2);
+    }
+    e2 = warp_sum(e2);
+    if (lane == 0) red[warp] = e2;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int k = 0; k < CHOL_THREADS / 32; ++k) t += red[k];
+      s_e2 = t;
+    }
+    __syncthreads();
+    if (s_e2 <= ns_tol2) {
+      for (int idx = tid; idx < w * w; idx += CHOL_THREADS) {
+        const int i = idx / w, j = idx % w;
+        const double d = __ldcg(G + i + static_cast<int64_t>(j) * ldg) - (i == j ? 1.0 : 0.0);
+        Rinv[static_cast<int64_t>(i) * ldr + j] = (i == j ? 1.0 : 0.0) - 0.5 * d;
+      }
+      if (tid == 0) status[0] = CHOL_ST_NS;
+      return;
+    }
+  }
 
   for (int j = tid; j < w; j += CHOL_THREADS) dg[j] = __ldcg(G + j + j * ldg);
   __syncthreads();
@@ -240,7 +280,14 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_kernel(const double* __rest
     }
     if (!s_fail) break;
   }
-  if (tid == 0) status[0] = attempt;  // 0, 1, or 2 (= failed twice)
+  if (tid == 0) {
+    status[0] = attempt;  // 0, 1, or 2 (= failed twice)
+    if (attempt == 1) {
+      status[1] = 1;
+      atomicAdd(status + 2, 1);
+    }
+    if (attempt >= 2) status[3] = 1;
+  }
 }
 
 // K4 core, step 2 — trinv_kernel: grid = ceil(w/32) CTAs, CTA J computes block column J of
@@ -255,8 +302,10 @@ constexpr int TRINV_SMEM = (CHOL_MAXW * CHOL_PLD + CHOL_NB * TRINV_LRLD + 2 * CH
 __global__ void __launch_bounds__(TRINV_THREADS) trinv_kernel(int w, const double* __restrict__ L, int64_t ldl,
                                                               const double* __restrict__ Dinv,
                                                               const int* __restrict__ status,
-                                                              double* __restrict__ Rinv, int64_t ldr) {
-  if (__ldcg(status) >= 2) return;
+                                                              double* __restrict__ Rinv, int64_t ldr,
+                                                              const int* __restrict__ gate) {
+  if (gate != nullptr && __ldcg(gate) == 0) return;
+  if (__ldcg(status) >= 2) return;  // failed, or the Newton-Schulz path already wrote T
   extern __shared__ double sm[];
   constexpr int PLD = CHOL_PLD;
   double* X = sm;                             // [CHOL_MAXW][PLD] rows oJ.. of block column J
