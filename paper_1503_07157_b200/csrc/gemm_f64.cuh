@@ -50,7 +50,13 @@ struct GemmCfg {
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 8;
   static constexpr int B_BYTES = BN * GEMM_BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 2 * STAGES * 8 + WARPS * 8;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + (2 * STAGES + 1) * 8 + WARPS * 8;
+  // EPI_SUB_COL prefetches its C tile (128 x BN) by TMA into pipeline slots as they drain:
+  // box {16 m, BN n}, C_PER_SLOT boxes per slot, C_GROUPS slots.
+  static constexpr int C_BOX_BYTES = BN * 128;
+  static constexpr int C_PER_SLOT = STAGE_BYTES / C_BOX_BYTES;
+  static constexpr int C_GROUPS = (GEMM_BM / 16 + C_PER_SLOT - 1) / C_PER_SLOT;
+  static_assert(C_PER_SLOT >= 1 && C_GROUPS <= STAGES, "C tile must fit in the drained pipeline slots");
   static constexpr int MIN_BLOCKS = BN == 64 ? 2 : 1;
 };
 
@@ -70,10 +76,22 @@ __device__ __forceinline__ void gemm_issue_stage(const CUtensorMap* tA, const CU
   }
 }
 
+// Issue the TMA loads of C-tile box group g (EPI_SUB_COL prefetch) into pipeline slot `slot`.
+template <int BN>
+__device__ __forceinline__ void gemm_issue_c_group(const CUtensorMap* tC, uint8_t* smem, uint64_t* cbar, int g, int slot,
+                                                   int m0, int n0) {
+  using Cfg = GemmCfg<BN>;
+#pragma unroll
+  for (int j = 0; j < Cfg::C_PER_SLOT; ++j) {
+    const int b = g * Cfg::C_PER_SLOT + j;
+    if (b < GEMM_BM / 16) tma_load_2d(smem + slot * Cfg::STAGE_BYTES + j * Cfg::C_BOX_BYTES, tC, cbar, m0 + 16 * b, n0);
+  }
+}
+
 template <int LAYOUT, int BN, int EPI>
 __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
-                    const GemmParams p) {
+                    const __grid_constant__ CUtensorMap tC, const GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   if (p.gate != nullptr && __ldcg(p.gate) == 0) return;
@@ -83,7 +101,9 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  double* red = reinterpret_cast<double*>(empty + STAGES);
+  uint64_t* cbar = empty + STAGES;
+  double* red = reinterpret_cast<double*>(cbar + 1);
+  constexpr bool kPrefetchC = (EPI == EPI_SUB_COL);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
@@ -109,10 +129,20 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::WARPS);
     }
+    mbar_init(cbar, 1);
     fence_barrier_init();
   }
   __syncthreads();
   if (tid == 0) {
+    if (kPrefetchC) {
+      tma_prefetch_desc(&tC);
+      mbar_arrive_expect_tx(cbar, (GEMM_BM / 16) * Cfg::C_BOX_BYTES);
+      // groups whose slot no k-tile ever uses go out right away
+      for (int g = 0; g < Cfg::C_GROUPS; ++g) {
+        const int t = nk - Cfg::C_GROUPS + g;
+        if (t < 0) gemm_issue_c_group<BN>(&tC, smem, cbar, g, ((t % STAGES) + STAGES) % STAGES, m0, n0);
+      }
+    }
       for (int s = 0; s < STAGES && s < nk; ++s)
       gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + s * Cfg::STAGE_BYTES, smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES,
                                    &full[s], m0, n0, (kt0 + s) * GEMM_BK);
@@ -183,6 +213,10 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
                                    smem + slot * Cfg::STAGE_BYTES + Cfg::A_BYTES, &full[slot], m0, n0,
                                    (kt0 + i + STAGES) * GEMM_BK);
     }
+    if (kPrefetchC && tid == 0 && i >= nk - Cfg::C_GROUPS) {  // this slot has drained: fill it with C
+      mbar_wait(&empty[slot], par);
+      gemm_issue_c_group<BN>(&tC, smem, cbar, i - (nk - Cfg::C_GROUPS), slot, m0, n0);
+    }
   }
 
   // ------------------------------------------------------------ epilogue
@@ -219,40 +253,32 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
         }
       }
     }
-    } else {  // EPI_SUB_COL: C -= acc, sum of squares of the result
-    // 16 loads of C in flight per thread before the first dependent store (two m8 rows).
+    } else {  // EPI_SUB_COL: C -= acc with C read from the prefetched smem tile, sum of squares
+    mbar_wait(cbar, 0);
     double sq = 0.0;
 #pragma unroll
-    for (int mp = 0; mp < 8; mp += 2) {
-      double cv[2][4][2];
+    for (int mi = 0; mi < 8; ++mi) {
+      const int ml = wm * 64 + mi * 8 + (lane >> 2);
+      const int b = ml >> 4, g = b / Cfg::C_PER_SLOT;
+      const int slot = (((nk - Cfg::C_GROUPS + g) % STAGES) + STAGES) % STAGES;
+      const uint8_t* box = smem + slot * Cfg::STAGE_BYTES + (b - g * Cfg::C_PER_SLOT) * Cfg::C_BOX_BYTES;
+      const int m = m0 + ml;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = mb + (mp + h) * 8;
+      for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int n = nb + ni * 8 + e;
-            cv[h][ni][e] = (m < p.M && n < p.N) ? __ldcg(p.C + m + static_cast<int64_t>(n) * p.ldc) : 0.0;
+        for (int e = 0; e < 2; ++e) {
+          const int nl = wn * 32 + ni * 8 + 2 * (lane & 3) + e;
+          const double c = *reinterpret_cast<const double*>(
+              box + nl * 128 + ((((ml & 15) >> 1) ^ (nl & 7)) << 4) + ((ml & 1) << 3));
+          const int n = n0 + nl;
+          if (m < p.M && n < p.N) {
+            const double v = c - acc[mi][ni][e];
+            __stcg(p.C + m + static_cast<int64_t>(n) * p.ldc, v);
+            sq = fma(v, v, sq);
           }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = mb + (mp + h) * 8;
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int n = nb + ni * 8 + e;
-            if (m < p.M && n < p.N) {
-              const double v = cv[h][ni][e] - acc[mp + h][ni][e];
-              __stcg(p.C + m + static_cast<int64_t>(n) * p.ldc, v);
-              sq = fma(v, v, sq);
-            }
-          }
-      }
+        }
     }
-      if (p.norm_partials != nullptr) {
+    if (p.norm_partials != nullptr) {
       sq = warp_sum(sq);
       if (lane == 0) red[warp] = sq;
       __syncthreads();

@@ -142,7 +142,8 @@ qb_status make_map(qb_ctx ctx, CUtensorMap* map, const double* ptr, uint64_t inn
 
 // ---------------------------------------------------------------- GEMM launcher
 template <int LAYOUT, int BN, int EPI>
-qb_status launch_gemm_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits) {
+qb_status launch_gemm_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                        const GemmParams& p, int splits) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_f64_kernel<LAYOUT, BN, EPI>;
   static bool attr_done = false;
@@ -151,7 +152,7 @@ qb_status launch_gemm_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb
     attr_done = true;
   }
   dim3 grid(p.tiles_m * p.tiles_n, splits);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, p);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tc, p);
   return check_launch(ctx, "gemm_f64");
 }
 
@@ -210,6 +211,8 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   if (splits < 1) splits = 1;
 
   if (epi == EPI_SUB_COL) {
+    CUtensorMap tc;  // the C tile is prefetched by TMA (box {16 m, BN n})
+    QB_TRY(make_map(ctx, &tc, C, M, N, ldc, 16, kBN));
     p.C = C;
     p.ldc = ldc;
     p.split_stride = 0;
@@ -218,19 +221,19 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
       p.norm_partials = ctx->parts.d();
       if (nparts) *nparts = tiles;
     }
-    if (layout == GEMM_NN) return launch_gemm_t<GEMM_NN, kBN, EPI_SUB_COL>(ctx, ta, tb, p, 1);
-    return launch_gemm_t<GEMM_TN, kBN, EPI_SUB_COL>(ctx, ta, tb, p, 1);
+    if (layout == GEMM_NN) return launch_gemm_t<GEMM_NN, kBN, EPI_SUB_COL>(ctx, ta, tb, tc, p, 1);
+    return launch_gemm_t<GEMM_TN, kBN, EPI_SUB_COL>(ctx, ta, tb, tc, p, 1);
   }
 
   if (splits == 1) {
     p.C = C;
     p.ldc = ldc;
     if (layout == GEMM_NN) {
-      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, 1)));
-      else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, 1)));
+      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, 1)));
+      else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, 1)));
     } else {
-      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, 1)));
-      else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, 1)));
+      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, 1)));
+      else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, 1)));
     }
     if (want_norm) {
       // sum of squares of the stored result (rows x cols in "strided-row" form)
@@ -253,11 +256,11 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   p.ldc = ldp;
   p.split_stride = stride;
   if (layout == GEMM_NN) {
-    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, splits)));
-    else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, splits)));
+    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, splits)));
+    else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, splits)));
   } else {
-    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, p, splits)));
-    else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, p, splits)));
+    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, splits)));
+    else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, splits)));
   }
   const int64_t total = rows * cols;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
