@@ -11,9 +11,12 @@ point with the H2D copy of A and the D2H copy of Q, B inside the timed region (`
 The metric is BASELINE.json's: FP64 GFLOP/s of the algorithmic work F_alg (DESIGN.md §8,
 PAPER.md:902 cost model with C_mm = 2) and seconds-to-eps, as a fraction of the FP64 peak.
 
-Multi-GPU (torchrun, N > 1): the column-sharded path is not built yet, so each rank factors
-its own replica ("scaling": "weak", "parallelism": "replicas"); the time is the max over
-ranks and ``value`` counts the work of all ranks.
+Multi-GPU (torchrun, N > 1): the column-sharded path — every rank owns a
+column block of A, Y_i and the norm scalars are summed with NCCL, orth is replicated, B_i and
+the downdate stay local.  Default "weak" scaling: every rank holds a 20000 x 20000 block of
+the 20000 x 20000N matrix with the T spectrum (synth.make_shard_torch), so per-GPU work is
+fixed; ``--strong`` shards the one 20000 x 20000 T matrix instead.  The time is the max over
+ranks; ``value`` is the algorithmic work of the whole (global) factorization per second.
 """
 import argparse
 import json
@@ -171,16 +174,36 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
     import paper_1503_07157_b200 as qbp
+    import synth
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    dspec = None
+    sig = synth.config_sigma(cfg)
     if ws > 1:
+        from paper_1503_07157_b200.dist import dist_spec, shard_columns
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        n_global = cfg.n if args.strong else cfg.n * ws
+        dspec = dist_spec(n_global)
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream(dev)
-    A0 = make_A(cfg, dev)
+    if dspec is None:
+        A0 = make_A(cfg, dev)
+        n_global, n_local = cfg.n, cfg.n
+    elif args.strong:
+        Af = make_A(cfg, dev)
+        off, n_local = dspec["col_offset"], dspec["n_local"]
+        A0 = Af.t()[off:off + n_local].contiguous().t()
+        del Af
+        n_global = cfg.n
+    else:
+        n_local = cfg.n
+        n_global = cfg.n * ws
+        dspec["col_offset"], dspec["n_local"] = rank * n_local, n_local
+        A0 = synth.make_shard_torch(cfg.m, n_local, sig, cfg.seed_matrix, rank, ws, device=dev)
     torch.cuda.synchronize()
-    ctx = qbp.QB(local, stream=ctypes_stream(stream))
+    ctx = qbp.QB(local, stream=ctypes_stream(stream), dist=dspec)
+    m, b, q = cfg.m, cfg.b, cfg.q
 
     def step():
         return ctx.factor(A0, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=False)
@@ -211,15 +234,14 @@ def run_ours(args, cfg):
         ms = float(t.item())
         dist.barrier()
     k, stats = g["k"], g["stats"]
-    m, n, b, q = cfg.m, cfg.n, cfg.b, cfg.q
-    F = falg(m, n, k, b, q, len(stats))
-    value = ws * F / (ms * 1e-3) * 1e-9
+    F = falg(m, n_global, k, b, q, len(stats))
+    value = F / (ms * 1e-3) * 1e-9
     peak, peak_src, cublas = fp64_peak()
 
     # roofline of the dominant kernel: the downdate GEMM A -= Q_i B_i (fused norm epilogue)
     full = [s for s in stats if s["w"] == b]
     t_down = statistics.mean(s["ms_down"] for s in full) * 1e-3
-    achieved = 2.0 * m * n * b / t_down * 1e-12
+    achieved = 2.0 * m * n_local * b / t_down * 1e-12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
     if os.path.exists(prof):
@@ -230,19 +252,19 @@ def run_ours(args, cfg):
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "gemm_f64_kernel<NN,64,SUB_COL> (A -= Q_i B_i, fused ||A||_F^2)",
                 "peak_source": peak_src,
-                "algorithmic_per_launch": f"2*m*n*b = {2.0 * m * n * b:.4g} flop",
+                "algorithmic_per_launch": f"2*m*n_local*b = {2.0 * m * n_local * b:.4g} flop",
                 "share_of_step": sum(s["ms_down"] for s in stats) / ms}
 
     # end to end through the host-buffer entry point: H2D of A, D2H of Q and B per step
     e2e = None
     if not args.no_e2e:
-        A_h = torch.empty((n, m), dtype=torch.float64, pin_memory=True).t()   # column-major host A
+        A_h = torch.empty((n_local, m), dtype=torch.float64, pin_memory=True).t()   # column-major host A
         A_h.copy_(A0)
         kcap = k + b
         Q_h = torch.empty((kcap, m), dtype=torch.float64, pin_memory=True)
-        B_h = torch.empty((kcap, n), dtype=torch.float64, pin_memory=True)
-        res = qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n, m, cfg.eps, b, q, cfg.seed_omega, 0,
-                                 Q_h.data_ptr(), m, B_h.data_ptr(), n, kcap)
+        B_h = torch.empty((kcap, n_local), dtype=torch.float64, pin_memory=True)
+        res = qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n_local, m, cfg.eps, b, q, cfg.seed_omega, 0,
+                                 Q_h.data_ptr(), m, B_h.data_ptr(), n_local, kcap)
         torch.cuda.synchronize()
         esteps = max(1, min(args.steps, 3))
         if ws > 1:
@@ -250,8 +272,8 @@ def run_ours(args, cfg):
         t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(esteps):
-            res = qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n, m, cfg.eps, b, q, cfg.seed_omega, 0,
-                                     Q_h.data_ptr(), m, B_h.data_ptr(), n, kcap)
+            res = qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n_local, m, cfg.eps, b, q, cfg.seed_omega, 0,
+                                     Q_h.data_ptr(), m, B_h.data_ptr(), n_local, kcap)
         e1.record(stream)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) / esteps * 1e3
@@ -261,9 +283,10 @@ def run_ours(args, cfg):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         ke = res["k"]
-        e2e = {"value": ws * falg(m, n, ke, b, q, -(-ke // b)) / (ems * 1e-3) * 1e-9, "unit": "GFLOP/s",
-               "ms_per_step": ems, "h2d_bytes_per_step": m * n * 8, "d2h_bytes_per_step": ke * (m + n) * 8 + 16,
-               "entry_point": "qb_factor_host (pinned host A, Q, B)"}
+        e2e = {"value": falg(m, n_global, ke, b, q, -(-ke // b)) / (ems * 1e-3) * 1e-9, "unit": "GFLOP/s",
+               "ms_per_step": ems, "h2d_bytes_per_step": ws * m * n_local * 8,
+               "d2h_bytes_per_step": ws * ke * (m + n_local) * 8 + 16,
+               "entry_point": "qb_factor_host (pinned host A, Q, B; every rank its column block)"}
         del A_h, Q_h, B_h
 
     cpu = None
@@ -276,11 +299,15 @@ def run_ours(args, cfg):
         del A_np
 
     if rank == 0:
+        scaling = "strong" if (ws > 1 and args.strong) else "weak"
+        par = "single" if ws == 1 else f"column-sharded x{ws} (NCCL allreduce of Y_i, Gram, norms)"
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload_desc(cfg), "m": m, "n": n, "b": b, "q": q, "eps": cfg.eps,
-                           "k": k, "blocks": len(stats), "parallelism": "replicas" if ws > 1 else "single",
+                "config": {"workload": workload_desc(cfg) + ("" if ws == 1 else
+                           f"; {'one matrix sharded' if args.strong else 'weak: m x %d global' % n_global}"),
+                           "m": m, "n": n_global, "n_per_gpu": n_local, "b": b, "q": q, "eps": cfg.eps,
+                           "k": k, "blocks": len(stats), "parallelism": par,
                            "l2": "inputs larger than L2 (A is 3.2 GB; every step reads it >= 3 times)"},
                 "seconds_to_eps": ms * 1e-3, "frac_fp64_peak": value / ws / (peak * 1e3),
                 "frac_cublas_dgemm": (value / ws / (cublas * 1e3)) if cublas else None,
@@ -308,6 +335,7 @@ def main():
     ap.add_argument("--cpu-sample-blocks", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--strong", action="store_true", help="N > 1: shard one matrix (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -120,6 +120,28 @@ def qb_create(device=0, dtype=QB_F64, stream=None):
     return ctx
 
 
+def qb_nccl_unique_id():
+    """128-byte ncclUniqueId (bytes) for qb_create_dist; rank 0 creates it, all ranks share it."""
+    buf = ctypes.create_string_buffer(128)
+    s = lib().qb_nccl_unique_id(buf)
+    if s != QB_OK:
+        raise QBError(s, "qb_nccl_unique_id failed (is libnccl.so.2 loadable?)")
+    return buf.raw
+
+
+def qb_create_dist(device, rank, nranks, unique_id, col_offset, n_global, dtype=QB_F64, stream=None):
+    ctx = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+    s = lib().qb_create_dist(ctypes.byref(ctx), int(device), int(dtype), stream, int(rank), int(nranks), uid,
+                             int(col_offset), int(n_global))
+    if s != QB_OK:
+        msg = qb_last_error(ctx) if ctx.value else ""
+        if ctx.value:
+            lib().qb_destroy(ctx)
+        raise QBError(s, msg)
+    return ctx
+
+
 def qb_destroy(ctx):
     if ctx is not None and ctx.value:
         lib().qb_destroy(ctx)
@@ -215,14 +237,20 @@ class QB:
     ``factor(A, eps, b, q, seed)`` with A a CUDA float64 tensor whose columns are contiguous
     (``A.stride(0) == 1``)."""
 
-    def __init__(self, device=0, dtype=QB_F64, stream=None):
+    def __init__(self, device=0, dtype=QB_F64, stream=None, dist=None):
+        """dist: None, or dict(rank, nranks, unique_id, col_offset, n_global) for a
+        column-sharded context (see paper_1503_07157_b200.dist)."""
         # Default to torch's current stream on `device` so that the library's kernels are
         # stream-ordered after the torch work that produced their inputs.
         if stream is None:
             import torch
             h = torch.cuda.current_stream(device).cuda_stream
             stream = ctypes.c_void_p(h if h else 1)   # 0 (torch's default) -> cudaStreamLegacy
-        self.ctx = qb_create(device, dtype, stream)
+        if dist is None:
+            self.ctx = qb_create(device, dtype, stream)
+        else:
+            self.ctx = qb_create_dist(device, dist["rank"], dist["nranks"], dist["unique_id"], dist["col_offset"],
+                                      dist["n_global"], dtype, stream)
 
     def close(self):
         qb_destroy(self.ctx)

@@ -14,9 +14,12 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nccl.h>  // types only: NCCL is loaded at run time (dlopen), never linked
 
 #include "../../include/qb.h"
 #include "common.cuh"
@@ -38,6 +41,38 @@ struct DevBuf {
   double* d() const { return static_cast<double*>(p); }
 };
 
+// ---------------------------------------------------------------- NCCL (dlopen)
+// The multi-GPU path (column sharding) needs ncclAllReduce only.  NCCL is
+// resolved at run time from the process (torch's bundled libnccl.so.2 when torch is loaded)
+// or the system, so the library itself has no link-time NCCL dependency.
+struct NcclApi {
+  bool tried = false, ok = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  const char* env = getenv("QB_NCCL_LIB");
+  void* h = nullptr;
+  if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.getUniqueId = reinterpret_cast<decltype(&ncclGetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  api.commInitRank = reinterpret_cast<decltype(&ncclCommInitRank)>(dlsym(h, "ncclCommInitRank"));
+  api.commDestroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(h, "ncclCommDestroy"));
+  api.allReduce = reinterpret_cast<decltype(&ncclAllReduce)>(dlsym(h, "ncclAllReduce"));
+  api.errorString = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
+  api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.errorString;
+  return api;
+}
+
 }  // namespace
 
 struct qb_ctx_s {
@@ -54,6 +89,7 @@ struct qb_ctx_s {
   // distributed (column sharding); nranks == 1 on a plain context
   int rank = 0, nranks = 1;
   int64_t col_offset = 0, n_global = 0;
+  ncclComm_t comm = nullptr;  // set on distributed contexts (any nranks >= 1)
 
   DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status;
   int64_t kcap = 0, ldq = 0, ldb = 0, qbar_rows = 0, bbar_cols = 0;
@@ -120,6 +156,15 @@ qb_status check_launch(qb_ctx ctx, const char* what) {
     e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return fail(ctx, QB_ERR_CUDA, "after %s: %s", what, cudaGetErrorString(e));
   }
+  return QB_OK;
+}
+
+// Sum `count` doubles across the ranks of a distributed context, in place on the context
+// stream (no-op on a plain context).
+qb_status allreduce_sum(qb_ctx ctx, double* buf, size_t count) {
+  if (!ctx->comm || count == 0) return QB_OK;
+  ncclResult_t r = nccl().allReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) return fail(ctx, QB_ERR_NCCL, "ncclAllReduce: %s", nccl().errorString(r));
   return QB_OK;
 }
 
@@ -305,10 +350,11 @@ qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) 
 
 // One CholeskyQR pass: dst = src T, with T from chol_inv (all on the device; gated).
 qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
-                      const int* gate) {
+                      const int* gate, bool row_distributed) {
   const int64_t ldgb = round_up(kMaxB, 16);
   QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr, true,
               gate));
+  if (row_distributed) QB_TRY(allreduce_sum(ctx, ctx->G.d(), (size_t)(ldgb * w)));  // G = sum_p src_p^T src_p
   QB_TRY(chol_inv(ctx, w, m, true, gate));
   return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr, true,
               gate);
@@ -319,14 +365,18 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
 // R8) triggers two more passes (shifted CholeskyQR3), gated on the device flag status[1].
 // src and dst may alias; ctx->T1 is the scratch.  Nothing here synchronises with the host;
 // failures surface in status[3], read at the end of the block.
-qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w) {
+// row_distributed: src holds this rank's rows of a matrix whose rows are spread over the
+// ranks (the power step's Z = A^T Q on column shards); the Gram is summed with NCCL and the
+// replicated T applied to the local rows.
+qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
+                  bool row_distributed = false) {
   const int64_t ldt = round_up(m, 16);
   double* T = ctx->T1.d();
   QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, sizeof(int), ctx->stream));
-  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr));
-  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, nullptr));
-  QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1));
-  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1));
+  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr, row_distributed));
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, nullptr, row_distributed));
+  QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed));
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed));
   return QB_OK;
 }
 
@@ -451,23 +501,34 @@ qb_status qb_create(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream) 
 }
 
 qb_status qb_nccl_unique_id(void* out128) {
-  (void)out128;
-  return QB_ERR_NCCL;
+  if (!out128) return QB_ERR_INVALID_ARG;
+  if (!nccl().ok) return QB_ERR_NCCL;
+  ncclUniqueId id;
+  if (nccl().getUniqueId(&id) != ncclSuccess) return QB_ERR_NCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return QB_OK;
 }
 
 qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, int rank, int nranks,
                          const void* nccl_unique_id, int64_t col_offset, int64_t n_global) {
-  (void)nccl_unique_id;
   qb_status s = qb_create(out, device, dtype, cuda_stream);
   if (s != QB_OK) return s;
   qb_ctx ctx = *out;
-  if (nranks < 1 || rank < 0 || rank >= nranks || col_offset < 0 || n_global < 1)
+  if (nranks < 1 || rank < 0 || rank >= nranks || col_offset < 0 || n_global < 1 || !nccl_unique_id)
     return fail(ctx, QB_ERR_INVALID_ARG, "bad distributed arguments");
   ctx->rank = rank;
   ctx->nranks = nranks;
   ctx->col_offset = col_offset;
   ctx->n_global = n_global;
-  if (nranks > 1) return fail(ctx, QB_ERR_NCCL, "NCCL transport not built in this library version");
+  if (!nccl().ok) return fail(ctx, QB_ERR_NCCL, "libnccl.so.2 not found (set QB_NCCL_LIB)");
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  QB_CUDA(cudaSetDevice(device));
+  ncclResult_t r = nccl().commInitRank(&ctx->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    ctx->comm = nullptr;
+    return fail(ctx, QB_ERR_NCCL, "ncclCommInitRank: %s", nccl().errorString(r));
+  }
   return QB_OK;
 }
 
@@ -485,6 +546,7 @@ void qb_destroy(qb_ctx ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   for (auto& e : ctx->evp)
     if (e) cudaEventDestroy(e);
+  if (ctx->comm) nccl().commDestroy(ctx->comm);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -641,6 +703,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     sumsq_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(A, m, n, ldA, ctx->parts.d());
     QB_TRY(check_launch(ctx, "sumsq"));
     QB_TRY(reduce_to_scal(ctx, grid, 0));
+    QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 1));  // ||A||_F^2 over the column shards
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
@@ -676,13 +739,14 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
     QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Om.d(), bp, ctx->Y.d(), ldm, false,
                 nullptr));
+    QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));  // Y = sum_p A_p Omega_p (column shards)
     QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
     QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     for (int j = 0; j < q; ++j) {
       QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, Qi, ctx->ldq, ctx->Z.d(), ldn, false,
                   nullptr));
-      QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w));
+      QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, ctx->comm != nullptr));
       {
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w + 31) / 32));
         transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w, ctx->Zt.d(), bp);
@@ -690,6 +754,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       }
       QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Zt.d(), bp, ctx->Y.d(), ldm,
                   false, nullptr));
+      QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
       QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
@@ -715,6 +780,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
                 &na_parts));
     QB_CUDA(cudaEventRecord(ctx->evp[5], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
+    QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 2));  // ||A^(i)||_F^2 and ||B_i||_F^2 over the shards
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));

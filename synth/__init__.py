@@ -109,6 +109,28 @@ def make_matrix_torch(m, n, sig, seed, device="cuda", dtype=None):
     return At.to(dtype).t()
 
 
+def make_shard_torch(m, n_local, sig, seed, rank, nranks, device="cuda", dtype=None):
+    """Column block `rank` of the m x (nranks * n_local) matrix
+    A = U diag(σ) [V_0; ...; V_{P-1}]^T / sqrt(P), each V_p an n_local x r orthonormal factor.
+    The stacked right factor has orthonormal columns (sum_p V_p^T V_p / P = I), so A has
+    exactly the singular values σ for every P, and rank 0 of P = 1 is make_matrix_torch.
+    Used for weak scaling: every rank holds an m x n_local block."""
+    import torch
+    dtype = dtype or torch.float64
+    r = len(sig)
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    s = torch.as_tensor(np.asarray(sig), dtype=torch.float64, device=device) / np.sqrt(nranks)
+    U, _ = torch.linalg.qr(torch.randn(m, r, generator=g, dtype=torch.float64, device=device))
+    if rank > 0:
+        g = torch.Generator(device=device)
+        g.manual_seed(int(seed) * 1000003 + int(rank))
+    V, _ = torch.linalg.qr(torch.randn(n_local, r, generator=g, dtype=torch.float64, device=device))
+    At = (V * s[None, :]) @ U.T
+    del U, V
+    return At.to(dtype).t()
+
+
 def config_sigma(cfg):
     return sigma(cfg.spectrum, cfg.rank)
 

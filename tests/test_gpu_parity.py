@@ -256,3 +256,22 @@ def test_fresh_context_reproducible_across_growth(qbmod):
     assert g1["k"] == g2["k"] and g1["k"] > 1024
     assert torch.equal(g1["Q"], g2["Q"]) and torch.equal(g1["B"], g2["B"])
     assert [s["r2"] for s in g1["stats"]] == [s["r2"] for s in g2["stats"]]
+
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_distributed_context_single_rank_bitwise(qbmod, q):
+    """A column-sharded context (NCCL communicator of one rank) runs the allreduce code path
+    and must reproduce the plain context bit for bit."""
+    try:
+        uid = qbmod.qb_nccl_unique_id()
+    except qbmod.QBError:
+        pytest.skip("NCCL not loadable")
+    A, _ = make(600, 500, "exp10_25", 9)
+    plain = qbmod.QB(0)
+    g0 = plain.factor(to_dev(A), 1e-8, 32, q, seed=4)
+    plain.close()
+    d = qbmod.QB(0, dist=dict(rank=0, nranks=1, unique_id=uid, col_offset=0, n_global=500))
+    g1 = d.factor(to_dev(A), 1e-8, 32, q, seed=4)
+    d.close()
+    assert g0["k"] == g1["k"]
+    assert torch.equal(g0["Q"], g1["Q"]) and torch.equal(g0["B"], g1["B"])
