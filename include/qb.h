@@ -17,7 +17,10 @@
  *   B_i = Q_i^* A;  A = A - Q_i B_i;  stop once ||A||_F <= eps   (R1, R4)
  *
  * Conventions for every entry point:
- *   - All matrices are dense, FP64 (QB_F64) or FP32 (QB_F32) as chosen at qb_create.
+ *   - All matrices are dense, FP64 (QB_F64) or FP32 (QB_F32) as chosen at qb_create.  An FP32
+ *     context takes float A and returns float Q, B; in this build its arithmetic is FP64 on the
+ *     exactly widened input with Omega = RN32(Omega), so its results meet the
+ *     FP64 tolerances; qb_orth / qb_gemm are FP64-only.
  *   - "device" pointers are CUDA device pointers on the context's device; the caller owns
  *     everything it passes in; the context owns everything it hands out.
  *   - Column-major means element (i, j) at ptr[i + j*ld]; row-major means ptr[i*ld + j].

@@ -264,13 +264,14 @@ class QB:
 
     def factor(self, A, eps, b, q=0, seed=1, kmax=0, overwrite=False, copy_out=True):
         import torch
-        assert A.is_cuda and A.dtype == torch.float64 and A.dim() == 2 and A.stride(0) == 1
+        assert A.is_cuda and A.dtype in (torch.float64, torch.float32) and A.dim() == 2 and A.stride(0) == 1
         m, n = A.shape
         r = qb_factor(self.ctx, A.data_ptr(), m, n, A.stride(1) if n > 1 else m, eps, b, q, seed, kmax,
                       QB_OVERWRITE_A if overwrite else 0)
         k = r["k"]
-        Q = view_colmajor(r["Q"], m, k, r["ldq"]) if k > 0 else torch.zeros(m, 0, dtype=A.dtype, device=A.device)
-        B = view_rowmajor(r["B"], k, n, r["ldb"]) if k > 0 else torch.zeros(0, n, dtype=A.dtype, device=A.device)
+        ts = "<f8" if A.dtype == torch.float64 else "<f4"
+        Q = view_colmajor(r["Q"], m, k, r["ldq"], ts) if k > 0 else torch.zeros(m, 0, dtype=A.dtype, device=A.device)
+        B = view_rowmajor(r["B"], k, n, r["ldb"], ts) if k > 0 else torch.zeros(0, n, dtype=A.dtype, device=A.device)
         if copy_out:
             Q, B = Q.clone(), B.clone()
         return dict(status=r["status"], k=k, Q=Q, B=B, resid=r["resid"], stats=qb_stats(self.ctx))

@@ -100,7 +100,9 @@ __device__ __forceinline__ void gaussian_pair(uint64_t seed, uint64_t p, uint64_
 }
 
 // out[(r - row0)*ldo + (c - col0)] = Ω(r, c) for r in [row0, row1), c in [col0, col0 + w).
-template <typename T>
+// T = double with Round32 = true stores RN_32(Ω) widened back to FP64 (the FP32 path's Ω,
+// DESIGN.md §3.3 rule 7, for FP64 arithmetic on FP32 data).
+template <typename T, bool Round32 = false>
 __global__ void __launch_bounds__(256) omega_kernel(uint64_t seed, int64_t row0, int64_t row1, int64_t col0,
                                                     int64_t w, T* __restrict__ out, int64_t ldo,
                                                     const OmegaConsts K) {
@@ -113,6 +115,10 @@ __global__ void __launch_bounds__(256) omega_kernel(uint64_t seed, int64_t row0,
     const int64_t p = p0 + pi;
     double ev, od;
     gaussian_pair(seed, static_cast<uint64_t>(p), static_cast<uint64_t>(col0 + ci), K, ev, od);
+    if (Round32) {
+      ev = static_cast<double>(static_cast<float>(ev));
+      od = static_cast<double>(static_cast<float>(od));
+    }
     const int64_t r_even = 2 * p, r_odd = 2 * p + 1;
     if (r_even >= row0 && r_even < row1) out[(r_even - row0) * ldo + ci] = static_cast<T>(ev);
     if (r_odd >= row0 && r_odd < row1) out[(r_odd - row0) * ldo + ci] = static_cast<T>(od);

@@ -91,7 +91,7 @@ struct qb_ctx_s {
   int64_t col_offset = 0, n_global = 0;
   ncclComm_t comm = nullptr;  // set on distributed contexts (any nranks >= 1)
 
-  DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status;
+  DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status, Qf, Bf, Ain32;
   int64_t kcap = 0, ldq = 0, ldb = 0, qbar_rows = 0, bbar_cols = 0;
   double* h_scal = nullptr;  // pinned: [0] r2, [1] sum B^2, [2..3] spare
   int* h_status = nullptr;   // pinned
@@ -385,18 +385,31 @@ qb_status reset_flags(qb_ctx ctx) {
   return QB_OK;
 }
 
+// kind 0: FP64 Ω; 1: FP32 Ω (qb_omega on an FP32 context); 2: FP64 buffer holding RN_32(Ω).
 qb_status launch_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_t col0, int64_t w, void* out,
-                       int64_t ldo) {
+                       int64_t ldo, int kind) {
   const int64_t npairs = ((row1 - 1) >> 1) - (row0 >> 1) + 1;
   const int64_t total = npairs * w;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 32 * ctx->num_sms));
-  if (ctx->dtype == QB_F64)
+  if (kind == 0)
     omega_kernel<double><<<grid, 256, 0, ctx->stream>>>(seed, row0, row1, col0, w, static_cast<double*>(out), ldo,
                                                         ctx->omega_consts);
-  else
+  else if (kind == 1)
     omega_kernel<float><<<grid, 256, 0, ctx->stream>>>(seed, row0, row1, col0, w, static_cast<float*>(out), ldo,
                                                        ctx->omega_consts);
+  else
+    omega_kernel<double, true><<<grid, 256, 0, ctx->stream>>>(seed, row0, row1, col0, w, static_cast<double*>(out),
+                                                              ldo, ctx->omega_consts);
   return check_launch(ctx, "omega");
+}
+
+template <typename Tin, typename Tout>
+qb_status launch_convert(qb_ctx ctx, const Tin* in, int64_t ldi, int64_t rows, int64_t cols, Tout* out, int64_t ldo) {
+  if (rows <= 0 || cols <= 0) return QB_OK;
+  const int64_t total = rows * cols;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16 * ctx->num_sms));
+  convert_kernel<Tin, Tout><<<grid, 256, 0, ctx->stream>>>(in, ldi, rows, cols, out, ldo);
+  return check_launch(ctx, "convert");
 }
 
 qb_status grow_factors(qb_ctx ctx, int64_t m, int64_t n, int64_t need, int64_t kmax) {
@@ -465,6 +478,28 @@ qb_status init_ctx(qb_ctx ctx, int device, qb_dtype dtype, void* stream) {
   QB_CUDA(cudaEventCreate(&ctx->ev0));
   QB_CUDA(cudaEventCreate(&ctx->ev1));
   for (auto& e : ctx->evp) QB_CUDA(cudaEventCreate(&e));
+  return QB_OK;
+}
+
+// Hand out Q̄ (column-major, ld ldq) and B̄ (row-major, ld ldb): the FP64 factors, or for an
+// FP32 context their RN_32 copies in context-owned FP32 buffers with the same layouts.
+qb_status publish_outputs(qb_ctx ctx, int64_t m, int64_t n, int64_t k, const void** Q_out, int64_t* ldq_out,
+                          const void** B_out, int64_t* ldb_out) {
+  const void* Qp = ctx->Qbar.p;
+  const void* Bp = ctx->Bbar.p;
+  if (ctx->dtype == QB_F32) {
+    QB_TRY(ensure(ctx, ctx->Qf, sizeof(float) * (size_t)(ctx->ldq * std::max<int64_t>(k, 1))));
+    QB_TRY(ensure(ctx, ctx->Bf, sizeof(float) * (size_t)(ctx->ldb * std::max<int64_t>(k, 1))));
+    QB_TRY(launch_convert(ctx, ctx->Qbar.d(), ctx->ldq, m, k, static_cast<float*>(ctx->Qf.p), ctx->ldq));
+    QB_TRY(launch_convert(ctx, ctx->Bbar.d(), ctx->ldb, n, k, static_cast<float*>(ctx->Bf.p), ctx->ldb));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    Qp = ctx->Qf.p;
+    Bp = ctx->Bf.p;
+  }
+  if (Q_out) *Q_out = Qp;
+  if (ldq_out) *ldq_out = ctx->ldq;
+  if (B_out) *B_out = Bp;
+  if (ldb_out) *ldb_out = ctx->ldb;
   return QB_OK;
 }
 
@@ -537,7 +572,8 @@ void qb_destroy(qb_ctx ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->Awork, &ctx->Qbar, &ctx->Bbar, &ctx->Om, &ctx->Y,     &ctx->T1,    &ctx->Z,   &ctx->Zt,
-                    &ctx->G,     &ctx->L,    &ctx->Rinv, &ctx->W,  &ctx->P,     &ctx->parts, &ctx->scal, &ctx->status};
+                    &ctx->G,     &ctx->L,    &ctx->Rinv, &ctx->W,  &ctx->P,     &ctx->parts, &ctx->scal, &ctx->status,
+                    &ctx->Qf,    &ctx->Bf,   &ctx->Ain32};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -566,7 +602,7 @@ qb_status qb_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_
     return fail(ctx, QB_ERR_INVALID_ARG, "qb_omega: bad arguments");
   if (row1 == row0 || w == 0) return QB_OK;
   QB_CUDA(cudaSetDevice(ctx->device));
-  return launch_omega(ctx, seed, row0, row1, col0, w, out, ldo);
+  return launch_omega(ctx, seed, row0, row1, col0, w, out, ldo, ctx->dtype == QB_F64 ? 0 : 1);
 }
 
 qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
@@ -657,7 +693,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   ctx->stats.clear();
   if (!k_out) return fail(ctx, QB_ERR_INVALID_ARG, "k must not be NULL");
   *k_out = 0;
-  if (ctx->dtype != QB_F64) return fail(ctx, QB_ERR_UNSUPPORTED, "the FP32 path is not built yet");
+  const bool is_f32 = ctx->dtype == QB_F32;
   if (!Ain || m < 1 || n < 1 || lda < m || m > INT32_MAX || n > INT32_MAX)
     return fail(ctx, QB_ERR_INVALID_ARG, "bad matrix arguments (m=%lld n=%lld lda=%lld)", (long long)m, (long long)n,
                 (long long)lda);
@@ -669,10 +705,18 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   QB_CUDA(cudaSetDevice(ctx->device));
 
   // ---- residual workspace A^(0) = A (A^(j) overwrites A^(j-1), :112)
+  // FP32 contexts ("FP32 path"): A is widened once into the FP64 residual
+  // workspace (exact), the loop runs in FP64 with Ω = RN_32(Ω), and Q, B are rounded to FP32.
   double* A = static_cast<double*>(Ain);
   int64_t ldA = lda;
-  const bool inplace_ok = (flags & QB_OVERWRITE_A) && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(Ain) & 15) == 0);
-  if (!inplace_ok) {
+  const bool inplace_ok = !is_f32 && (flags & QB_OVERWRITE_A) && (lda % 2 == 0) &&
+                          ((reinterpret_cast<uintptr_t>(Ain) & 15) == 0);
+  if (is_f32) {
+    ldA = round_up(m, 16);
+    QB_TRY(ensure(ctx, ctx->Awork, sizeof(double) * (size_t)(ldA * n)));
+    QB_TRY(launch_convert(ctx, static_cast<const float*>(Ain), lda, m, n, ctx->Awork.d(), ldA));
+    A = ctx->Awork.d();
+  } else if (!inplace_ok) {
     ldA = round_up(m, 16);
     QB_TRY(ensure(ctx, ctx->Awork, sizeof(double) * (size_t)(ldA * n)));
     QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * 8, Ain, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -716,11 +760,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   if (resid_out) *resid_out = std::sqrt(r2_0);
   if (r2_0 <= eps2) {
     QB_TRY(grow_factors(ctx, m, n, 1, std::max<int64_t>(kmax_eff, 1)));
-    if (Q_out) *Q_out = ctx->Qbar.p;
-    if (ldq_out) *ldq_out = ctx->ldq;
-    if (B_out) *B_out = ctx->Bbar.p;
-    if (ldb_out) *ldb_out = ctx->ldb;
-    return QB_OK;
+    return publish_outputs(ctx, m, n, 0, Q_out, ldq_out, B_out, ldb_out);
   }
 
   int64_t ell = 0;
@@ -735,7 +775,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
 
     // line (2): Ω_i = randn(n, w), global columns ell .. ell+w-1, row-major (ld bp)
     QB_CUDA(cudaEventRecord(ctx->evp[0], ctx->stream));
-    QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp));
+    QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp, is_f32 ? 2 : 0));
     // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
     QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Om.d(), bp, ctx->Y.d(), ldm, false,
                 nullptr));
@@ -812,10 +852,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     if (r2 <= eps2) break;  // line (11): stop test (R1, R4)
   }
   *k_out = ell;
-  if (Q_out) *Q_out = ctx->Qbar.p;
-  if (ldq_out) *ldq_out = ctx->ldq;
-  if (B_out) *B_out = ctx->Bbar.p;
-  if (ldb_out) *ldb_out = ctx->ldb;
+  QB_TRY(publish_outputs(ctx, m, n, ell, Q_out, ldq_out, B_out, ldb_out));
   if (resid_out) *resid_out = std::sqrt(r2);
   return r2 <= eps2 ? QB_OK : QB_NOT_CONVERGED;
 }
@@ -828,19 +865,20 @@ qb_status qb_factor_host(qb_ctx ctx, const void* A_host, int64_t m, int64_t n, i
       (Q_host && ldq_host < m) || (B_host && ldb_host < n))
     return fail(ctx, QB_ERR_INVALID_ARG, "qb_factor_host: bad arguments");
   QB_CUDA(cudaSetDevice(ctx->device));
+  const int64_t es = ctx->dtype == QB_F64 ? 8 : 4;
   const int64_t ldA = round_up(m, 16);
-  QB_TRY(ensure(ctx, ctx->Awork, sizeof(double) * (size_t)(ldA * n)));
-  QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * 8, A_host, lda_host * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream));
+  DevBuf& dst = ctx->dtype == QB_F64 ? ctx->Awork : ctx->Ain32;  // FP32 input is widened by qb_factor
+  QB_TRY(ensure(ctx, dst, (size_t)(es * ldA * n)));
+  QB_CUDA(cudaMemcpy2DAsync(dst.p, ldA * es, A_host, lda_host * es, m * es, n, cudaMemcpyHostToDevice, ctx->stream));
   const void* Qd = nullptr;
   const void* Bd = nullptr;
   int64_t ldq = 0, ldb = 0;
-  qb_status s = qb_factor(ctx, ctx->Awork.p, m, n, ldA, eps, b, q, seed, kmax, QB_OVERWRITE_A, k, &Qd, &ldq, &Bd,
-                          &ldb, resid);
+  qb_status s = qb_factor(ctx, dst.p, m, n, ldA, eps, b, q, seed, kmax, QB_OVERWRITE_A, k, &Qd, &ldq, &Bd, &ldb, resid);
   if (s != QB_OK && s != QB_NOT_CONVERGED) return s;
   const int64_t kc = std::min(*k, kcap_host);
   if (kc > 0) {
-    QB_CUDA(cudaMemcpy2DAsync(Q_host, ldq_host * 8, Qd, ldq * 8, m * 8, kc, cudaMemcpyDeviceToHost, ctx->stream));
-    QB_CUDA(cudaMemcpy2DAsync(B_host, ldb_host * 8, Bd, ldb * 8, n * 8, kc, cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaMemcpy2DAsync(Q_host, ldq_host * es, Qd, ldq * es, m * es, kc, cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaMemcpy2DAsync(B_host, ldb_host * es, Bd, ldb * es, n * es, kc, cudaMemcpyDeviceToHost, ctx->stream));
   }
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
   return s;

@@ -97,6 +97,19 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
   }
 }
 
+// out[r + c*ldo] = (Tout) in[r + c*ldi], column-major rows x cols (FP32 <-> FP64 staging of
+// the FP32 path).
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in, int64_t ldi, int64_t rows,
+                                                      int64_t cols, Tout* __restrict__ out, int64_t ldo) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = idx / rows, r = idx - c * rows;
+    out[r + c * ldo] = static_cast<Tout>(in[r + c * ldi]);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K4 core, step 1 — chol_kernel: one CTA, w <= CHOL_MAXW.  Given the w x w Gram matrix
 // G = X^T X (column-major), produce T (row-major, in `Rinv`) such that X T is orthonormal:

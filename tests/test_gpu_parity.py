@@ -275,3 +275,27 @@ def test_distributed_context_single_rank_bitwise(qbmod, q):
     d.close()
     assert g0["k"] == g1["k"]
     assert torch.equal(g0["Q"], g1["Q"]) and torch.equal(g0["B"], g1["B"])
+
+
+@pytest.mark.parametrize("case", [(400, 300, "exp10_20", 1e-4, 10, 0), (3000, 200, "exp_100", 1e-3, 32, 0),
+                                  (1000, 260, "poly2", 1e-4, 64, 1)])
+def test_fp32_path_parity(qbmod, case):
+    """FP32 path (BASELINE configs[3] family): float A in, float Q, B out.  The oracle runs in
+    FP64 on the same FP32 input with Ω = RN_32(Ω) (reading R18); north_star FP32 tolerances
+    1e-5 (orthogonality) and 1e-4 (QB parity)."""
+    m, n, kind, eps, b, q = case
+    A64, _ = make(m, n, kind, 31 + m)
+    A32 = A64.astype(np.float32)
+    Aw = A32.astype(np.float64)
+    o = oqb.randqb_pb(Aw, eps, b, q, seed=2, omega_dtype=np.float32)
+    c = qbmod.QB(0, dtype=qbmod.QB_F32)
+    g = c.factor(torch.from_numpy(np.asfortranarray(A32)).cuda(), eps, b, q, seed=2)
+    c.close()
+    assert g["Q"].dtype == torch.float32 and g["B"].dtype == torch.float32
+    assert g["k"] == o.k
+    Qg = g["Q"].double().cpu().numpy()
+    Bg = g["B"].double().cpu().numpy()
+    nA = np.linalg.norm(Aw)
+    assert np.abs(Qg.T @ Qg - np.eye(g["k"])).max() <= 1e-5
+    assert np.linalg.norm(np.hstack([Qg, o.Q]) @ np.vstack([Bg, -o.B])) / nA <= 1e-4
+    assert np.linalg.norm(Aw - Qg @ Bg) <= eps * (1 + 1e-4) + 1e-6 * nA
