@@ -136,6 +136,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
   if (tid == 0) {
     if (kPrefetchC) {
       tma_prefetch_desc(&tC);
+      // pull the C tile towards L2 now; the shared-memory copy is taken when slots drain
+      for (int b = 0; b < GEMM_BM / 16; ++b) tma_prefetch_l2_2d(&tC, m0 + 16 * b, n0);
       mbar_arrive_expect_tx(cbar, (GEMM_BM / 16) * Cfg::C_BOX_BYTES);
       // groups whose slot no k-tile ever uses go out right away
       for (int g = 0; g < Cfg::C_GROUPS; ++g) {
