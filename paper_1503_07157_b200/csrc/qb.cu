@@ -333,19 +333,13 @@ int* status_dev(qb_ctx ctx) { return static_cast<int*>(ctx->status.p); }
 qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) {
   static bool attr_done = false;
   if (!attr_done) {
-    QB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CHOL_SMEM));
-    QB_CUDA(cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRINV_SMEM));
+    QB_CUDA(cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CHOL_SMEM));
     attr_done = true;
   }
   const int64_t ld = round_up(kMaxB, 16);
-  double* Dinv = ctx->L.d() + ld * ld;
-  chol_kernel<<<1, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(ctx->G.d(), ld, w, m_rows, ctx->L.d(), ld, Dinv,
-                                                           ctx->Rinv.d(), ld, status_dev(ctx), 1e-13,
-                                                           ns ? 1e-16 : -1.0, gate);
-  QB_TRY(check_launch(ctx, "chol"));
-  trinv_kernel<<<(w + CHOL_NB - 1) / CHOL_NB, TRINV_THREADS, TRINV_SMEM, ctx->stream>>>(
-      w, ctx->L.d(), ld, Dinv, status_dev(ctx), ctx->Rinv.d(), ld, gate);
-  return check_launch(ctx, "trinv");
+  chol_cluster_kernel<<<CHOL_CTAS, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(
+      ctx->G.d(), ld, w, m_rows, ctx->Rinv.d(), ld, status_dev(ctx), 1e-13, ns ? 1e-16 : -1.0, gate);
+  return check_launch(ctx, "chol");
 }
 
 // One CholeskyQR pass: dst = src T, with T from chol_inv (all on the device; gated).
