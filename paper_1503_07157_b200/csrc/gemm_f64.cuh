@@ -40,6 +40,7 @@ struct GemmParams {
   int64_t split_stride;  // elements between split partial outputs
   double* norm_partials; // EPI_SUB_COL: per-CTA sum of squares of the new C
   const int* gate;       // optional: the kernel does nothing unless *gate != 0
+  int a3d, b3d;          // NN: operand maps are 3D {16, K, rows/16} -> one TMA per operand per stage
 };
 
 template <int BN>
@@ -62,14 +63,25 @@ struct GemmCfg {
 
 template <int LAYOUT, int BN>
 __device__ __forceinline__ void gemm_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, uint8_t* sA,
-                                                 uint8_t* sB, uint64_t* bar, int m0, int n0, int k0) {
+                                                 uint8_t* sB, uint64_t* bar, int m0, int n0, int k0, int a3d,
+                                                 int b3d) {
   using Cfg = GemmCfg<BN>;
   mbar_arrive_expect_tx(bar, Cfg::STAGE_BYTES);
   if (LAYOUT == GEMM_NN) {
+    // the 16-row chunks of an MN-contiguous tile land at c * 2048 either way; a 3D map
+    // {16, K, rows/16} moves them with one instruction when rows % 16 == 0
+    if (a3d) {
+      tma_load_3d(sA, tA, bar, 0, k0, m0 / 16);
+    } else {
 #pragma unroll
-    for (int c = 0; c < GEMM_BM / 16; ++c) tma_load_2d(sA + c * 2048, tA, bar, m0 + 16 * c, k0);
+      for (int c = 0; c < GEMM_BM / 16; ++c) tma_load_2d(sA + c * 2048, tA, bar, m0 + 16 * c, k0);
+    }
+    if (b3d) {
+      tma_load_3d(sB, tB, bar, 0, k0, n0 / 16);
+    } else {
 #pragma unroll
-    for (int c = 0; c < BN / 16; ++c) tma_load_2d(sB + c * 2048, tB, bar, n0 + 16 * c, k0);
+      for (int c = 0; c < BN / 16; ++c) tma_load_2d(sB + c * 2048, tB, bar, n0 + 16 * c, k0);
+    }
   } else {
     tma_load_2d(sA, tA, bar, k0, m0);
     tma_load_2d(sB, tB, bar, k0, n0);
@@ -147,7 +159,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
     }
       for (int s = 0; s < STAGES && s < nk; ++s)
       gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + s * Cfg::STAGE_BYTES, smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES,
-                                   &full[s], m0, n0, (kt0 + s) * GEMM_BK);
+                                   &full[s], m0, n0, (kt0 + s) * GEMM_BK, p.a3d, p.b3d);
   }
 
   double acc[8][4][2];
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
       mbar_wait(&empty[slot], par);
       gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + slot * Cfg::STAGE_BYTES,
                                    smem + slot * Cfg::STAGE_BYTES + Cfg::A_BYTES, &full[slot], m0, n0,
-                                   (kt0 + i + STAGES) * GEMM_BK);
+                                   (kt0 + i + STAGES) * GEMM_BK, p.a3d, p.b3d);
     }
     if (kPrefetchC && tid == 0 && i >= nk - Cfg::C_GROUPS) {  // this slot has drained: fill it with C
       mbar_wait(&empty[slot], par);

@@ -169,6 +169,22 @@ qb_status allreduce_sum(qb_ctx ctx, double* buf, size_t count) {
 }
 
 // ---------------------------------------------------------------- tensor maps
+// 3D view {16, K, rows/16} of an MN-contiguous operand (rows % 16 == 0): box {16, BK, box_chunks}.
+qb_status make_map3d(qb_ctx ctx, CUtensorMap* map, const double* ptr, uint64_t rows, uint64_t K, int64_t ld,
+                     uint32_t box_chunks) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * 8) & 15) != 0 || rows % 16 != 0)
+    return fail(ctx, QB_ERR_INVALID_ARG, "3D TMA operand not aligned");
+  cuuint64_t dims[3] = {16, K, rows / 16};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8, 128};
+  cuuint32_t box[3] = {16, GEMM_BK, box_chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cuTensorMapEncodeTiled (3D) failed (%d)", (int)r);
+  return QB_OK;
+}
+
 qb_status make_map(qb_ctx ctx, CUtensorMap* map, const double* ptr, uint64_t inner, uint64_t outer, int64_t ld,
                    uint32_t box_inner, uint32_t box_outer) {
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * 8) & 15) != 0)
@@ -231,9 +247,15 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   if (nparts) *nparts = 0;
   if (M <= 0 || N <= 0) return QB_OK;
   CUtensorMap ta, tb;
+  int a3d = 0, b3d = 0;
   if (layout == GEMM_NN) {
-    QB_TRY(make_map(ctx, &ta, A, M, K, lda, 16, GEMM_BK));
-    QB_TRY(make_map(ctx, &tb, B, N, K, ldb, 16, GEMM_BK));
+    static const int no3d = debug_env("QB_NO_TMA3D");
+    a3d = !no3d && M % 16 == 0;
+    b3d = !no3d && N % 16 == 0;
+    if (a3d) QB_TRY(make_map3d(ctx, &ta, A, M, K, lda, GEMM_BM / 16));
+    else QB_TRY(make_map(ctx, &ta, A, M, K, lda, 16, GEMM_BK));
+    if (b3d) QB_TRY(make_map3d(ctx, &tb, B, N, K, ldb, kBN / 16));
+    else QB_TRY(make_map(ctx, &tb, B, N, K, ldb, 16, GEMM_BK));
   } else {
     QB_TRY(make_map(ctx, &ta, A, K, M, lda, 16, GEMM_BM));
     QB_TRY(make_map(ctx, &tb, B, K, N, ldb, 16, kBN));
@@ -247,6 +269,8 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   p.nkt = (K + GEMM_BK - 1) / GEMM_BK;
   p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
   p.gate = gate;
+  p.a3d = a3d;
+  p.b3d = b3d;
   const int tiles = p.tiles_m * p.tiles_n;
   const int slots = ctx->num_sms * GemmCfg<kBN>::MIN_BLOCKS;
   int splits = 1;

@@ -31,3 +31,8 @@ for r in range(reps):
     print(f"{name} rep{r}: {dt * 1e3:.1f} ms k={k} status={g['status']} resid={g['resid']:.3e} "
           f"GF/s={F / dt * 1e-9:.0f} frac37.2={F / dt / 37.2e12:.3f} launches={ctx.launches()}", flush=True)
     print("  block ms:", [round(x["ms"], 2) for x in g["stats"]], "fallbacks", sum(x["fallback"] for x in g["stats"]))
+    st = g["stats"]
+    sk = sum(x["ms_sketch"] for x in st); bm = sum(x["ms_bmat"] for x in st); dn = sum(x["ms_down"] for x in st)
+    tot = sum(x["ms"] for x in st)
+    print(f"  phases: sketch {sk:.1f} ms, B {bm:.1f} ms, downdate {dn:.1f} ms, rest (orth/reproj/power/sync) "
+          f"{tot - sk - bm - dn:.1f} ms of {tot:.1f} ms")
