@@ -192,6 +192,22 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
     }
   }
 
+  // Slot of k-tile j has been read by this warp: once every warp has, load k-tile j + STAGES
+  // into it, or — past the last k-tile — a group of the EPI_SUB_COL C tile.
+  auto refill = [&](int j) {
+    const int slot = j % STAGES;
+    const uint32_t par = (j / STAGES) & 1;
+    if (j + STAGES < nk) {
+      mbar_wait(&empty[slot], par);
+      gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + slot * Cfg::STAGE_BYTES,
+                                   smem + slot * Cfg::STAGE_BYTES + Cfg::A_BYTES, &full[slot], m0, n0,
+                                   (kt0 + j + STAGES) * GEMM_BK, p.a3d, p.b3d);
+    } else if (kPrefetchC && j >= nk - Cfg::C_GROUPS) {
+      mbar_wait(&empty[slot], par);
+      gemm_issue_c_group<BN>(&tC, smem, cbar, j - (nk - Cfg::C_GROUPS), slot, m0, n0);
+    }
+  };
+
   for (int i = 0; i < nk; ++i) {
     const int slot = i % STAGES;
     const uint32_t par = (i / STAGES) & 1;
@@ -221,17 +237,11 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
-    if (tid == 0 && i + STAGES < nk) {
-      mbar_wait(&empty[slot], par);
-      gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + slot * Cfg::STAGE_BYTES,
-                                   smem + slot * Cfg::STAGE_BYTES + Cfg::A_BYTES, &full[slot], m0, n0,
-                                   (kt0 + i + STAGES) * GEMM_BK, p.a3d, p.b3d);
-    }
-    if (kPrefetchC && tid == 0 && i >= nk - Cfg::C_GROUPS) {  // this slot has drained: fill it with C
-      mbar_wait(&empty[slot], par);
-      gemm_issue_c_group<BN>(&tC, smem, cbar, i - (nk - Cfg::C_GROUPS), slot, m0, n0);
-    }
+    // Thread 0 refills the slot of the PREVIOUS k-tile: the other warps have usually released it
+    // already, so the producer rarely stalls its own warp (STAGES-1 tiles stay in flight).
+    if (tid == 0 && i >= 1) refill(i - 1);
   }
+  if (tid == 0 && nk >= 1) refill(nk - 1);
 
   // ------------------------------------------------------------ epilogue
   const int mb = m0 + wm * 64 + (lane >> 2);
