@@ -274,10 +274,12 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   const int tiles = p.tiles_m * p.tiles_n;
   const int slots = ctx->num_sms * GemmCfg<kBN>::MIN_BLOCKS;
   int splits = 1;
-  if (epi != EPI_SUB_COL && allow_split) splits = choose_splits(tiles, p.nkt, slots, 64);
+  if (allow_split) splits = choose_splits(tiles, p.nkt, slots, 64);
   p.kt_per_split = (p.nkt + splits - 1) / splits;
   splits = (p.nkt + p.kt_per_split - 1) / p.kt_per_split;
   if (splits < 1) splits = 1;
+  const bool subtract = epi == EPI_SUB_COL;
+  if (subtract && splits > 1) epi = EPI_STORE_COL;  // split products are summed, then subtracted
 
   if (epi == EPI_SUB_COL) {
     CUtensorMap tc;  // the C tile is prefetched by TMA (box {16 m, BN n})
@@ -340,7 +342,7 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
     if (nparts) *nparts = grid;
   }
   splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp, C, ldc, sq,
-                                                               gate);
+                                                               gate, subtract ? 1 : 0);
   return check_launch(ctx, "splitk_reduce");
 }
 
@@ -390,16 +392,22 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
                   bool row_distributed = false) {
   const int64_t ldt = round_up(m, 16);
   double* T = ctx->T1.d();
-  QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, sizeof(int), ctx->stream));
+  QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, 2 * sizeof(int), ctx->stream));
   QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr, row_distributed));
-  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, nullptr, row_distributed));
+  // second pass only after a factorization (status[2]); a Newton-Schulz first pass is final
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 2, row_distributed));
+  {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
+    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, status_dev(ctx) + 2);
+    QB_TRY(check_launch(ctx, "gated_copy"));
+  }
   QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed));
   QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed));
   return QB_OK;
 }
 
 qb_status reset_flags(qb_ctx ctx) {
-  QB_CUDA(cudaMemsetAsync(status_dev(ctx), 0, 4 * sizeof(int), ctx->stream));
+  QB_CUDA(cudaMemsetAsync(status_dev(ctx), 0, 8 * sizeof(int), ctx->stream));
   return QB_OK;
 }
 
@@ -646,9 +654,9 @@ qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
     QB_TRY(cholqr2(ctx, ctx->Y.d(), ldy, ctx->Y.d(), ldy, m, (int)w));
     QB_CUDA(cudaMemcpy2DAsync(X, ldx * 8, ctx->Y.p, ldy * 8, m * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (ctx->h_status[3]) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift (w=%lld)", (long long)w);
+  if (ctx->h_status[4]) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift (w=%lld)", (long long)w);
   return QB_OK;
 }
 
@@ -687,7 +695,7 @@ qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_
   QB_CUDA(cudaMemcpy2DAsync(ctx->G.p, ld * 8, G, ldg * 8, w * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
   QB_TRY(reset_flags(ctx));
   QB_TRY(chol_inv(ctx, (int)w, m_rows, false, nullptr));
-  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
   const int st = ctx->h_status[0];
   if (shifted) *shifted = st;
@@ -840,13 +848,13 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
     QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 2));  // ||A^(i)||_F^2 and ||B_i||_F^2 over the shards
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (ctx->h_status[3])
+    if (ctx->h_status[4])
       return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift in the block ending at %lld",
                   (long long)(ell + w));
-    ctx->block_fallbacks = ctx->h_status[2];
+    ctx->block_fallbacks = ctx->h_status[3];
     r2 = ctx->h_scal[0];
     ei -= ctx->h_scal[1];
     ell += w;

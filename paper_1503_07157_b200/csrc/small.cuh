@@ -51,12 +51,13 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_kernel(const double* __res
 }
 
 // out[r*ldo + c] = sum_{s<S} P[s*stride + r*ldp + c] for r < rows, c < cols (any layout
-// where "r" is the strided index).  Optional per-block sum of squares of the result.
+// where "r" is the strided index), or out -= that sum when `subtract`.  Optional per-block
+// sum of squares of the result.
 __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double* __restrict__ P, int S, int64_t stride,
                                                                     int64_t rows, int64_t cols, int64_t ldp,
                                                                     double* __restrict__ out, int64_t ldo,
                                                                     double* __restrict__ sq_partials,
-                                                                    const int* __restrict__ gate) {
+                                                                    const int* __restrict__ gate, int subtract) {
   if (gate != nullptr && __ldcg(gate) == 0) return;
   __shared__ double red[RED_THREADS / 32];
   double sq = 0.0;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
     const double* src = P + r * ldp + c;
     double v = 0.0;
     for (int s = 0; s < S; ++s) v += src[s * stride];
+    if (subtract) v = out[r * ldo + c] - v;  // C -= sum of the split products
     out[r * ldo + c] = v;
     sq = fma(v, v, sq);
   }
@@ -111,6 +113,20 @@ __global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in
   }
 }
 
+// dst = src (column-major rows x cols) unless *gate != 0 (CholeskyQR: a first pass that took the
+// Newton-Schulz step is final; its result moves from the scratch to the destination).
+__global__ void __launch_bounds__(256) gated_copy_kernel(const double* __restrict__ src, int64_t lds,
+                                                         double* __restrict__ dst, int64_t ldd, int64_t rows,
+                                                         int64_t cols, const int* __restrict__ gate) {
+  if (__ldcg(gate) != 0) return;
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = idx / rows, r = idx - c * rows;
+    dst[r + c * ldd] = src[r + c * lds];
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K4 core — chol_cluster_kernel: the CholeskyQR "T" of a w x w Gram matrix G = X^T X
 // (column-major), w <= 256, on ONE thread-block cluster of 8 CTAs (one 32-column panel of the
@@ -127,8 +143,9 @@ __global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in
 //     R^-1 = L^-T (upper triangular).  A pivot that is not > tol * G_jj (or NaN) is a breakdown
 //     (reading R8): the cluster restarts once with the shifted-CholeskyQR shift
 //     s = 11 (m w + w (w+1)) u trace(G).  status[0] = 0 ok / 1 shifted / 2 failed.
-// Block-level flags: status[1] = 1 when the shift was used (gates the extra CholeskyQR3
-// passes), status[2] += 1 per shifted factorization, status[3] = 1 on failure.
+// Flags: status[1] = 1 when the shift was used (gates the extra CholeskyQR3 passes),
+// status[2] = 1 when the Cholesky path ran (gates CholeskyQR's second pass; a Newton-Schulz
+// first pass needs none), status[3] += 1 per shifted factorization, status[4] = 1 on failure.
 // `gate` (may be null): the kernel does nothing unless *gate != 0.
 constexpr int CHOL_MAXW = 256;
 constexpr int CHOL_NB = 32;
@@ -289,11 +306,12 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
   }
   if (cta == 0 && tid == 0) {
     status[0] = attempt;  // 0, 1, or 2 (= failed twice)
+    status[2] = 1;
     if (attempt == 1) {
       status[1] = 1;
-      atomicAdd(status + 2, 1);
+      atomicAdd(status + 3, 1);
     }
-    if (attempt >= 2) status[3] = 1;
+    if (attempt >= 2) status[4] = 1;
   }
   if (attempt >= 2) {
     cluster.sync();
