@@ -241,12 +241,71 @@ int choose_splits(int tiles, int nkt, int slots, int max_splits) {
 // want_norm; *nparts receives the number of partials).  For the STORE epilogues the
 // K dimension may be split; then partials land in ctx->P and are reduced in a fixed order
 // (with the sum of squares of C into ctx->parts when want_norm).
+template <int CPI>
+qb_status launch_down_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                        const GemmParams& p, int grid) {
+  using Cfg = GemmCfg<64>;
+  auto kern = gemm_f64_down_kernel<CPI>;
+  constexpr int smem = Cfg::SMEM_BYTES + 16;
+  static bool attr_done = false;
+  if (!attr_done) {
+    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_done = true;
+  }
+  kern<<<grid, Cfg::THREADS, smem, ctx->stream>>>(ta, tb, tc, p);
+  return check_launch(ctx, "gemm_f64_down");
+}
+
+template <int BN>
+qb_status dispatch_gemm(qb_ctx ctx, int layout, int epi, const CUtensorMap& ta, const CUtensorMap& tb,
+                        const CUtensorMap& tc, const GemmParams& p, int splits) {
+  if (layout == GEMM_NN) {
+    if (epi == EPI_STORE_COL) return launch_gemm_t<GEMM_NN, BN, EPI_STORE_COL>(ctx, ta, tb, tc, p, splits);
+    if (epi == EPI_STORE_ROW) return launch_gemm_t<GEMM_NN, BN, EPI_STORE_ROW>(ctx, ta, tb, tc, p, splits);
+    return launch_gemm_t<GEMM_NN, BN, EPI_SUB_COL>(ctx, ta, tb, tc, p, splits);
+  }
+  if (epi == EPI_STORE_COL) return launch_gemm_t<GEMM_TN, BN, EPI_STORE_COL>(ctx, ta, tb, tc, p, splits);
+  if (epi == EPI_STORE_ROW) return launch_gemm_t<GEMM_TN, BN, EPI_STORE_ROW>(ctx, ta, tb, tc, p, splits);
+  return launch_gemm_t<GEMM_TN, BN, EPI_SUB_COL>(ctx, ta, tb, tc, p, splits);
+}
+
+// C = opA * opB.  epi: EPI_STORE_COL (C[i + j*ldc]), EPI_STORE_ROW (C[i*ldc + j]) or
+// EPI_SUB_COL (C[i + j*ldc] -= ..., per-CTA sum of squares into ctx->parts when
+// want_norm; *nparts receives the number of partials).  The K dimension may be split
+// (fixed-order reduction of partials in ctx->P, the sum of squares of C into ctx->parts
+// when want_norm).  Tile width: 64 (two CTAs per SM), or 128 (one CTA per SM, twice the
+// work per tile) for an unsplit subtract-update such as the downdate A -= Q_i B_i, whose
+// K = b is short and whose per-tile prologue/epilogue would otherwise show.
 qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const double* A, int64_t lda, const double* B,
                int64_t ldb, double* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true,
                const int* gate = nullptr) {
   if (nparts) *nparts = 0;
   if (M <= 0 || N <= 0) return QB_OK;
-  CUtensorMap ta, tb;
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.nkt = (K + GEMM_BK - 1) / GEMM_BK;
+  p.gate = gate;
+  p.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  int bn = 64;
+  p.tiles_n = (N + bn - 1) / bn;
+  int splits = 1;
+  if (allow_split) splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 64);
+  const bool subtract = epi == EPI_SUB_COL;
+  static const int wide_env = debug_env("QB_WIDE_DOWNDATE");  // experiment: 1 = 128-wide tiles
+  if (subtract && splits == 1 && wide_env > 0 && N >= 2048) {
+    bn = 128;
+    p.tiles_n = (N + bn - 1) / bn;
+  }
+  p.kt_per_split = (p.nkt + splits - 1) / splits;
+  splits = (p.nkt + p.kt_per_split - 1) / p.kt_per_split;
+  if (splits < 1) splits = 1;
+  if (subtract && splits > 1) epi = EPI_STORE_COL;  // split products are summed, then subtracted
+  p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
+  const int tiles = p.tiles_m * p.tiles_n;
+
+  CUtensorMap ta, tb, tc;
   int a3d = 0, b3d = 0;
   if (layout == GEMM_NN) {
     static const int no3d = debug_env("QB_NO_TMA3D");
@@ -254,58 +313,46 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
     b3d = !no3d && N % 16 == 0;
     if (a3d) QB_TRY(make_map3d(ctx, &ta, A, M, K, lda, GEMM_BM / 16));
     else QB_TRY(make_map(ctx, &ta, A, M, K, lda, 16, GEMM_BK));
-    if (b3d) QB_TRY(make_map3d(ctx, &tb, B, N, K, ldb, kBN / 16));
+    if (b3d) QB_TRY(make_map3d(ctx, &tb, B, N, K, ldb, bn / 16));
     else QB_TRY(make_map(ctx, &tb, B, N, K, ldb, 16, GEMM_BK));
   } else {
     QB_TRY(make_map(ctx, &ta, A, K, M, lda, 16, GEMM_BM));
-    QB_TRY(make_map(ctx, &tb, B, K, N, ldb, 16, kBN));
+    QB_TRY(make_map(ctx, &tb, B, K, N, ldb, 16, bn));
   }
-  GemmParams p{};
-  p.M = M;
-  p.N = N;
-  p.K = K;
-  p.tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
-  p.tiles_n = (N + kBN - 1) / kBN;
-  p.nkt = (K + GEMM_BK - 1) / GEMM_BK;
-  p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
-  p.gate = gate;
   p.a3d = a3d;
   p.b3d = b3d;
-  const int tiles = p.tiles_m * p.tiles_n;
-  const int slots = ctx->num_sms * GemmCfg<kBN>::MIN_BLOCKS;
-  int splits = 1;
-  if (allow_split) splits = choose_splits(tiles, p.nkt, slots, 64);
-  p.kt_per_split = (p.nkt + splits - 1) / splits;
-  splits = (p.nkt + p.kt_per_split - 1) / p.kt_per_split;
-  if (splits < 1) splits = 1;
-  const bool subtract = epi == EPI_SUB_COL;
-  if (subtract && splits > 1) epi = EPI_STORE_COL;  // split products are summed, then subtracted
+  tc = ta;
 
   if (epi == EPI_SUB_COL) {
-    CUtensorMap tc;  // the C tile is prefetched by TMA (box {16 m, BN n})
-    QB_TRY(make_map(ctx, &tc, C, M, N, ldc, 16, kBN));
+    QB_TRY(make_map(ctx, &tc, C, M, N, ldc, 16, bn));  // the C tile is prefetched by TMA
     p.C = C;
     p.ldc = ldc;
     p.split_stride = 0;
+    // persistent kernel with the epilogue hidden under the next tile (TMEM-parked accumulators)
+    static const int no_persist = debug_env("QB_NO_PERSISTENT_DOWNDATE");
+    const int pslots = 2 * ctx->num_sms;
+    if (!no_persist && layout == GEMM_NN && bn == 64 && p.nkt >= 8 && tiles >= 4 * pslots) {
+      const int grid = std::min(tiles, pslots);
+      if (want_norm) {
+        QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
+        p.norm_partials = ctx->parts.d();
+        if (nparts) *nparts = grid;
+      }
+      return p.nkt >= 16 ? launch_down_t<1>(ctx, ta, tb, tc, p, grid) : launch_down_t<2>(ctx, ta, tb, tc, p, grid);
+    }
     if (want_norm) {
       QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)tiles));
       p.norm_partials = ctx->parts.d();
       if (nparts) *nparts = tiles;
     }
-    if (layout == GEMM_NN) return launch_gemm_t<GEMM_NN, kBN, EPI_SUB_COL>(ctx, ta, tb, tc, p, 1);
-    return launch_gemm_t<GEMM_TN, kBN, EPI_SUB_COL>(ctx, ta, tb, tc, p, 1);
+    return bn == 128 ? dispatch_gemm<128>(ctx, layout, epi, ta, tb, tc, p, 1)
+                     : dispatch_gemm<64>(ctx, layout, epi, ta, tb, tc, p, 1);
   }
 
   if (splits == 1) {
     p.C = C;
     p.ldc = ldc;
-    if (layout == GEMM_NN) {
-      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, 1)));
-      else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, 1)));
-    } else {
-      if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, 1)));
-      else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, 1)));
-    }
+    QB_TRY(dispatch_gemm<64>(ctx, layout, epi, ta, tb, tc, p, 1));
     if (want_norm) {
       // sum of squares of the stored result (rows x cols in "strided-row" form)
       const int64_t rows = epi == EPI_STORE_ROW ? M : N, cols = epi == EPI_STORE_ROW ? N : M;
@@ -326,13 +373,7 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   p.C = ctx->P.d();
   p.ldc = ldp;
   p.split_stride = stride;
-  if (layout == GEMM_NN) {
-    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, splits)));
-    else QB_TRY((launch_gemm_t<GEMM_NN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, splits)));
-  } else {
-    if (epi == EPI_STORE_COL) QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_COL>(ctx, ta, tb, ta, p, splits)));
-    else QB_TRY((launch_gemm_t<GEMM_TN, kBN, EPI_STORE_ROW>(ctx, ta, tb, ta, p, splits)));
-  }
+  QB_TRY(dispatch_gemm<64>(ctx, layout, epi, ta, tb, tc, p, splits));
   const int64_t total = rows * cols;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
   double* sq = nullptr;

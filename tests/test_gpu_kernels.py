@@ -33,7 +33,7 @@ def from_colmajor(buf, r):
 
 
 SHAPES = [(1, 1, 1), (7, 5, 3), (128, 64, 16), (129, 65, 17), (300, 200, 1000), (1000, 256, 5000),
-          (256, 20000 // 16, 333), (4000, 130, 64)]
+          (256, 20000 // 16, 333), (4000, 130, 64), (200, 2100, 40), (385, 4096, 256)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -130,3 +130,29 @@ def test_gram_gemm_bitwise_reproducible(q):
         outs.append(G)
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+@pytest.mark.parametrize("M,N,K", [(2000, 20000, 256), (1990, 19970, 130), (300, 40000, 64)])
+def test_persistent_downdate_matches_fp64(q, M, N, K):
+    """The persistent subtract-update (TMEM-parked accumulators, epilogue hidden under the next
+    tile) that runs the downdate A -= Q_i B_i: ragged M and N, nk >= 16 and 8 <= nk < 16."""
+    qbp, c = q
+    rng = np.random.default_rng(M + N + K)
+    Qm = rng.standard_normal((M, K)) / np.sqrt(K)
+    Bm = rng.standard_normal((K, N))
+    C0 = rng.standard_normal((M, N))
+    A, lda = dev_colmajor(Qm)
+    B, ldb = dev_colmajor(Bm.T)
+    C, ldc = dev_colmajor(C0)
+    outs = []
+    for _ in range(2):
+        Cw = C.clone()
+        ss = qbp.qb_gemm(c.ctx, 0, 2, M, N, K, A.data_ptr(), lda, B.data_ptr(), ldb, Cw.data_ptr(), ldc,
+                         split=False, want_sumsq=True)
+        outs.append((Cw, ss))
+    assert torch.equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+    got = from_colmajor(outs[0][0], M)
+    want = C0 - Qm @ Bm
+    scale = np.sqrt(K) * 1e-15 * (np.abs(Qm) @ np.abs(Bm)).max()
+    assert np.abs(got - want).max() <= 8 * scale + 1e-15
+    assert abs(outs[0][1] - float(np.sum(want * want))) <= 1e-12 * float(np.sum(want * want))
