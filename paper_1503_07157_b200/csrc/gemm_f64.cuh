@@ -316,252 +316,4 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
 }
 
 
-// ---------------------------------------------------------------------------------------
-// Persistent subtract-update for the downdate A -= Q_i B_i (NN, K = b short, 10^4-10^5 tiles).
-// Same 128 x 64 tile, warp tiles, TMA ring and swizzles as gemm_f64_kernel, but each CTA
-// walks tiles t = blockIdx.x, +gridDim.x, ... with ONE continuous k-tile stream (the producer
-// runs ahead across tile boundaries), and the epilogue of tile t is hidden under the mainloop
-// of tile t+1: at the end of a tile every thread parks its 64 FP64 accumulators in its own
-// TMEM lane (tcgen05.st, 128 columns per CTA — TMEM used as a register-file extension, since
-// FP64 has no tcgen05.mma kind), and during the next tile's k-iterations it takes them back 4
-// at a time (tcgen05.ld), subtracts them from C (read from L2, prefetched one iteration ahead;
-// the C tile itself is TMA-prefetched into L2 one tile ahead) and stores the result.  The
-// squared norm of the new C is accumulated per thread and reduced once per CTA (fixed order).
-// CPI = epilogue chunks (of 4 values) per k-iteration: 1 for nk >= 16, 2 for 8 <= nk < 16.
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
-      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
-      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-               : "r"(taddr)
-               : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-template <int CPI>
-__global__ void __launch_bounds__(GemmCfg<64>::THREADS, 2)
-    gemm_f64_down_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
-                         const __grid_constant__ CUtensorMap tC, const GemmParams p) {
-  using Cfg = GemmCfg<64>;
-  constexpr int BN = 64;
-  constexpr int STAGES = Cfg::STAGES;
-  constexpr int CHUNKS = 16;  // 64 accumulators per thread, 4 per chunk
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + STAGES);
-  double* red = reinterpret_cast<double*>(tmem_slot + 2);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int tiles = p.tiles_m * p.tiles_n;
-  const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int nk = p.nkt;
-  const int total = my_tiles * nk;
-  auto origin = [&](int it, int& m0, int& n0) {
-    const int t = blockIdx.x + it * gridDim.x;
-    int tm, tn;
-    if (p.raster_m_fast) {
-      tm = t % p.tiles_m;
-      tn = t / p.tiles_m;
-    } else {
-      tn = t % p.tiles_n;
-      tm = t / p.tiles_n;
-    }
-    m0 = tm * GEMM_BM;
-    n0 = tn * BN;
-  };
-  auto issue = [&](int g) {
-    int m0, n0;
-    origin(g / nk, m0, n0);
-    const int slot = g % STAGES;
-    gemm_issue_stage<GEMM_NN, BN>(&tA, &tB, smem + slot * Cfg::STAGE_BYTES,
-                                  smem + slot * Cfg::STAGE_BYTES + Cfg::A_BYTES, &full[slot], m0, n0,
-                                  (g % nk) * GEMM_BK, p.a3d, p.b3d);
-  };
-  auto refill = [&](int j) {  // slot of stream index j was read by this warp: reuse it for j + STAGES
-    if (j + STAGES < total) {
-      mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
-      issue(j + STAGES);
-    }
-  };
-  auto prefetch_c_l2 = [&](int it) {
-    int m0, n0;
-    origin(it, m0, n0);
-    for (int b = 0; b < GEMM_BM / 16; ++b) tma_prefetch_l2_2d(&tC, m0 + 16 * b, n0);
-  };
-
-  if (tid == 0) {
-    tma_prefetch_desc(&tA);
-    tma_prefetch_desc(&tB);
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::WARPS);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 0) {  // 128 TMEM columns: one lane per thread, 128 32-bit words each
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t taddr = *tmem_slot + (static_cast<uint32_t>(warp * 32) << 16);
-
-  if (tid == 0) {
-    if (my_tiles > 0) prefetch_c_l2(0);
-    for (int g = 0; g < STAGES && g < total; ++g) issue(g);
-  }
-
-  uint32_t offA[4][2];
-#pragma unroll
-  for (int kq = 0; kq < 4; ++kq) {
-    const int k = kq + 4 * (lane & 3);
-    const int rsw = k & 7;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) offA[kq][h] = k * 128 + ((((h * 4) + (lane >> 3)) ^ rsw) << 4) + (((lane >> 2) & 1) << 3);
-  }
-
-  double acc[8][4][2];
-  double cv[CPI][4];
-  double sq = 0.0;
-  int pm0 = -1, pn0 = 0;  // origin of the tile parked in TMEM (epilogue pending)
-  // C values of chunk c of the parked tile (4 accumulators r = 4c .. 4c+3)
-  auto load_c = [&](int c, double (&v)[4]) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = 4 * c + j, mi = r >> 3, ni = (r >> 1) & 3, e = r & 1;
-      const int m = pm0 + wm * 64 + mi * 8 + (lane >> 2), n = pn0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
-      v[j] = (m < p.M && n < p.N) ? __ldcg(p.C + m + static_cast<int64_t>(n) * p.ldc) : 0.0;
-    }
-  };
-  auto finish_chunk = [&](int c, const double (&v)[4]) {
-    uint32_t w8[8];
-    tmem_ld8(taddr + 8 * c, w8);
-    tmem_wait_ld();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = 4 * c + j, mi = r >> 3, ni = (r >> 1) & 3, e = r & 1;
-      const int m = pm0 + wm * 64 + mi * 8 + (lane >> 2), n = pn0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
-      const double a = __hiloint2double(static_cast<int>(w8[2 * j + 1]), static_cast<int>(w8[2 * j]));
-      if (m < p.M && n < p.N) {
-        const double x = v[j] - a;
-        __stcg(p.C + m + static_cast<int64_t>(n) * p.ldc, x);
-        sq = fma(x, x, sq);
-      }
-    }
-  };
-
-  for (int it = 0; it < my_tiles; ++it) {
-    if (tid == 0 && it + 1 < my_tiles) prefetch_c_l2(it + 1);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int kk = 0; kk < nk; ++kk) {
-      const int g = it * nk + kk;
-      const int slot = g % STAGES;
-      mbar_wait(&full[slot], (g / STAGES) & 1);
-      __syncwarp();
-      const uint8_t* aS = smem + slot * Cfg::STAGE_BYTES;
-      const uint8_t* bS = aS + Cfg::A_BYTES;
-#pragma unroll
-      for (int kq = 0; kq < 4; ++kq) {
-        double a[8], b[4];
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi) a[mi] = *reinterpret_cast<const double*>(aS + (wm * 4 + (mi >> 1)) * 2048 + offA[kq][mi & 1]);
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) b[ni] = *reinterpret_cast<const double*>(bS + (wn * 2 + (ni >> 1)) * 2048 + offA[kq][ni & 1]);
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (tid == 0 && g >= 1) refill(g - 1);
-      // hidden epilogue of the parked tile: chunks kk*CPI .. kk*CPI + CPI - 1
-      if (pm0 >= 0 && kk * CPI < CHUNKS) {
-#pragma unroll
-        for (int cc = 0; cc < CPI; ++cc) finish_chunk(kk * CPI + cc, cv[cc]);
-        if ((kk + 1) * CPI < CHUNKS) {
-#pragma unroll
-          for (int cc = 0; cc < CPI; ++cc) load_c((kk + 1) * CPI + cc, cv[cc]);
-        }
-      }
-    }
-    if (it + 1 < my_tiles) {  // park this tile's accumulators in TMEM, prefetch C of chunk(s) 0
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t v[32];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int r = 16 * q + j, mi = r >> 3, ni = (r >> 1) & 3, e = r & 1;
-          v[2 * j] = static_cast<uint32_t>(__double2loint(acc[mi][ni][e]));
-          v[2 * j + 1] = static_cast<uint32_t>(__double2hiint(acc[mi][ni][e]));
-        }
-        tmem_st32(taddr + 32 * q, v);
-      }
-      tmem_wait_st();
-      origin(it, pm0, pn0);
-#pragma unroll
-      for (int cc = 0; cc < CPI; ++cc) load_c(cc, cv[cc]);
-    } else {  // last tile: epilogue straight from the registers, 16 loads in flight per round
-      origin(it, pm0, pn0);
-#pragma unroll
-      for (int mp = 0; mp < 8; mp += 2) {
-        double c2[2][4][2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int m = pm0 + wm * 64 + (mp + h) * 8 + (lane >> 2), n = pn0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
-              c2[h][ni][e] = (m < p.M && n < p.N) ? __ldcg(p.C + m + static_cast<int64_t>(n) * p.ldc) : 0.0;
-            }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int m = pm0 + wm * 64 + (mp + h) * 8 + (lane >> 2), n = pn0 + wn * 32 + ni * 8 + 2 * (lane & 3) + e;
-              if (m < p.M && n < p.N) {
-                const double x = c2[h][ni][e] - acc[mp + h][ni][e];
-                __stcg(p.C + m + static_cast<int64_t>(n) * p.ldc, x);
-                sq = fma(x, x, sq);
-              }
-            }
-      }
-    }
-  }
-
-  sq = warp_sum(sq);
-  if (lane == 0) red[warp] = sq;
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (tid == 0 && p.norm_partials != nullptr) {
-    double t = 0.0;
-    for (int w = 0; w < Cfg::WARPS; ++w) t += red[w];
-    p.norm_partials[blockIdx.x] = t;
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tmem_slot));
-  }
-}
-
 }  // namespace qbk

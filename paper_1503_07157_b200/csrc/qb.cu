@@ -241,21 +241,6 @@ int choose_splits(int tiles, int nkt, int slots, int max_splits) {
 // want_norm; *nparts receives the number of partials).  For the STORE epilogues the
 // K dimension may be split; then partials land in ctx->P and are reduced in a fixed order
 // (with the sum of squares of C into ctx->parts when want_norm).
-template <int CPI>
-qb_status launch_down_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                        const GemmParams& p, int grid) {
-  using Cfg = GemmCfg<64>;
-  auto kern = gemm_f64_down_kernel<CPI>;
-  constexpr int smem = Cfg::SMEM_BYTES + 16;
-  static bool attr_done = false;
-  if (!attr_done) {
-    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_done = true;
-  }
-  kern<<<grid, Cfg::THREADS, smem, ctx->stream>>>(ta, tb, tc, p);
-  return check_launch(ctx, "gemm_f64_down");
-}
-
 template <int BN>
 qb_status dispatch_gemm(qb_ctx ctx, int layout, int epi, const CUtensorMap& ta, const CUtensorMap& tb,
                         const CUtensorMap& tc, const GemmParams& p, int splits) {
@@ -328,18 +313,6 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
     p.C = C;
     p.ldc = ldc;
     p.split_stride = 0;
-    // persistent kernel with the epilogue hidden under the next tile (TMEM-parked accumulators)
-    static const int no_persist = debug_env("QB_NO_PERSISTENT_DOWNDATE");
-    const int pslots = 2 * ctx->num_sms;
-    if (!no_persist && layout == GEMM_NN && bn == 64 && p.nkt >= 8 && tiles >= 4 * pslots) {
-      const int grid = std::min(tiles, pslots);
-      if (want_norm) {
-        QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
-        p.norm_partials = ctx->parts.d();
-        if (nparts) *nparts = grid;
-      }
-      return p.nkt >= 16 ? launch_down_t<1>(ctx, ta, tb, tc, p, grid) : launch_down_t<2>(ctx, ta, tb, tc, p, grid);
-    }
     if (want_norm) {
       QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)tiles));
       p.norm_partials = ctx->parts.d();
