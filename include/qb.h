@@ -59,7 +59,9 @@ enum {
   QB_OVERWRITE_A = 1u,  /* A may be used as the residual workspace and is destroyed (P:112:
                            "A^(j) can overwrite A^(j-1)"); requires lda even and A 16-byte
                            aligned, otherwise an internal copy is made anyway.              */
-  QB_NO_REPROJ = 2u     /* skip line (3')/(8) — for demonstrating P:684-696 only            */
+  QB_NO_REPROJ = 2u,    /* skip line (3')/(8) — for demonstrating P:684-696 only            */
+  QB_SKIP_POWER_ORTH = 4u /* q >= 1: Y = A (A^* Y) q times, one orth per block (P:915-931,
+                             the blocked "skip re-orthonormalization" variant, NEXT-3)     */
 };
 
 /* Per-block record (qb_stats).  r2 is the directly computed ||A^(i)||_F^2 (the stop test,

@@ -65,7 +65,7 @@ class QBResult:
         return float(np.sqrt(self.hist[-1][2])) if self.hist else float(np.sqrt(self.r2_0))
 
 
-def randqb_pb(A, eps, b, q=0, seed=1, kmax=None, reproj=True, omega_dtype=np.float64):
+def randqb_pb(A, eps, b, q=0, seed=1, kmax=None, reproj=True, omega_dtype=np.float64, skip_power_orth=False):
     """randQB_pb (Fig. 4) with P = q power steps; q = 0 is exactly
     randQB_b (Fig. 2, PAPER.md:698-725).
 
@@ -76,6 +76,9 @@ def randqb_pb(A, eps, b, q=0, seed=1, kmax=None, reproj=True, omega_dtype=np.flo
     indicator EI_i = ||A||_F^2 - sum_j ||B_j||_F^2 is recorded beside it.  Before the first
     block, ||A||_F <= eps returns k = 0 (Algorithm 1 line (2), reading R3).  kmax caps the
     rank; the last block is narrowed to hit it (reading R5).
+
+    skip_power_orth: the variant of PAPER.md:915-931 ("Is re-orthonormalizing truly
+    necessary?") applied per block: Y = A Ω; q times Y = A (A^* Y); Q_i = orth(Y).
     """
     A = np.array(A, dtype=np.float64, copy=True)          # A^(0) = A
     m, n = A.shape
@@ -91,10 +94,16 @@ def randqb_pb(A, eps, b, q=0, seed=1, kmax=None, reproj=True, omega_dtype=np.flo
     while ell < kmax:
         w = min(b, kmax - ell)
         Om = omega(seed, n, ell, w, omega_dtype)                     # line (2)
-        Qi = orth(A @ Om)                                            # line (3)
-        for _ in range(q):                                           # lines (4)-(7)
-            Qi = orth(A.T @ Qi)                                      # line (5)
-            Qi = orth(A @ Qi)                                        # line (6)
+        if skip_power_orth:
+            Y = A @ Om
+            for _ in range(q):
+                Y = A @ (A.T @ Y)
+            Qi = orth(Y)
+        else:
+            Qi = orth(A @ Om)                                        # line (3)
+            for _ in range(q):                                       # lines (4)-(7)
+                Qi = orth(A.T @ Qi)                                  # line (5)
+                Qi = orth(A @ Qi)                                    # line (6)
         if ell > 0 and reproj:                                       # line (8) / (3')
             Qbar = np.hstack(Qs)
             Qi = orth(Qi - Qbar @ (Qbar.T @ Qi))
@@ -124,10 +133,17 @@ def randqb(A, ell, seed=1):
     return Q, Q.T @ A
 
 
-def randqb_p(A, ell, P, seed=1):
+def randqb_p(A, ell, P, seed=1, skip_power_orth=False):
     """randQB_p (Fig. 3, PAPER.md:826-849): Q = orth(AΩ); P times {Q = orth(A^*Q);
-    Q = orth(AQ)}; B = Q^* A."""
+    Q = orth(AQ)}; B = Q^* A.  skip_power_orth: Y = AΩ; P times Y = A(A^*Y); Q = orth(Y)
+    (PAPER.md:919-927)."""
     A = np.asarray(A, dtype=np.float64)
+    if skip_power_orth:
+        Y = A @ omega(seed, A.shape[1], 0, ell)
+        for _ in range(P):
+            Y = A @ (A.T @ Y)
+        Q = orth(Y)
+        return Q, Q.T @ A
     Q = orth(A @ omega(seed, A.shape[1], 0, ell))
     for _ in range(P):
         Q = orth(A.T @ Q)

@@ -29,6 +29,7 @@ QB_F32 = 1
 
 QB_OVERWRITE_A = 1
 QB_NO_REPROJ = 2
+QB_SKIP_POWER_ORTH = 4
 
 
 class QBError(RuntimeError):
@@ -262,12 +263,12 @@ class QB:
         except Exception:
             pass
 
-    def factor(self, A, eps, b, q=0, seed=1, kmax=0, overwrite=False, copy_out=True):
+    def factor(self, A, eps, b, q=0, seed=1, kmax=0, overwrite=False, copy_out=True, flags=0):
         import torch
         assert A.is_cuda and A.dtype in (torch.float64, torch.float32) and A.dim() == 2 and A.stride(0) == 1
         m, n = A.shape
         r = qb_factor(self.ctx, A.data_ptr(), m, n, A.stride(1) if n > 1 else m, eps, b, q, seed, kmax,
-                      QB_OVERWRITE_A if overwrite else 0)
+                      (QB_OVERWRITE_A if overwrite else 0) | flags)
         k = r["k"]
         ts = "<f8" if A.dtype == torch.float64 else "<f4"
         Q = view_colmajor(r["Q"], m, k, r["ldq"], ts) if k > 0 else torch.zeros(m, 0, dtype=A.dtype, device=A.device)

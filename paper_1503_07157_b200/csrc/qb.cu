@@ -420,6 +420,8 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
   return QB_OK;
 }
 
+bool skip_orth_flag(unsigned flags) { return (flags & QB_SKIP_POWER_ORTH) != 0; }
+
 qb_status reset_flags(qb_ctx ctx) {
   QB_CUDA(cudaMemsetAsync(status_dev(ctx), 0, 8 * sizeof(int), ctx->stream));
   return QB_OK;
@@ -821,9 +823,23 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
                 nullptr));
     QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));  // Y = sum_p A_p Omega_p (column shards)
     QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
-    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
+    if (!(skip_orth_flag(flags) && q > 0)) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
-    for (int j = 0; j < q; ++j) {
+    const bool skip_orth = (flags & QB_SKIP_POWER_ORTH) != 0;
+    for (int j = 0; j < q && skip_orth; ++j) {  // NEXT-3: Y = A (A^* Y), orth once
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, ctx->Y.d(), ldm, ctx->Z.d(), ldn,
+                  false, nullptr));
+      {
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w + 31) / 32));
+        transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w, ctx->Zt.d(), bp);
+        QB_TRY(check_launch(ctx, "transpose"));
+      }
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Zt.d(), bp, ctx->Y.d(), ldm,
+                  false, nullptr));
+      QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
+    }
+    if (skip_orth && q > 0) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
+    for (int j = 0; j < q && !skip_orth; ++j) {
       QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, Qi, ctx->ldq, ctx->Z.d(), ldn, false,
                   nullptr));
       QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, ctx->comm != nullptr));

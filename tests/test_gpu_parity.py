@@ -299,3 +299,14 @@ def test_fp32_path_parity(qbmod, case):
     assert np.abs(Qg.T @ Qg - np.eye(g["k"])).max() <= 1e-5
     assert np.linalg.norm(np.hstack([Qg, o.Q]) @ np.vstack([Bg, -o.B])) / nA <= 1e-4
     assert np.linalg.norm(Aw - Qg @ Bg) <= eps * (1 + 1e-4) + 1e-6 * nA
+
+
+@pytest.mark.parametrize("q", [1, 2])
+def test_skip_power_orth_parity(qbmod, ctx, q):
+    """NEXT-3: the blocked scheme without re-orthonormalisation between
+    applications of A and A^* (flag QB_SKIP_POWER_ORTH) against the oracle's same variant."""
+    A, _ = make(600, 400, "exp10_25", 3)
+    eps = 1e-7
+    o = oqb.randqb_pb(A, eps, 20, q, seed=1, skip_power_orth=True)
+    g = ctx.factor(to_dev(A), eps, 20, q, seed=1, flags=qbmod.QB_SKIP_POWER_ORTH)
+    check_parity(A, g, o, eps)

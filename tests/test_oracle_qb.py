@@ -238,3 +238,26 @@ def test_matrix1_rank_about_75():
     kq = synth.eps_rank(d, 1e-14)
     assert kq <= res.k <= kq + 10
     assert lo <= res.k <= hi
+
+
+@pytest.mark.parametrize("P,floor", [(1, 1e-5), (2, 1e-3)])
+def test_skip_power_orth_floors(P, floor):
+    """PAPER.md:1170-1182 (Fig. 'skipqr' caption and Remark): without re-orthonormalisation
+    between applications of A and A^*, the unblocked scheme cannot resolve beyond
+    sigma_1 eps_mach^(1/(2P+1)) (1e-5 for P = 1, 1e-3 for P = 2), while the blocked scheme
+    "always reaches full precision"."""
+    r = 400
+    sig = 10.0 ** (-np.arange(1, r + 1) / 25.0)
+    A = synth.make_matrix_np(600, 400, sig, 3)
+    opt = synth.optimal_error(sig, 200)
+    Qu, Bu = qb.randqb_p(A, 200, P, seed=1, skip_power_orth=True)
+    eu = np.linalg.norm(A - Qu @ Bu)
+    assert 0.1 * floor <= eu <= 10 * floor            # stuck at the predicted floor
+    Qo, Bo = qb.randqb_p(A, 200, P, seed=1)
+    assert np.linalg.norm(A - Qo @ Bo) <= 1.2 * opt   # with orth: near-optimal
+    rb = qb.randqb_pb(A, 0.0, 20, P, seed=1, kmax=200, skip_power_orth=True)
+    assert np.linalg.norm(A - rb.Q @ rb.B) <= 1.2 * opt  # blocked, no orth: full precision
+    # q = 0: the variant is the plain scheme
+    r0 = qb.randqb_pb(A, 0.0, 20, 0, seed=1, kmax=60, skip_power_orth=True)
+    r1 = qb.randqb_pb(A, 0.0, 20, 0, seed=1, kmax=60)
+    assert np.array_equal(r0.Q, r1.Q)
