@@ -1,0 +1,395 @@
+// FP32 GEMM for sm_100a on the 5th-generation tensor cores (tcgen05.mma kind::tf32, TMEM
+// accumulators), split "3xTF32" so that the products keep FP32 accuracy.  This is the FP32
+// context's path for the contractions with the residual A (K2f/K5f/K6f):
+// Y = A Ω, B = Q^* A (:710), A -= Q B (:712), and the power steps A^* Q, A Z
+// (:868-870).  The small m x b panel work (CholeskyQR, re-projection) stays in FP64.
+//
+// Splitting (reading R18b): every operand x is written x = hi + lo with hi = RN_tf32(x) (10
+// explicit mantissa bits, exactly representable in TF32) and lo = x - hi (exact in FP32,
+// |lo| <= 2^-11 |x|); the tensor core forms hi*hi + hi*lo + lo*hi with FP32 accumulation.
+// The dropped lo*lo term and the TF32 rounding of lo are below 2^-21 relative per product,
+// under the FP32 accumulation error of the K-term sums.
+//
+// Accumulation (reading R18b): the tensor core's FP32 accumulation in TMEM is not
+// round-to-nearest (measured: the error of a K-term sum grows like K^1.5, 1.4e-4 relative at
+// K = 20000), so each chunk of TF_PROMO k-tiles (128 k) is accumulated in TMEM and then added
+// into FP32 registers with IEEE rounding; two TMEM buffers let the MMAs of chunk c+1 run while
+// chunk c is drained.
+//
+// CTA tile 128 x BN, k-tile 32 floats (one 128-byte swizzle row); 10 warps:
+//   warp 0      TMA producer (one thread): raw FP32 tiles -> the stage's "hi" buffers
+//   warp 1      TMEM allocator + MMA issuer (one thread): 4 k-steps x 3 tcgen05.mma per stage
+//   warps 2..5  split the stage in place (hi = RN_tf32(x), lo = x - hi)
+//   warps 6..9  drain TMEM chunks into register accumulators, then the epilogue
+//               (warp w reads TMEM lanes 32 (w % 4) .. + 31 = tile rows)
+// Barriers per stage: full (TMA bytes landed), conv (128 splitters done), empty (MMAs done,
+// tcgen05.commit); per TMEM buffer: acc_full (chunk's MMAs done), acc_empty (drained).  One
+// tile per CTA; split-K over blockIdx.y as in the FP64 kernel.
+//
+// Operand layouts in shared memory (UMMA canonical 128B-swizzle layouts):
+//   K-major (TN): box {32 k, rows}: row r at r*128 B, 8-row groups at 1024 B (SBO), the k-th
+//                 K=8 slice 32 B further (descriptor start + 2 per step)
+//   MN-major (NN): chunks of 32 rows (128 B) x 32 k, chunk c at c*4096 B (LBO), 4-k groups at
+//                 512 B (SBO) in the 32-byte-granule swizzle (SWIZZLE_128B_BASE32B, the only
+//                 MN-major swizzle for 32-bit operands); the k-th K=8 slice 1024 B further
+#pragma once
+#include "common.cuh"
+
+namespace qbk {
+
+constexpr int TF_BM = 128;
+constexpr int TF_BK = 32;
+constexpr int TF_PROMO = 4;       // k-tiles (128 k) per TMEM accumulation chunk
+constexpr int TF_THREADS = 320;   // producer, MMA, 4 splitter warps, 4 promoter/epilogue warps
+
+enum TfEpi { TF_STORE_COL = 0, TF_STORE_ROW = 1, TF_SUB_COL = 2 };
+
+struct TfParams {
+  int M, N, K;
+  int tiles_m, tiles_n;
+  int nkt;            // ceil(K / 32)
+  int kt_per_split;
+  int raster_m_fast;
+  void* C;            // STORE_*: double output (or split partials); SUB_COL: float C
+  int64_t ldc;
+  int64_t split_stride;
+  double* norm_partials;  // SUB_COL: per-CTA sum of squares of the new C (FP64)
+  int a3d, b3d;       // NN: one 3D TMA per operand per stage ({32, K, rows/32} view)
+};
+
+template <int BN>
+struct TfCfg {
+  static constexpr int THREADS = TF_THREADS;
+  static constexpr int A_BYTES = TF_BM * TF_BK * 4;
+  static constexpr int B_BYTES = BN * TF_BK * 4;
+  static constexpr int HI_BYTES = A_BYTES + B_BYTES;   // [A_hi][B_hi], then [A_lo][B_lo]
+  static constexpr int STAGE_BYTES = 2 * HI_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers (chunk c in buffer c & 1)
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + (3 * STAGES + 4) * 8 + 64;
+  static_assert(STAGES >= 2, "at least double buffering");
+  static_assert(BN == 64 || BN == 128, "BN: register accumulators of the promoter warps");
+};
+
+// Shared-memory matrix descriptor: layout 2 = SWIZZLE_128B (K-major operands), 1 =
+// SWIZZLE_128B_BASE32B (MN-major 32-bit operands: 32-byte granules of each 128-byte row XORed
+// with the row index mod 4, the layout TMA writes with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout) {
+  uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(layout) << 61;
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, majors, N, M = 128.
+template <int BN>
+__host__ __device__ constexpr uint32_t tf32_idesc(int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
+         (static_cast<uint32_t>(TF_BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 consecutive TMEM columns of this thread's lane; the wait carries the registers as
+// in/out operands so that no use of them can be scheduled before it.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+__device__ __forceinline__ void pin8(float (&t)[8]) {
+  asm volatile("" : "+f"(t[0]), "+f"(t[1]), "+f"(t[2]), "+f"(t[3]), "+f"(t[4]), "+f"(t[5]), "+f"(t[6]), "+f"(t[7]));
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <int LAYOUT, int BN>
+__device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, uint8_t* sA, uint8_t* sB,
+                                               uint64_t* bar, int m0, int n0, int k0, int a3d, int b3d) {
+  using Cfg = TfCfg<BN>;
+  mbar_arrive_expect_tx(bar, Cfg::HI_BYTES);
+  if (LAYOUT == 0) {  // NN: MN-major chunks of 32 rows x 32 k
+    if (a3d) {
+      tma_load_3d(sA, tA, bar, 0, k0, m0 / 32);
+    } else {
+#pragma unroll
+      for (int c = 0; c < TF_BM / 32; ++c) tma_load_2d(sA + c * 4096, tA, bar, m0 + 32 * c, k0);
+    }
+    if (b3d) {
+      tma_load_3d(sB, tB, bar, 0, k0, n0 / 32);
+    } else {
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tma_load_2d(sB + c * 4096, tB, bar, n0 + 32 * c, k0);
+    }
+  } else {  // TN: K-major rows
+    tma_load_2d(sA, tA, bar, k0, m0);
+    tma_load_2d(sB, tB, bar, k0, n0);
+  }
+}
+
+template <int LAYOUT, int BN, int EPI>
+__global__ void __launch_bounds__(TF_THREADS, 1)
+    gemm_tf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                     const TfParams p) {
+  using Cfg = TfCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* conv = full + STAGES;
+  uint64_t* empty = conv + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  double* red = reinterpret_cast<double*>(tmem_slot + 2);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int tm, tn;
+  if (p.raster_m_fast) {
+    tm = blockIdx.x % p.tiles_m;
+    tn = blockIdx.x / p.tiles_m;
+  } else {
+    tn = blockIdx.x % p.tiles_n;
+    tm = blockIdx.x / p.tiles_n;
+  }
+  const int m0 = tm * TF_BM, n0 = tn * BN;
+  const int kt0 = blockIdx.y * p.kt_per_split;
+  const int kt1 = min(p.nkt, kt0 + p.kt_per_split);
+  const int nk = max(kt1 - kt0, 0);
+  const int nchunks = (nk + TF_PROMO - 1) / TF_PROMO;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tA);
+    tma_prefetch_desc(&tB);
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int j = 0; j < nk; ++j) {
+        const int slot = j % STAGES;
+        if (j >= STAGES) mbar_wait(&empty[slot], ((j / STAGES) - 1) & 1);
+        uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
+        tf_issue_stage<LAYOUT, BN>(&tA, &tB, st, st + Cfg::A_BYTES, &full[slot], m0, n0, (kt0 + j) * TF_BK, p.a3d,
+                                   p.b3d);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc<BN>(LAYOUT == 0 ? 1 : 0, LAYOUT == 0 ? 1 : 0);
+      // K-major: rows at 128 B, 8-row groups at 1024 B (SBO).  MN-major (BASE32B): 4-k groups
+      // at 512 B (SBO), 32-row chunks at 4096 B (LBO)
+      constexpr uint32_t LBO = LAYOUT == 0 ? 4096u : 16u;
+      constexpr uint32_t SBO = LAYOUT == 0 ? 512u : 1024u;
+      constexpr uint32_t LT = LAYOUT == 0 ? 1u : 2u;
+      constexpr uint32_t KSTEP = LAYOUT == 0 ? 64u : 2u;  // descriptor units (16 B) per K=8 slice
+      for (int j = 0; j < nk; ++j) {
+        const int slot = j % STAGES;
+        const int c = j / TF_PROMO, b = c & 1;
+        const bool first = (j % TF_PROMO) == 0;
+        // a chunk starts in accumulator buffer b once the promoters have drained it
+        if (first && c >= 2) mbar_wait(&acc_empty[b], ((c >> 1) - 1) & 1);
+        mbar_wait(&conv[slot], (j / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tacc = tmem_base + static_cast<uint32_t>(b * BN);
+        const uint32_t a_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES);
+        const uint32_t b_hi = a_hi + Cfg::A_BYTES;
+        const uint64_t dAh = umma_desc(a_hi, LBO, SBO, LT), dBh = umma_desc(b_hi, LBO, SBO, LT);
+        const uint64_t dAl = umma_desc(a_hi + Cfg::HI_BYTES, LBO, SBO, LT);
+        const uint64_t dBl = umma_desc(b_hi + Cfg::HI_BYTES, LBO, SBO, LT);
+#pragma unroll
+        for (int kk = 0; kk < TF_BK / 8; ++kk) {
+          const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
+          umma_tf32(tacc, dAh + adv, dBh + adv, idesc, (!first || kk > 0) ? 1u : 0u);
+          umma_tf32(tacc, dAh + adv, dBl + adv, idesc, 1u);
+          umma_tf32(tacc, dAl + adv, dBh + adv, idesc, 1u);
+        }
+        umma_commit(&empty[slot]);
+        if ((j % TF_PROMO) == TF_PROMO - 1 || j == nk - 1) umma_commit(&acc_full[b]);
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------------------------------------------------------- splitters
+    const int t = tid - 64;
+    for (int j = 0; j < nk; ++j) {
+      const int slot = j % STAGES;
+      mbar_wait(&full[slot], (j / STAGES) & 1);
+      uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
+#pragma unroll 4
+      for (int i = t; i < Cfg::HI_BYTES / 16; i += 128) {
+        float4* hp = reinterpret_cast<float4*>(st + i * 16);
+        const float4 v = *hp;
+        float4 h, l;
+        h.x = tf32_rna(v.x);
+        h.y = tf32_rna(v.y);
+        h.z = tf32_rna(v.z);
+        h.w = tf32_rna(v.w);
+        l.x = v.x - h.x;
+        l.y = v.y - h.y;
+        l.z = v.z - h.z;
+        l.w = v.w - h.w;
+        *hp = h;
+        *reinterpret_cast<float4*>(st + Cfg::HI_BYTES + i * 16) = l;
+      }
+      // generic-proxy writes -> visible to the tensor core (async proxy) before the MMA reads
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&conv[slot]);
+    }
+  } else {
+    // ---------------------------------------------------------------- promoters + epilogue
+    // Each K chunk of TF_PROMO k-tiles is accumulated by the tensor core in TMEM, then added
+    // into FP32 registers here (round-to-nearest), which bounds the length of the tensor
+    // core's own accumulation chain (reading R18b).  TMEM lane = tile row.
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int m = m0 + row;
+    const uint32_t trow = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    float acc[BN];
+#pragma unroll
+    for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int b = c & 1;
+      mbar_wait(&acc_full[b], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(trow + static_cast<uint32_t>(b * BN + c0), r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[c0 + i] += __uint_as_float(r[i]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acc_empty[b]);
+    }
+
+    double sq = 0.0;
+    if (m < p.M) {
+      const int ncols = min(BN, p.N - n0);
+      // groups of 8 columns, pinned in order so that the compiler does not widen all BN
+      // accumulators to FP64 at once (register pressure)
+      if (EPI == TF_STORE_COL) {
+        double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(blockIdx.y) * p.split_stride + m +
+                      static_cast<int64_t>(n0) * p.ldc;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 8) {
+          float t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
+          pin8(t);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (c0 + i < ncols) *dst = static_cast<double>(t[i]);
+            dst += p.ldc;
+          }
+        }
+      } else if (EPI == TF_STORE_ROW) {
+        double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(blockIdx.y) * p.split_stride +
+                      static_cast<int64_t>(m) * p.ldc + n0;
+        const bool vec = ncols == BN && (p.ldc & 1) == 0;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 8) {
+          float t[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
+          pin8(t);
+          if (vec) {
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(dst + c0 + i) = make_double2(t[i], t[i + 1]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (c0 + i < ncols) dst[c0 + i] = static_cast<double>(t[i]);
+          }
+        }
+      } else {  // TF_SUB_COL: C -= acc (FP32), sum of squares in FP64
+        float* col = static_cast<float*>(p.C) + m + static_cast<int64_t>(n0) * p.ldc;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 8) {
+          float cv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) cv[i] = c0 + i < ncols ? __ldcg(col + (c0 + i) * p.ldc) : 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (c0 + i < ncols) {
+              const float r = cv[i] - acc[c0 + i];
+              __stcg(col + (c0 + i) * p.ldc, r);
+              sq = fma(static_cast<double>(r), static_cast<double>(r), sq);
+            }
+          }
+        }
+      }
+    }
+    if (EPI == TF_SUB_COL && p.norm_partials != nullptr) {
+      sq = warp_sum(sq);
+      if (lane == 0) red[warp - 6] = sq;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 6 && lane == 0)
+        p.norm_partials[blockIdx.y * gridDim.x + blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+  }
+}
+
+}  // namespace qbk

@@ -24,6 +24,7 @@
 #include "../../include/qb.h"
 #include "common.cuh"
 #include "gemm_f64.cuh"
+#include "gemm_tf32.cuh"
 #include "omega.cuh"
 #include "small.cuh"
 
@@ -360,6 +361,155 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   return check_launch(ctx, "splitk_reduce");
 }
 
+// ---------------------------------------------------------------- FP32 (3xTF32 tcgen05) GEMM
+// K-major boxes use the plain 128-byte swizzle; MN-major boxes (mn_major) the 32-byte-atom
+// variant that the MN-major TF32 descriptor expects.
+qb_status make_map_f32(qb_ctx ctx, CUtensorMap* map, const float* ptr, uint64_t inner, uint64_t outer, int64_t ld,
+                       uint32_t box_inner, uint32_t box_outer, bool mn_major) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * 4) & 15) != 0)
+    return fail(ctx, QB_ERR_INVALID_ARG, "TMA operand not 16-byte aligned (ptr %p, ld %lld)", (const void*)ptr,
+                (long long)ld);
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (%d)", (int)r);
+  return QB_OK;
+}
+
+// 3D view {32, K, rows/32} of an MN-contiguous FP32 operand (rows % 32 == 0).
+qb_status make_map3d_f32(qb_ctx ctx, CUtensorMap* map, const float* ptr, uint64_t rows, uint64_t K, int64_t ld,
+                         uint32_t box_chunks) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * 4) & 15) != 0 || rows % 32 != 0)
+    return fail(ctx, QB_ERR_INVALID_ARG, "3D TMA operand (f32) not aligned");
+  cuuint64_t dims[3] = {32, K, rows / 32};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4, 128};
+  cuuint32_t box[3] = {32, TF_BK, box_chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cuTensorMapEncodeTiled (3D f32) failed (%d)", (int)r);
+  return QB_OK;
+}
+
+template <int LAYOUT, int BN, int EPI>
+qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const TfParams& p, int splits) {
+  using Cfg = TfCfg<BN>;
+  auto kern = gemm_tf32_kernel<LAYOUT, BN, EPI>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_done = true;
+  }
+  dim3 grid(p.tiles_m * p.tiles_n, splits);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, p);
+  return check_launch(ctx, "gemm_tf32");
+}
+
+template <int BN>
+qb_status dispatch_tf(qb_ctx ctx, int layout, int epi, const CUtensorMap& ta, const CUtensorMap& tb,
+                      const TfParams& p, int splits) {
+  if (layout == GEMM_NN) {
+    if (epi == TF_STORE_COL) return launch_tf_t<GEMM_NN, BN, TF_STORE_COL>(ctx, ta, tb, p, splits);
+    if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_NN, BN, TF_STORE_ROW>(ctx, ta, tb, p, splits);
+    return launch_tf_t<GEMM_NN, BN, TF_SUB_COL>(ctx, ta, tb, p, splits);
+  }
+  if (epi == TF_STORE_COL) return launch_tf_t<GEMM_TN, BN, TF_STORE_COL>(ctx, ta, tb, p, splits);
+  if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_TN, BN, TF_STORE_ROW>(ctx, ta, tb, p, splits);
+  return launch_tf_t<GEMM_TN, BN, TF_SUB_COL>(ctx, ta, tb, p, splits);
+}
+
+// FP32 operands, 3xTF32 products with FP32 accumulation.  epi TF_STORE_COL / TF_STORE_ROW
+// write a DOUBLE C (column- / row-major); TF_SUB_COL updates a FLOAT column-major C -= result
+// with the per-CTA FP64 sum of squares of the new C in ctx->parts (want_norm).  Split-K
+// partials (STORE only) are FP64 and reduced in a fixed order as in gemm().
+qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const float* A, int64_t lda, const float* B,
+                  int64_t ldb, void* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true) {
+  if (nparts) *nparts = 0;
+  if (M <= 0 || N <= 0) return QB_OK;
+  TfParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.nkt = (K + TF_BK - 1) / TF_BK;
+  p.tiles_m = (M + TF_BM - 1) / TF_BM;
+  static const int bn_env = debug_env("QB_TF_BN");
+  const int bn = bn_env ? bn_env : (N <= 64 ? 64 : 128);
+  p.tiles_n = (N + bn - 1) / bn;
+  const int tiles = p.tiles_m * p.tiles_n;
+  int splits = 1;
+  if (allow_split && epi != TF_SUB_COL) splits = choose_splits(tiles, p.nkt, ctx->num_sms, 64);
+  p.kt_per_split = (p.nkt + splits - 1) / splits;
+  splits = std::max(1, (p.nkt + p.kt_per_split - 1) / p.kt_per_split);
+  p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
+
+  CUtensorMap ta, tb;
+  if (layout == GEMM_NN) {
+    p.a3d = M % 32 == 0;
+    p.b3d = N % 32 == 0 && N >= bn;
+    if (p.a3d) QB_TRY(make_map3d_f32(ctx, &ta, A, M, K, lda, TF_BM / 32));
+    else QB_TRY(make_map_f32(ctx, &ta, A, M, K, lda, 32, TF_BK, true));
+    if (p.b3d) QB_TRY(make_map3d_f32(ctx, &tb, B, N, K, ldb, bn / 32));
+    else QB_TRY(make_map_f32(ctx, &tb, B, N, K, ldb, 32, TF_BK, true));
+  } else {
+    QB_TRY(make_map_f32(ctx, &ta, A, K, M, lda, TF_BK, TF_BM, false));
+    QB_TRY(make_map_f32(ctx, &tb, B, K, N, ldb, TF_BK, bn, false));
+  }
+  auto run = [&](int e, int s) -> qb_status {
+    if (bn == 64) return dispatch_tf<64>(ctx, layout, e, ta, tb, p, s);
+    if (bn == 128) return dispatch_tf<128>(ctx, layout, e, ta, tb, p, s);
+    return fail(ctx, QB_ERR_INVALID_ARG, "QB_TF_BN must be 64 or 128");
+  };
+
+  if (epi == TF_SUB_COL) {
+    p.C = C;
+    p.ldc = ldc;
+    if (want_norm) {
+      QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)tiles));
+      p.norm_partials = ctx->parts.d();
+      if (nparts) *nparts = tiles;
+    }
+    return run(TF_SUB_COL, 1);
+  }
+  const int64_t rows = epi == TF_STORE_ROW ? M : N, cols = epi == TF_STORE_ROW ? N : M;
+  if (splits == 1) {
+    p.C = C;
+    p.ldc = ldc;
+    QB_TRY(run(epi, 1));
+    if (want_norm) {
+      const int grid = (int)std::min<int64_t>(rows, 4 * ctx->num_sms);
+      QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
+      sumsq_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(static_cast<double*>(C), cols, rows, ldc, ctx->parts.d());
+      QB_TRY(check_launch(ctx, "sumsq"));
+      if (nparts) *nparts = grid;
+    }
+    return QB_OK;
+  }
+  const int64_t ldp = round_up(cols, 2);
+  const int64_t stride = rows * ldp;
+  QB_TRY(ensure(ctx, ctx->P, sizeof(double) * (size_t)(stride * splits)));
+  p.C = ctx->P.d();
+  p.ldc = ldp;
+  p.split_stride = stride;
+  QB_TRY(run(epi, splits));
+  const int64_t total = rows * cols;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
+  double* sq = nullptr;
+  if (want_norm) {
+    QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
+    sq = ctx->parts.d();
+    if (nparts) *nparts = grid;
+  }
+  splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp,
+                                                               static_cast<double*>(C), ldc, sq, nullptr, 0);
+  return check_launch(ctx, "splitk_reduce");
+}
+
 qb_status reduce_to_scal(qb_ctx ctx, int64_t nparts, int slot) {
   reduce_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->parts.d(), nparts, ctx->scal.d(), slot);
   return check_launch(ctx, "reduce");
@@ -679,7 +829,6 @@ qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
 qb_status qb_gemm(qb_ctx ctx, int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                   const void* B, int64_t ldb, void* C, int64_t ldc, int split, double* sumsq) {
   if (!ctx) return QB_ERR_INVALID_ARG;
-  if (ctx->dtype != QB_F64) return fail(ctx, QB_ERR_UNSUPPORTED, "qb_gemm: FP64 contexts only");
   if ((layout != GEMM_NN && layout != GEMM_TN) || epi < 0 || epi > 2 || M < 0 || N < 0 || K < 1 || M > INT32_MAX ||
       N > INT32_MAX || K > INT32_MAX || !A || !B || !C)
     return fail(ctx, QB_ERR_INVALID_ARG, "qb_gemm: bad arguments");
@@ -687,8 +836,12 @@ qb_status qb_gemm(qb_ctx ctx, int layout, int epi, int64_t M, int64_t N, int64_t
   QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)std::max<int64_t>(
                                      ((M + GEMM_BM - 1) / GEMM_BM) * ((N + kBN - 1) / kBN), 16 * ctx->num_sms)));
   int64_t np = 0;
-  QB_TRY(gemm(ctx, layout, epi, (int)M, (int)N, (int)K, static_cast<const double*>(A), lda,
-              static_cast<const double*>(B), ldb, static_cast<double*>(C), ldc, sumsq != nullptr, &np, split != 0));
+  if (ctx->dtype == QB_F32)
+    QB_TRY(gemm_tf(ctx, layout, epi, (int)M, (int)N, (int)K, static_cast<const float*>(A), lda,
+                   static_cast<const float*>(B), ldb, C, ldc, sumsq != nullptr, &np, split != 0));
+  else
+    QB_TRY(gemm(ctx, layout, epi, (int)M, (int)N, (int)K, static_cast<const double*>(A), lda,
+                static_cast<const double*>(B), ldb, static_cast<double*>(C), ldc, sumsq != nullptr, &np, split != 0));
   if (sumsq) {
     QB_TRY(reduce_to_scal(ctx, np, 2));
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal + 2, ctx->scal.d() + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
