@@ -18,9 +18,10 @@
  *
  * Conventions for every entry point:
  *   - All matrices are dense, FP64 (QB_F64) or FP32 (QB_F32) as chosen at qb_create.  An FP32
- *     context takes float A and returns float Q, B; in this build its arithmetic is FP64 on the
- *     exactly widened input with Omega = RN32(Omega), so its results meet the
- *     FP64 tolerances; qb_orth / qb_gemm are FP64-only.
+ *     context takes float A and returns float Q, B: the residual A^(i) is kept in FP32 and its
+ *     products run on the tensor cores as 3xTF32 with FP32 accumulation (reading R18b), with
+ *     Omega = RN32(Omega); orth, re-projection and all norms are FP64.  Its
+ *     results meet FP32 tolerances.  qb_orth is FP64-only.
  *   - "device" pointers are CUDA device pointers on the context's device; the caller owns
  *     everything it passes in; the context owns everything it hands out.
  *   - Column-major means element (i, j) at ptr[i + j*ld]; row-major means ptr[i*ld + j].
@@ -151,8 +152,10 @@ qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx);
  * B row-major); layout 1 (TN): C = A^T B with A[k + i*lda] and B[k + j*ldb].  epi 0: C
  * column-major = result; 1: C row-major (C[i*ldc + j]) = result; 2: C column-major -= result
  * (then *sumsq = ||C||_F^2 of the updated C, else *sumsq = ||result||_F^2 when sumsq != NULL).
- * split != 0 lets the library split K (fixed-order reduction).  FP64 contexts only.  Blocking.
- * Pointers must be 16-byte aligned with even leading dimensions (TMA).                       */
+ * split != 0 lets the library split K (fixed-order reduction).  Blocking.  FP64 context: A, B,
+ * C double.  FP32 context: the 3xTF32 tensor-core GEMM — A, B float; C double for epi 0/1,
+ * float for epi 2.  Pointers must be 16-byte aligned, leading dimensions multiples of 16 bytes
+ * (TMA).                                                                                       */
 qb_status qb_gemm(qb_ctx ctx, int layout, int epi, int64_t M, int64_t N, int64_t K,
                   const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                   int split, double* sumsq);

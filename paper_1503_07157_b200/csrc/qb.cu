@@ -92,7 +92,7 @@ struct qb_ctx_s {
   int64_t col_offset = 0, n_global = 0;
   ncclComm_t comm = nullptr;  // set on distributed contexts (any nranks >= 1)
 
-  DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status, Qf, Bf, Ain32;
+  DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status, Qf, Bf, Astage, Q32, B32;
   int64_t kcap = 0, ldq = 0, ldb = 0, qbar_rows = 0, bbar_cols = 0;
   double* h_scal = nullptr;  // pinned: [0] r2, [1] sum B^2, [2..3] spare
   int* h_status = nullptr;   // pinned
@@ -332,7 +332,7 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
       const int64_t rows = epi == EPI_STORE_ROW ? M : N, cols = epi == EPI_STORE_ROW ? N : M;
       const int grid = (int)std::min<int64_t>(rows, 4 * ctx->num_sms);
       QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
-      sumsq_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(C, cols, rows, ldc, ctx->parts.d());
+      sumsq_kernel<double><<<grid, RED_THREADS, 0, ctx->stream>>>(C, cols, rows, ldc, ctx->parts.d());
       QB_TRY(check_launch(ctx, "sumsq"));
       if (nparts) *nparts = grid;
     }
@@ -484,7 +484,7 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
     if (want_norm) {
       const int grid = (int)std::min<int64_t>(rows, 4 * ctx->num_sms);
       QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
-      sumsq_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(static_cast<double*>(C), cols, rows, ldc, ctx->parts.d());
+      sumsq_kernel<double><<<grid, RED_THREADS, 0, ctx->stream>>>(static_cast<double*>(C), cols, rows, ldc, ctx->parts.d());
       QB_TRY(check_launch(ctx, "sumsq"));
       if (nparts) *nparts = grid;
     }
@@ -765,7 +765,7 @@ void qb_destroy(qb_ctx ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->Awork, &ctx->Qbar, &ctx->Bbar, &ctx->Om, &ctx->Y,     &ctx->T1,    &ctx->Z,   &ctx->Zt,
                     &ctx->G,     &ctx->L,    &ctx->Rinv, &ctx->W,  &ctx->P,     &ctx->parts, &ctx->scal, &ctx->status,
-                    &ctx->Qf,    &ctx->Bf,   &ctx->Ain32};
+                    &ctx->Qf,    &ctx->Bf,   &ctx->Astage, &ctx->Q32,  &ctx->B32};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -900,23 +900,22 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   QB_CUDA(cudaSetDevice(ctx->device));
 
   // ---- residual workspace A^(0) = A (A^(j) overwrites A^(j-1), :112)
-  // FP32 contexts ("FP32 path"): A is widened once into the FP64 residual
-  // workspace (exact), the loop runs in FP64 with Ω = RN_32(Ω), and Q, B are rounded to FP32.
-  double* A = static_cast<double*>(Ain);
+  // FP32 contexts ("FP32 path"): the residual stays FP32 and its contractions run
+  // on the 3xTF32 tensor-core GEMM (gemm_tf32.cuh); the m x b panel work (CholeskyQR,
+  // re-projection) and all norms are FP64.
+  const size_t es = is_f32 ? 4 : 8;
+  void* Av = Ain;
   int64_t ldA = lda;
-  const bool inplace_ok = !is_f32 && (flags & QB_OVERWRITE_A) && (lda % 2 == 0) &&
+  const bool inplace_ok = (flags & QB_OVERWRITE_A) && (lda % (is_f32 ? 4 : 2) == 0) &&
                           ((reinterpret_cast<uintptr_t>(Ain) & 15) == 0);
-  if (is_f32) {
+  if (!inplace_ok) {
     ldA = round_up(m, 16);
-    QB_TRY(ensure(ctx, ctx->Awork, sizeof(double) * (size_t)(ldA * n)));
-    QB_TRY(launch_convert(ctx, static_cast<const float*>(Ain), lda, m, n, ctx->Awork.d(), ldA));
-    A = ctx->Awork.d();
-  } else if (!inplace_ok) {
-    ldA = round_up(m, 16);
-    QB_TRY(ensure(ctx, ctx->Awork, sizeof(double) * (size_t)(ldA * n)));
-    QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * 8, Ain, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
-    A = ctx->Awork.d();
+    QB_TRY(ensure(ctx, ctx->Awork, es * (size_t)(ldA * n)));
+    QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * es, Ain, lda * es, m * es, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    Av = ctx->Awork.p;
   }
+  double* A = static_cast<double*>(Av);  // FP64 contexts
+  float* A32 = static_cast<float*>(Av);  // FP32 contexts
 
   // ---- scratch
   const int64_t ldm = round_up(m, 16), ldn = round_up(n, 16), bp = round_up(kMaxB, 16);
@@ -930,6 +929,12 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(ensure(ctx, ctx->Z, sizeof(double) * (size_t)(ldn * b)));
     QB_TRY(ensure(ctx, ctx->Zt, sizeof(double) * (size_t)(n * bp)));
   }
+  if (is_f32) {  // FP32 copies of the panel operands of the tensor-core GEMMs
+    QB_TRY(ensure(ctx, ctx->Q32, sizeof(float) * (size_t)(ldm * b)));
+    QB_TRY(ensure(ctx, ctx->B32, sizeof(float) * (size_t)(ldn * b)));
+  }
+  float* Q32 = static_cast<float*>(ctx->Q32.p);
+  float* B32 = static_cast<float*>(ctx->B32.p);
 
   // per-CTA partials of the largest reduction (the downdate GEMM grid), sized once up front
   QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)std::max<int64_t>(
@@ -939,7 +944,10 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   {
     const int grid = (int)std::min<int64_t>(n, 8 * ctx->num_sms);
     QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
-    sumsq_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(A, m, n, ldA, ctx->parts.d());
+    if (is_f32)
+      sumsq_kernel<float><<<grid, RED_THREADS, 0, ctx->stream>>>(A32, m, n, ldA, ctx->parts.d());
+    else
+      sumsq_kernel<double><<<grid, RED_THREADS, 0, ctx->stream>>>(A, m, n, ldA, ctx->parts.d());
     QB_TRY(check_launch(ctx, "sumsq"));
     QB_TRY(reduce_to_scal(ctx, grid, 0));
     QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 1));  // ||A||_F^2 over the column shards
@@ -968,41 +976,57 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     double* Qi = Qbar + ell * ctx->ldq;
     double* Bi = ctx->Bbar.d() + ell * ctx->ldb;
 
-    // line (2): Ω_i = randn(n, w), global columns ell .. ell+w-1, row-major (ld bp)
+    // Y = A X for a row-major n x w operand X (ld bp): Ω_i or Z^T
+    auto sketch = [&](const void* X) -> qb_status {
+      if (is_f32)
+        return gemm_tf(ctx, GEMM_NN, TF_STORE_COL, (int)m, (int)w, (int)n, A32, ldA, static_cast<const float*>(X), bp,
+                       ctx->Y.d(), ldm, false, nullptr);
+      return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, static_cast<const double*>(X), bp,
+                  ctx->Y.d(), ldm, false, nullptr);
+    };
+    // Z = A^T X for a column-major m x w FP64 panel X (ld ldx)
+    auto adjoint = [&](const double* X, int64_t ldx) -> qb_status {
+      if (!is_f32)
+        return gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, X, ldx, ctx->Z.d(), ldn, false,
+                    nullptr);
+      QB_TRY(launch_convert(ctx, X, ldx, m, w, Q32, ldm));
+      return gemm_tf(ctx, GEMM_TN, TF_STORE_COL, (int)n, (int)w, (int)m, A32, ldA, Q32, ldm, ctx->Z.d(), ldn, false,
+                     nullptr);
+    };
+    // Z^T (row-major n x w, ld bp) in the residual's precision
+    auto transpose_z = [&]() -> qb_status {
+      dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w + 31) / 32));
+      if (is_f32)
+        transpose_kernel<float><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w,
+                                                                        static_cast<float*>(ctx->Zt.p), bp);
+      else
+        transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w, ctx->Zt.d(), bp);
+      return check_launch(ctx, "transpose");
+    };
+
+    // line (2): Ω_i = randn(n, w), global columns ell .. ell+w-1, row-major (ld bp); FP32
+    // contexts draw RN_32(Ω_i) (reading R18)
     QB_CUDA(cudaEventRecord(ctx->evp[0], ctx->stream));
-    QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp, is_f32 ? 2 : 0));
+    QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp, is_f32 ? 1 : 0));
     // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
-    QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Om.d(), bp, ctx->Y.d(), ldm, false,
-                nullptr));
+    QB_TRY(sketch(ctx->Om.p));
     QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));  // Y = sum_p A_p Omega_p (column shards)
     QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
     if (!(skip_orth_flag(flags) && q > 0)) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     const bool skip_orth = (flags & QB_SKIP_POWER_ORTH) != 0;
     for (int j = 0; j < q && skip_orth; ++j) {  // NEXT-3: Y = A (A^* Y), orth once
-      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, ctx->Y.d(), ldm, ctx->Z.d(), ldn,
-                  false, nullptr));
-      {
-        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w + 31) / 32));
-        transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w, ctx->Zt.d(), bp);
-        QB_TRY(check_launch(ctx, "transpose"));
-      }
-      QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Zt.d(), bp, ctx->Y.d(), ldm,
-                  false, nullptr));
+      QB_TRY(adjoint(ctx->Y.d(), ldm));
+      QB_TRY(transpose_z());
+      QB_TRY(sketch(ctx->Zt.p));
       QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
     }
     if (skip_orth && q > 0) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     for (int j = 0; j < q && !skip_orth; ++j) {
-      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)w, (int)m, A, ldA, Qi, ctx->ldq, ctx->Z.d(), ldn, false,
-                  nullptr));
+      QB_TRY(adjoint(Qi, ctx->ldq));
       QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, ctx->comm != nullptr));
-      {
-        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((w + 31) / 32));
-        transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, w, ctx->Zt.d(), bp);
-        QB_TRY(check_launch(ctx, "transpose"));
-      }
-      QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, ctx->Zt.d(), bp, ctx->Y.d(), ldm,
-                  false, nullptr));
+      QB_TRY(transpose_z());
+      QB_TRY(sketch(ctx->Zt.p));
       QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
       QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     }
@@ -1018,15 +1042,27 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
     int64_t nb_parts = 0;
     QB_CUDA(cudaEventRecord(ctx->evp[2], ctx->stream));
-    QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)w, (int)n, (int)m, Qi, ctx->ldq, A, ldA, Bi, ctx->ldb, true,
-                &nb_parts));
+    if (is_f32) {  // the residual's GEMMs take Q_i rounded to FP32: the factor the caller receives
+      QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Q32, ldm));
+      QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)w, (int)n, (int)m, Q32, ldm, A32, ldA, Bi, ctx->ldb, true,
+                     &nb_parts));
+    } else {
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)w, (int)n, (int)m, Qi, ctx->ldq, A, ldA, Bi, ctx->ldb, true,
+                  &nb_parts));
+    }
     QB_CUDA(cudaEventRecord(ctx->evp[3], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, nb_parts, 1));
     // line (10): A^(i) = A^(i-1) - Q_i B_i, with sum A^(i)^2 in the epilogue (the stop test, R1)
     int64_t na_parts = 0;
     QB_CUDA(cudaEventRecord(ctx->evp[4], ctx->stream));
-    QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)n, (int)w, Qi, ctx->ldq, Bi, ctx->ldb, A, ldA, true,
-                &na_parts));
+    if (is_f32) {  // A -= RN32(Q_i) RN32(B_i): the residual of the factors the caller receives
+      QB_TRY(launch_convert(ctx, static_cast<const double*>(Bi), ctx->ldb, n, w, B32, ctx->ldb));
+      QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)n, (int)w, Q32, ldm, B32, ctx->ldb, A32, ldA, true,
+                     &na_parts));
+    } else {
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)n, (int)w, Qi, ctx->ldq, Bi, ctx->ldb, A, ldA, true,
+                  &na_parts));
+    }
     QB_CUDA(cudaEventRecord(ctx->evp[5], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
     QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 2));  // ||A^(i)||_F^2 and ||B_i||_F^2 over the shards
@@ -1076,7 +1112,7 @@ qb_status qb_factor_host(qb_ctx ctx, const void* A_host, int64_t m, int64_t n, i
   QB_CUDA(cudaSetDevice(ctx->device));
   const int64_t es = ctx->dtype == QB_F64 ? 8 : 4;
   const int64_t ldA = round_up(m, 16);
-  DevBuf& dst = ctx->dtype == QB_F64 ? ctx->Awork : ctx->Ain32;  // FP32 input is widened by qb_factor
+  DevBuf& dst = ctx->Astage;  // staged input, factored in place
   QB_TRY(ensure(ctx, dst, (size_t)(es * ldA * n)));
   QB_CUDA(cudaMemcpy2DAsync(dst.p, ldA * es, A_host, lda_host * es, m * es, n, cudaMemcpyHostToDevice, ctx->stream));
   const void* Qd = nullptr;

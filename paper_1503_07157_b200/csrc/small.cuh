@@ -16,13 +16,17 @@ namespace qbk {
 constexpr int RED_THREADS = 256;
 
 // Per-block sum of squares of a column-major m x n matrix (ld), grid-stride over columns.
-__global__ void __launch_bounds__(RED_THREADS) sumsq_kernel(const double* __restrict__ A, int64_t m, int64_t n,
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) sumsq_kernel(const T* __restrict__ A, int64_t m, int64_t n,
                                                             int64_t lda, double* __restrict__ partials) {
   __shared__ double red[RED_THREADS / 32];
   double s = 0.0;
   for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
-    const double* col = A + j * lda;
-    for (int64_t i = threadIdx.x; i < m; i += RED_THREADS) s = fma(col[i], col[i], s);
+    const T* col = A + j * lda;
+    for (int64_t i = threadIdx.x; i < m; i += RED_THREADS) {
+      const double v = static_cast<double>(col[i]);
+      s = fma(v, v, s);
+    }
   }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -85,8 +89,9 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
 }
 
 // out[r*ldo + c] = in[r + c*ldi] for r < rows, c < cols (column-major -> row-major).
+template <typename Tout>
 __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ in, int64_t ldi, int64_t rows,
-                                                        int64_t cols, double* __restrict__ out, int64_t ldo) {
+                                                        int64_t cols, Tout* __restrict__ out, int64_t ldo) {
   __shared__ double t[32][33];
   const int64_t r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
   for (int j = threadIdx.y; j < 32; j += 8) {
@@ -96,7 +101,7 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
   __syncthreads();
   for (int j = threadIdx.y; j < 32; j += 8) {
     const int64_t r = r0 + j, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) out[r * ldo + c] = t[threadIdx.x][j];
+    if (r < rows && c < cols) out[r * ldo + c] = static_cast<Tout>(t[threadIdx.x][j]);
   }
 }
 

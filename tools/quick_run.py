@@ -12,10 +12,11 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 cfg = synth.CONFIGS[name]
 sig = synth.config_sigma(cfg)
 t = time.time()
-A0 = synth.make_matrix_torch(cfg.m, cfg.n, sig, cfg.seed_matrix)
+dt = torch.float32 if cfg.dtype == "f32" else torch.float64
+A0 = synth.make_matrix_torch(cfg.m, cfg.n, sig, cfg.seed_matrix, dtype=dt)
 torch.cuda.synchronize()
 print(f"gen {time.time() - t:.2f}s", flush=True)
-ctx = qbp.QB(0)
+ctx = qbp.QB(0, dtype=qbp.QB_F32 if cfg.dtype == "f32" else qbp.QB_F64)
 A = torch.empty_like(A0)
 for r in range(reps):
     A.copy_(A0)
