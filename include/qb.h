@@ -167,8 +167,15 @@ qb_status qb_gemm(qb_ctx ctx, int layout, int epi, int64_t M, int64_t N, int64_t
 qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_t m_rows,
                        void* Rinv, int64_t ldr, int* shifted);
 
-/* Partial SVD from the last factorization: B = Uhat D V^*, U = Q Uhat.
- * NEXT-1 row; returns QB_ERR_UNSUPPORTED in this build.                                   */
+/* Partial SVD from the context's last qb_factor (NEXT-1): B = Uhat D V^*, U = Q Uhat,
+ * so that A ~ U diag(S) V^* with U^*U = V^*V = I and S descending.  B^T = Q_B R by block
+ * Gram-Schmidt + CholeskyQR2, R's k x k SVD by cuSOLVER dgesvd (loaded at run time), U = Q Vr,
+ * V = Q_B Ur on the library's GEMMs; FP64 internally on every context.
+ * kkeep > 0 keeps the leading kkeep triplets (the tail rule), else all k.
+ * Outputs (context-owned, valid until the next call): U column-major m x kkeep (ld *ldu),
+ * S kkeep values, V column-major n x kkeep (ld *ldv), in the context's dtype.  k = 0 gives
+ * NULL pointers.  Errors: QB_ERR_INVALID_ARG without a prior factorization,
+ * QB_ERR_UNSUPPORTED on distributed contexts or without libcusolver.  Blocking.            */
 qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U, int64_t* ldu, const void** S,
                   const void** V, int64_t* ldv);
 

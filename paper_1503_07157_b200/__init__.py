@@ -187,6 +187,16 @@ def qb_stats(ctx):
                  ms_down=a.ms_down, fallback=a.fallback) for a in arr[:n.value]]
 
 
+def rqb_svd(ctx, kkeep=0):
+    """QB -> partial SVD of the context's last factorization (see include/qb.h).
+    Returns dict(U, ldu, S, V, ldv) of device pointers (context-owned)."""
+    U, S, V = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    ldu, ldv = ctypes.c_int64(), ctypes.c_int64()
+    _check(ctx, lib().rqb_svd(ctx, kkeep, ctypes.byref(U), ctypes.byref(ldu), ctypes.byref(S), ctypes.byref(V),
+                              ctypes.byref(ldv)))
+    return dict(U=U.value or 0, ldu=ldu.value, S=S.value or 0, V=V.value or 0, ldv=ldv.value)
+
+
 def qb_omega(ctx, seed, row0, row1, col0, w, out_ptr, ldo):
     _check(ctx, lib().qb_omega(ctx, seed, row0, row1, col0, w, ctypes.c_void_p(out_ptr), ldo))
 
@@ -275,7 +285,26 @@ class QB:
         B = view_rowmajor(r["B"], k, n, r["ldb"], ts) if k > 0 else torch.zeros(0, n, dtype=A.dtype, device=A.device)
         if copy_out:
             Q, B = Q.clone(), B.clone()
+        self._last = (m, n, k, A.dtype)
         return dict(status=r["status"], k=k, Q=Q, B=B, resid=r["resid"], stats=qb_stats(self.ctx))
+
+    def svd(self, kkeep=0, copy_out=True):
+        """Partial SVD A ~ U diag(S) V^T from the last ``factor`` (rqb_svd):
+        U m x k', S k', V n x k' with k' = kkeep if 0 < kkeep < k else k."""
+        import torch
+        r = rqb_svd(self.ctx, kkeep)  # raises QBError without a prior factorization
+        m, n, k, dt = self._last
+        kk = kkeep if 0 < kkeep < k else k
+        ts = "<f8" if dt == torch.float64 else "<f4"
+        if kk == 0:
+            z = lambda *s: torch.zeros(*s, dtype=dt, device="cuda")  # noqa: E731
+            return dict(U=z(m, 0), S=z(0), V=z(n, 0))
+        U = view_colmajor(r["U"], m, kk, r["ldu"], ts)
+        S = view_colmajor(r["S"], kk, 1, kk, ts)[:, 0]
+        V = view_colmajor(r["V"], n, kk, r["ldv"], ts)
+        if copy_out:
+            U, S, V = U.clone(), S.clone(), V.clone()
+        return dict(U=U, S=S, V=V)
 
     def launches(self):
         return qb_kernel_launches(self.ctx)

@@ -57,16 +57,19 @@ struct TfParams {
   int a3d, b3d;       // NN: one 3D TMA per operand per stage ({32, K, rows/32} view)
 };
 
-template <int BN>
+template <int BN, bool SUB = false>
 struct TfCfg {
   static constexpr int THREADS = TF_THREADS;
   static constexpr int A_BYTES = TF_BM * TF_BK * 4;
   static constexpr int B_BYTES = BN * TF_BK * 4;
   static constexpr int HI_BYTES = A_BYTES + B_BYTES;   // [A_hi][B_hi], then [A_lo][B_lo]
   static constexpr int STAGE_BYTES = 2 * HI_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
+  // TF_SUB_COL keeps its whole C tile (128 x BN floats, column-major) in shared memory: TMA-
+  // loaded at tile start, updated in place, TMA-stored back
+  static constexpr int C_BYTES = SUB ? TF_BM * BN * 4 : 0;
+  static constexpr int STAGES = (200 * 1024 - C_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers (chunk c in buffer c & 1)
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + (3 * STAGES + 4) * 8 + 64;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + C_BYTES + (3 * STAGES + 5) * 8 + 64;
   static_assert(STAGES >= 2, "at least double buffering");
   static_assert(BN == 64 || BN == 128, "BN: register accumulators of the promoter warps");
 };
@@ -141,7 +144,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
 template <int LAYOUT, int BN>
 __device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, uint8_t* sA, uint8_t* sB,
                                                uint64_t* bar, int m0, int n0, int k0, int a3d, int b3d) {
-  using Cfg = TfCfg<BN>;
+  using Cfg = TfCfg<BN>;  // operand stage sizes do not depend on the epilogue
   mbar_arrive_expect_tx(bar, Cfg::HI_BYTES);
   if (LAYOUT == 0) {  // NN: MN-major chunks of 32 rows x 32 k
     if (a3d) {
@@ -165,17 +168,20 @@ __device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUte
 template <int LAYOUT, int BN, int EPI>
 __global__ void __launch_bounds__(TF_THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
-                     const TfParams p) {
-  using Cfg = TfCfg<BN>;
+                     const __grid_constant__ CUtensorMap tC, const TfParams p) {
+  constexpr bool SUB = EPI == TF_SUB_COL;
+  using Cfg = TfCfg<BN, SUB>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  float* sC = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);  // SUB: [BN][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::C_BYTES);
   uint64_t* conv = full + STAGES;
   uint64_t* empty = conv + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* cbar = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 1);
   double* red = reinterpret_cast<double*>(tmem_slot + 2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -206,6 +212,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 128);
     }
+    mbar_init(cbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -221,6 +228,11 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
+      if (SUB) {  // the C tile travels beside the operands
+        tma_prefetch_desc(&tC);
+        mbar_arrive_expect_tx(cbar, Cfg::C_BYTES);
+        tma_load_2d(sC, &tC, cbar, m0, n0);
+      }
       for (int j = 0; j < nk; ++j) {
         const int slot = j % STAGES;
         if (j >= STAGES) mbar_wait(&empty[slot], ((j / STAGES) - 1) & 1);
@@ -357,22 +369,30 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
               if (c0 + i < ncols) dst[c0 + i] = static_cast<double>(t[i]);
           }
         }
-      } else {  // TF_SUB_COL: C -= acc (FP32), sum of squares in FP64
-        float* col = static_cast<float*>(p.C) + m + static_cast<int64_t>(n0) * p.ldc;
+      }
+    }
+    if (SUB) {
+      // TF_SUB_COL: C -= acc on the shared-memory copy of the tile (column n at n*128 floats:
+      // a warp touches 32 consecutive floats per column), FP64 sum of squares of the new C
+      mbar_wait(cbar, 0);
+      const int ncols = m < p.M ? min(BN, p.N - n0) : 0;
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 8) {
-          float cv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) cv[i] = c0 + i < ncols ? __ldcg(col + (c0 + i) * p.ldc) : 0.f;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (c0 + i < ncols) {
-              const float r = cv[i] - acc[c0 + i];
-              __stcg(col + (c0 + i) * p.ldc, r);
-              sq = fma(static_cast<double>(r), static_cast<double>(r), sq);
-            }
-          }
-        }
+      for (int i = 0; i < BN; ++i) {
+        const float r = sC[i * TF_BM + row] - acc[i];
+        sC[i * TF_BM + row] = r;
+        if (i < ncols) sq = fma(static_cast<double>(r), static_cast<double>(r), sq);
+      }
+      // generic-proxy writes -> visible to the TMA store (async proxy); one thread stores the
+      // tile (clipped to the matrix by TMA) once all 128 epilogue threads are done
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (warp == 6 && lane == 0) {
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tC)),
+                     "r"(smem_u32(sC)), "r"(m0), "r"(n0)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
     }
     if (EPI == TF_SUB_COL && p.norm_partials != nullptr) {

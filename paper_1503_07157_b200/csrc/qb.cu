@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>  // types only: NCCL is loaded at run time (dlopen), never linked
+#include <cusolverDn.h>  // types only: cuSOLVER (the k x k SVD core of rqb_svd) is loaded at run time
 
 #include "../../include/qb.h"
 #include "common.cuh"
@@ -74,6 +75,60 @@ NcclApi& nccl() {
   return api;
 }
 
+// ---------------------------------------------------------------- cuSOLVER (dlopen)
+// rqb_svd (NEXT-1) needs one dense SVD of a k x k matrix (k = the QB rank); that small core is
+// the library's dgesvd, every O(mk^2) / O(nk^2) step around it runs in this library's kernels.
+struct SolverApi {
+  bool tried = false, ok = false;
+  decltype(&cusolverDnCreate) create = nullptr;
+  decltype(&cusolverDnDestroy) destroy = nullptr;
+  decltype(&cusolverDnSetStream) setStream = nullptr;
+  decltype(&cusolverDnDgesvd_bufferSize) gesvdBufferSize = nullptr;
+  decltype(&cusolverDnDgesvd) gesvd = nullptr;
+  decltype(&cusolverDnCreateParams) createParams = nullptr;
+  decltype(&cusolverDnDestroyParams) destroyParams = nullptr;
+  decltype(&cusolverDnDestroyGesvdjInfo) destroyGesvdjInfo = nullptr;
+  decltype(&cusolverDnXgesvdp_bufferSize) gesvdpBufferSize = nullptr;
+  decltype(&cusolverDnXgesvdp) gesvdp = nullptr;
+  decltype(&cusolverDnCreateGesvdjInfo) createGesvdjInfo = nullptr;
+  decltype(&cusolverDnXgesvdjSetTolerance) gesvdjSetTol = nullptr;
+  decltype(&cusolverDnXgesvdjSetMaxSweeps) gesvdjSetSweeps = nullptr;
+  decltype(&cusolverDnDgesvdj_bufferSize) gesvdjBufferSize = nullptr;
+  decltype(&cusolverDnDgesvdj) gesvdj = nullptr;
+};
+
+SolverApi& solver() {
+  static SolverApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libcusolver.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.create = reinterpret_cast<decltype(&cusolverDnCreate)>(dlsym(h, "cusolverDnCreate"));
+  api.destroy = reinterpret_cast<decltype(&cusolverDnDestroy)>(dlsym(h, "cusolverDnDestroy"));
+  api.setStream = reinterpret_cast<decltype(&cusolverDnSetStream)>(dlsym(h, "cusolverDnSetStream"));
+  api.gesvdBufferSize =
+      reinterpret_cast<decltype(&cusolverDnDgesvd_bufferSize)>(dlsym(h, "cusolverDnDgesvd_bufferSize"));
+  api.gesvd = reinterpret_cast<decltype(&cusolverDnDgesvd)>(dlsym(h, "cusolverDnDgesvd"));
+#define QB_SYM(field, name) api.field = reinterpret_cast<decltype(&name)>(dlsym(h, #name))
+  QB_SYM(createParams, cusolverDnCreateParams);
+  QB_SYM(destroyParams, cusolverDnDestroyParams);
+  QB_SYM(destroyGesvdjInfo, cusolverDnDestroyGesvdjInfo);
+  QB_SYM(gesvdpBufferSize, cusolverDnXgesvdp_bufferSize);
+  QB_SYM(gesvdp, cusolverDnXgesvdp);
+  QB_SYM(createGesvdjInfo, cusolverDnCreateGesvdjInfo);
+  QB_SYM(gesvdjSetTol, cusolverDnXgesvdjSetTolerance);
+  QB_SYM(gesvdjSetSweeps, cusolverDnXgesvdjSetMaxSweeps);
+  QB_SYM(gesvdjBufferSize, cusolverDnDgesvdj_bufferSize);
+  QB_SYM(gesvdj, cusolverDnDgesvdj);
+#undef QB_SYM
+  api.ok = api.create && api.destroy && api.setStream && api.gesvdBufferSize && api.gesvd && api.createParams &&
+           api.destroyParams && api.destroyGesvdjInfo &&
+           api.gesvdpBufferSize && api.gesvdp && api.createGesvdjInfo && api.gesvdjSetTol && api.gesvdjSetSweeps &&
+           api.gesvdjBufferSize && api.gesvdj;
+  return api;
+}
+
 }  // namespace
 
 struct qb_ctx_s {
@@ -92,13 +147,17 @@ struct qb_ctx_s {
   int64_t col_offset = 0, n_global = 0;
   ncclComm_t comm = nullptr;  // set on distributed contexts (any nranks >= 1)
 
-  DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status, Qf, Bf, Astage, Q32, B32;
+  DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status, Qf, Bf, Astage, Q32, B32,
+      Qbar32, W32;
   int64_t kcap = 0, ldq = 0, ldb = 0, qbar_rows = 0, bbar_cols = 0;
   double* h_scal = nullptr;  // pinned: [0] r2, [1] sum B^2, [2..3] spare
   int* h_status = nullptr;   // pinned
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evp[6] = {};  // phase events: sketch, B, downdate (begin/end)
   std::vector<qb_block_stats> stats;
+  int64_t last_m = 0, last_n = 0, last_k = -1;  // the last qb_factor (for rqb_svd); -1: none
+  DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
+  cusolverDnHandle_t solver = nullptr;
   int block_fallbacks = 0;
   const double* outQ = nullptr;
   const double* outB = nullptr;
@@ -362,10 +421,11 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
 }
 
 // ---------------------------------------------------------------- FP32 (3xTF32 tcgen05) GEMM
-// K-major boxes use the plain 128-byte swizzle; MN-major boxes (mn_major) the 32-byte-atom
-// variant that the MN-major TF32 descriptor expects.
+// K-major operand boxes use the plain 128-byte swizzle (SWIZZLE_128B), MN-major ones the
+// 32-byte-atom variant that the MN-major TF32 descriptor expects (SWIZZLE_128B_ATOM_32B); the
+// subtract-update's C tile is unswizzled (SWIZZLE_NONE).
 qb_status make_map_f32(qb_ctx ctx, CUtensorMap* map, const float* ptr, uint64_t inner, uint64_t outer, int64_t ld,
-                       uint32_t box_inner, uint32_t box_outer, bool mn_major) {
+                       uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * 4) & 15) != 0)
     return fail(ctx, QB_ERR_INVALID_ARG, "TMA operand not 16-byte aligned (ptr %p, ld %lld)", (const void*)ptr,
                 (long long)ld);
@@ -374,8 +434,7 @@ qb_status make_map_f32(qb_ctx ctx, CUtensorMap* map, const float* ptr, uint64_t 
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (%d)", (int)r);
   return QB_OK;
@@ -398,8 +457,9 @@ qb_status make_map3d_f32(qb_ctx ctx, CUtensorMap* map, const float* ptr, uint64_
 }
 
 template <int LAYOUT, int BN, int EPI>
-qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const TfParams& p, int splits) {
-  using Cfg = TfCfg<BN>;
+qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                      const TfParams& p, int splits) {
+  using Cfg = TfCfg<BN, EPI == TF_SUB_COL>;
   auto kern = gemm_tf32_kernel<LAYOUT, BN, EPI>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -407,21 +467,21 @@ qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, 
     attr_done = true;
   }
   dim3 grid(p.tiles_m * p.tiles_n, splits);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, p);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tc, p);
   return check_launch(ctx, "gemm_tf32");
 }
 
 template <int BN>
 qb_status dispatch_tf(qb_ctx ctx, int layout, int epi, const CUtensorMap& ta, const CUtensorMap& tb,
-                      const TfParams& p, int splits) {
+                      const CUtensorMap& tc, const TfParams& p, int splits) {
   if (layout == GEMM_NN) {
-    if (epi == TF_STORE_COL) return launch_tf_t<GEMM_NN, BN, TF_STORE_COL>(ctx, ta, tb, p, splits);
-    if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_NN, BN, TF_STORE_ROW>(ctx, ta, tb, p, splits);
-    return launch_tf_t<GEMM_NN, BN, TF_SUB_COL>(ctx, ta, tb, p, splits);
+    if (epi == TF_STORE_COL) return launch_tf_t<GEMM_NN, BN, TF_STORE_COL>(ctx, ta, tb, tc, p, splits);
+    if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_NN, BN, TF_STORE_ROW>(ctx, ta, tb, tc, p, splits);
+    return launch_tf_t<GEMM_NN, BN, TF_SUB_COL>(ctx, ta, tb, tc, p, splits);
   }
-  if (epi == TF_STORE_COL) return launch_tf_t<GEMM_TN, BN, TF_STORE_COL>(ctx, ta, tb, p, splits);
-  if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_TN, BN, TF_STORE_ROW>(ctx, ta, tb, p, splits);
-  return launch_tf_t<GEMM_TN, BN, TF_SUB_COL>(ctx, ta, tb, p, splits);
+  if (epi == TF_STORE_COL) return launch_tf_t<GEMM_TN, BN, TF_STORE_COL>(ctx, ta, tb, tc, p, splits);
+  if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_TN, BN, TF_STORE_ROW>(ctx, ta, tb, tc, p, splits);
+  return launch_tf_t<GEMM_TN, BN, TF_SUB_COL>(ctx, ta, tb, tc, p, splits);
 }
 
 // FP32 operands, 3xTF32 products with FP32 accumulation.  epi TF_STORE_COL / TF_STORE_ROW
@@ -453,16 +513,19 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
     p.a3d = M % 32 == 0;
     p.b3d = N % 32 == 0 && N >= bn;
     if (p.a3d) QB_TRY(make_map3d_f32(ctx, &ta, A, M, K, lda, TF_BM / 32));
-    else QB_TRY(make_map_f32(ctx, &ta, A, M, K, lda, 32, TF_BK, true));
+    else QB_TRY(make_map_f32(ctx, &ta, A, M, K, lda, 32, TF_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
     if (p.b3d) QB_TRY(make_map3d_f32(ctx, &tb, B, N, K, ldb, bn / 32));
-    else QB_TRY(make_map_f32(ctx, &tb, B, N, K, ldb, 32, TF_BK, true));
+    else QB_TRY(make_map_f32(ctx, &tb, B, N, K, ldb, 32, TF_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   } else {
-    QB_TRY(make_map_f32(ctx, &ta, A, K, M, lda, TF_BK, TF_BM, false));
-    QB_TRY(make_map_f32(ctx, &tb, B, K, N, ldb, TF_BK, bn, false));
+    QB_TRY(make_map_f32(ctx, &ta, A, K, M, lda, TF_BK, TF_BM, CU_TENSOR_MAP_SWIZZLE_128B));
+    QB_TRY(make_map_f32(ctx, &tb, B, K, N, ldb, TF_BK, bn, CU_TENSOR_MAP_SWIZZLE_128B));
   }
+  CUtensorMap tc = ta;
+  if (epi == TF_SUB_COL)
+    QB_TRY(make_map_f32(ctx, &tc, static_cast<const float*>(C), M, N, ldc, TF_BM, bn, CU_TENSOR_MAP_SWIZZLE_NONE));
   auto run = [&](int e, int s) -> qb_status {
-    if (bn == 64) return dispatch_tf<64>(ctx, layout, e, ta, tb, p, s);
-    if (bn == 128) return dispatch_tf<128>(ctx, layout, e, ta, tb, p, s);
+    if (bn == 64) return dispatch_tf<64>(ctx, layout, e, ta, tb, tc, p, s);
+    if (bn == 128) return dispatch_tf<128>(ctx, layout, e, ta, tb, tc, p, s);
     return fail(ctx, QB_ERR_INVALID_ARG, "QB_TF_BN must be 64 or 128");
   };
 
@@ -621,6 +684,18 @@ qb_status grow_factors(qb_ctx ctx, int64_t m, int64_t n, int64_t need, int64_t k
                             ctx->stream));
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  if (ctx->dtype == QB_F32) {  // FP32 copy of Q̄ (the published Q and the residual GEMMs' operand)
+    DevBuf nq32;
+    QB_CUDA(cudaMalloc(&nq32.p, sizeof(float) * (size_t)(ldq * cap)));
+    nq32.bytes = sizeof(float) * (size_t)(ldq * cap);
+    if (ctx->Qbar32.p && ctx->qbar_rows == m && ctx->bbar_cols == n && ctx->kcap > 0) {
+      QB_CUDA(cudaMemcpyAsync(nq32.p, ctx->Qbar32.p, sizeof(float) * (size_t)(ldq * ctx->kcap),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+      QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    if (ctx->Qbar32.p) QB_CUDA(cudaFree(ctx->Qbar32.p));
+    ctx->Qbar32 = nq32;
+  }
   if (ctx->Qbar.p) QB_CUDA(cudaFree(ctx->Qbar.p));
   if (ctx->Bbar.p) QB_CUDA(cudaFree(ctx->Bbar.p));
   ctx->Qbar = nq;
@@ -680,12 +755,10 @@ qb_status publish_outputs(qb_ctx ctx, int64_t m, int64_t n, int64_t k, const voi
   const void* Qp = ctx->Qbar.p;
   const void* Bp = ctx->Bbar.p;
   if (ctx->dtype == QB_F32) {
-    QB_TRY(ensure(ctx, ctx->Qf, sizeof(float) * (size_t)(ctx->ldq * std::max<int64_t>(k, 1))));
     QB_TRY(ensure(ctx, ctx->Bf, sizeof(float) * (size_t)(ctx->ldb * std::max<int64_t>(k, 1))));
-    QB_TRY(launch_convert(ctx, ctx->Qbar.d(), ctx->ldq, m, k, static_cast<float*>(ctx->Qf.p), ctx->ldq));
     QB_TRY(launch_convert(ctx, ctx->Bbar.d(), ctx->ldb, n, k, static_cast<float*>(ctx->Bf.p), ctx->ldb));
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
-    Qp = ctx->Qf.p;
+    Qp = ctx->Qbar32.p;  // RN_32 of each finished Q_i, kept block by block
     Bp = ctx->Bf.p;
   }
   if (Q_out) *Q_out = Qp;
@@ -765,7 +838,9 @@ void qb_destroy(qb_ctx ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->Awork, &ctx->Qbar, &ctx->Bbar, &ctx->Om, &ctx->Y,     &ctx->T1,    &ctx->Z,   &ctx->Zt,
                     &ctx->G,     &ctx->L,    &ctx->Rinv, &ctx->W,  &ctx->P,     &ctx->parts, &ctx->scal, &ctx->status,
-                    &ctx->Qf,    &ctx->Bf,   &ctx->Astage, &ctx->Q32,  &ctx->B32};
+                    &ctx->Qf,    &ctx->Bf,   &ctx->Astage, &ctx->Q32,  &ctx->B32, &ctx->Qbar32, &ctx->W32,
+                    &ctx->QB,    &ctx->R,    &ctx->Usv,    &ctx->Vsv,  &ctx->Ssv, &ctx->Wsv,    &ctx->Ut,
+                    &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -775,6 +850,7 @@ void qb_destroy(qb_ctx ctx) {
   for (auto& e : ctx->evp)
     if (e) cudaEventDestroy(e);
   if (ctx->comm) nccl().commDestroy(ctx->comm);
+  if (ctx->solver) solver().destroy(ctx->solver);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -875,10 +951,173 @@ qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_
   return QB_OK;
 }
 
-qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U, int64_t* ldu, const void** S, const void** V,
-                  int64_t* ldv) {
-  (void)kkeep; (void)U; (void)ldu; (void)S; (void)V; (void)ldv;
-  return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd is the NEXT-1 row; not built yet");
+qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_out, const void** S_out,
+                  const void** V_out, int64_t* ldv_out) {
+  // QB -> partial SVD: B̄ = Û D V^*, U = Q̄ Û.  B̄^T (n x k) = Q_B R by block
+  // Gram-Schmidt (two projections) + CholeskyQR2 per 256 columns; R = Q_B^T B̄^T; dgesvd of the
+  // k x k R = Ũ D Ṽ^T; then B̄ = R^T Q_B^T = Ṽ D (Q_B Ũ)^T, so Û = Ṽ, V = Q_B Ũ, U = Q̄ Ṽ.
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  if (ctx->last_k < 0) return fail(ctx, QB_ERR_INVALID_ARG, "rqb_svd: no factorization to convert");
+  if (ctx->nranks > 1) return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: column-sharded B̄ (distributed) not supported");
+  if (!solver().ok) return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: libcusolver.so.11 not loadable");
+  const int64_t m = ctx->last_m, n = ctx->last_n, k = ctx->last_k;
+  const int64_t kk = (kkeep > 0 && kkeep < k) ? kkeep : k;
+  QB_CUDA(cudaSetDevice(ctx->device));
+  if (k == 0) {
+    if (U_out) *U_out = nullptr;
+    if (S_out) *S_out = nullptr;
+    if (V_out) *V_out = nullptr;
+    if (ldu_out) *ldu_out = round_up(m, 16);
+    if (ldv_out) *ldv_out = round_up(n, 16);
+    return QB_OK;
+  }
+  if (k > INT32_MAX / 4) return fail(ctx, QB_ERR_INVALID_ARG, "rqb_svd: k too large");
+  const int64_t ldn = round_up(n, 16), ldm = round_up(m, 16), ldk = round_up(k, 16), bp = round_up(kMaxB, 16);
+  QB_TRY(ensure(ctx, ctx->QB, sizeof(double) * (size_t)(ldn * k)));
+  QB_TRY(ensure(ctx, ctx->R, sizeof(double) * (size_t)(ldk * k)));
+  QB_TRY(ensure(ctx, ctx->Ut, sizeof(double) * (size_t)(ldk * k)));
+  QB_TRY(ensure(ctx, ctx->Vt, sizeof(double) * (size_t)(ldk * k)));
+  QB_TRY(ensure(ctx, ctx->Ssv, sizeof(double) * (size_t)ldk));
+  QB_TRY(ensure(ctx, ctx->Wsv, sizeof(double) * (size_t)(ldk * bp)));
+  QB_TRY(ensure(ctx, ctx->Usv, sizeof(double) * (size_t)(ldm * kk)));
+  QB_TRY(ensure(ctx, ctx->Vsv, sizeof(double) * (size_t)(ldn * kk)));
+  QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(std::max(m, n), 16) * kMaxB)));
+  QB_TRY(ensure(ctx, ctx->G, sizeof(double) * bp * bp));
+  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (bp * bp + 8 * 32 * 32)));
+  QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * bp * bp));
+  QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)(16 * ctx->num_sms)));
+  double* QBm = ctx->QB.d();
+  const double* Bbar = ctx->Bbar.d();  // row-major k x n (ld ldb) == B̄^T column-major n x k
+  QB_TRY(reset_flags(ctx));
+
+  // 1. Q_B = orth(B̄^T), 256 columns at a time
+  for (int64_t j0 = 0; j0 < k; j0 += kMaxB) {
+    const int64_t w = std::min<int64_t>(kMaxB, k - j0);
+    double* X = QBm + j0 * ldn;
+    QB_CUDA(cudaMemcpy2DAsync(X, ldn * 8, Bbar + j0 * ctx->ldb, ctx->ldb * 8, n * 8, w, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+    for (int pass = 0; pass < 2 && j0 > 0; ++pass) {  // X -= Q_B (Q_B^T X), twice
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)j0, (int)w, (int)n, QBm, ldn, X, ldn, ctx->Wsv.d(), bp, false,
+                  nullptr));
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)n, (int)w, (int)j0, QBm, ldn, ctx->Wsv.d(), bp, X, ldn, false,
+                  nullptr));
+    }
+    QB_TRY(cholqr2(ctx, X, ldn, X, ldn, n, (int)w));
+  }
+  // 2. R = Q_B^T B̄^T (k x k, column-major)
+  QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)k, (int)k, (int)n, QBm, ldn, Bbar, ctx->ldb, ctx->R.d(), ldk, false,
+              nullptr));
+  // 3. R = Ũ D Ṽ^T (cuSOLVER dgesvd: Ũ -> Ut, Ṽ^T -> Vt, both column-major ld ldk)
+  if (!ctx->solver) {
+    if (solver().create(&ctx->solver) != CUSOLVER_STATUS_SUCCESS) {
+      ctx->solver = nullptr;
+      return fail(ctx, QB_ERR_CUDA, "cusolverDnCreate failed");
+    }
+  }
+  if (solver().setStream(ctx->solver, ctx->stream) != CUSOLVER_STATUS_SUCCESS)
+    return fail(ctx, QB_ERR_CUDA, "cusolverDnSetStream failed");
+  // method: 0 = dgesvd (QR iteration), 1 = gesvdj (Jacobi), 2 = Xgesvdp (polar decomposition);
+  // QB_SVD selects, default below.  Ut <- Ũ (column-major); Vt <- Ṽ^T (column-major) = Ṽ row-major.
+  static const int method = getenv("QB_SVD") ? atoi(getenv("QB_SVD")) : 2;
+  int* dinfo = nullptr;
+  if (method == 0) {
+    int lwork = 0;
+    if (solver().gesvdBufferSize(ctx->solver, (int)k, (int)k, &lwork) != CUSOLVER_STATUS_SUCCESS)
+      return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvd_bufferSize failed");
+    QB_TRY(ensure(ctx, ctx->Swork, sizeof(double) * (size_t)(lwork + ldk) + 64));
+    double* work = ctx->Swork.d();
+    dinfo = reinterpret_cast<int*>(work + lwork + ldk);
+    if (solver().gesvd(ctx->solver, 'S', 'S', (int)k, (int)k, ctx->R.d(), (int)ldk, ctx->Ssv.d(), ctx->Ut.d(),
+                       (int)ldk, ctx->Vt.d(), (int)ldk, work, lwork, work + lwork, dinfo) != CUSOLVER_STATUS_SUCCESS)
+      return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvd failed");
+  } else {
+    // V-returning methods write Ṽ (column-major) into Usv's storage first, transposed below
+    QB_TRY(ensure(ctx, ctx->Usv, sizeof(double) * (size_t)std::max(ldm * kk, ldk * k)));
+    double* Vcol = ctx->Usv.d();
+    if (method == 1) {
+      gesvdjInfo_t info = nullptr;
+      if (solver().createGesvdjInfo(&info) != CUSOLVER_STATUS_SUCCESS)
+        return fail(ctx, QB_ERR_CUDA, "cusolverDnCreateGesvdjInfo failed");
+      solver().gesvdjSetTol(info, 1e-15);
+      solver().gesvdjSetSweeps(info, 100);
+      int lwork = 0;
+      if (solver().gesvdjBufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 1, (int)k, (int)k, ctx->R.d(), (int)ldk,
+                                    ctx->Ssv.d(), ctx->Ut.d(), (int)ldk, Vcol, (int)ldk, &lwork,
+                                    info) != CUSOLVER_STATUS_SUCCESS)
+        return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvdj_bufferSize failed");
+      QB_TRY(ensure(ctx, ctx->Swork, sizeof(double) * (size_t)lwork + 64));
+      double* work = ctx->Swork.d();
+      dinfo = reinterpret_cast<int*>(work + lwork);
+      const cusolverStatus_t st = solver().gesvdj(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 1, (int)k, (int)k,
+                                                  ctx->R.d(), (int)ldk, ctx->Ssv.d(), ctx->Ut.d(), (int)ldk, Vcol,
+                                                  (int)ldk, work, lwork, dinfo, info);
+      QB_CUDA(cudaStreamSynchronize(ctx->stream));
+      solver().destroyGesvdjInfo(info);
+      if (st != CUSOLVER_STATUS_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvdj failed");
+    } else {
+      cusolverDnParams_t params = nullptr;
+      if (solver().createParams(&params) != CUSOLVER_STATUS_SUCCESS)
+        return fail(ctx, QB_ERR_CUDA, "cusolverDnCreateParams failed");
+      size_t dbytes = 0, hbytes = 0;
+      if (solver().gesvdpBufferSize(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 1, k, k, CUDA_R_64F, ctx->R.d(),
+                                    ldk, CUDA_R_64F, ctx->Ssv.d(), CUDA_R_64F, ctx->Ut.d(), ldk, CUDA_R_64F, Vcol,
+                                    ldk, CUDA_R_64F, &dbytes, &hbytes) != CUSOLVER_STATUS_SUCCESS)
+        return fail(ctx, QB_ERR_CUDA, "cusolverDnXgesvdp_bufferSize failed");
+      QB_TRY(ensure(ctx, ctx->Swork, dbytes + 64));
+      dinfo = reinterpret_cast<int*>(static_cast<char*>(ctx->Swork.p) + ((dbytes + 15) / 16) * 16);
+      std::vector<char> hwork(std::max<size_t>(hbytes, 1));
+      double err_sigma = 0.0;
+      const cusolverStatus_t st =
+          solver().gesvdp(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 1, k, k, CUDA_R_64F, ctx->R.d(), ldk,
+                          CUDA_R_64F, ctx->Ssv.d(), CUDA_R_64F, ctx->Ut.d(), ldk, CUDA_R_64F, Vcol, ldk, CUDA_R_64F,
+                          ctx->Swork.p, dbytes, hwork.data(), hbytes, dinfo, &err_sigma);
+      QB_CUDA(cudaStreamSynchronize(ctx->stream));  // hwork is host scratch of this call
+      solver().destroyParams(params);
+      if (st != CUSOLVER_STATUS_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cusolverDnXgesvdp failed");
+    }
+    dim3 grid((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
+    transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(Vcol, ldk, k, k, ctx->Vt.d(), ldk);
+    QB_TRY(check_launch(ctx, "transpose"));
+  }
+  ++ctx->launches;
+  // 4. U = Q̄ Ṽ: Ṽ^T column-major is Ṽ row-major (the NN kernel's N-contiguous operand)
+  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)kk, (int)k, ctx->Qbar.d(), ctx->ldq, ctx->Vt.d(), ldk,
+              ctx->Usv.d(), ldm, false, nullptr));
+  //    V = Q_B Ũ: Ũ^T row-major = Ũ transposed into R's storage
+  {
+    dim3 grid((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
+    transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Ut.d(), ldk, k, k, ctx->R.d(), ldk);
+    QB_TRY(check_launch(ctx, "transpose"));
+  }
+  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)n, (int)kk, (int)k, QBm, ldn, ctx->R.d(), ldk, ctx->Vsv.d(), ldn,
+              false, nullptr));
+  int hinfo = 0;
+  QB_CUDA(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->h_status[4]) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "rqb_svd: CholeskyQR of B^T failed");
+  if (hinfo != 0) return fail(ctx, QB_ERR_CUDA, "rqb_svd: dgesvd info = %d", hinfo);
+  const void* Up = ctx->Usv.p;
+  const void* Sp = ctx->Ssv.p;
+  const void* Vp = ctx->Vsv.p;
+  if (ctx->dtype == QB_F32) {
+    QB_TRY(ensure(ctx, ctx->Usv32, sizeof(float) * (size_t)(ldm * kk)));
+    QB_TRY(ensure(ctx, ctx->Vsv32, sizeof(float) * (size_t)(ldn * kk)));
+    QB_TRY(ensure(ctx, ctx->Ssv32, sizeof(float) * (size_t)ldk));
+    QB_TRY(launch_convert(ctx, ctx->Usv.d(), ldm, m, kk, static_cast<float*>(ctx->Usv32.p), ldm));
+    QB_TRY(launch_convert(ctx, ctx->Vsv.d(), ldn, n, kk, static_cast<float*>(ctx->Vsv32.p), ldn));
+    QB_TRY(launch_convert(ctx, ctx->Ssv.d(), 1, 1, kk, static_cast<float*>(ctx->Ssv32.p), 1));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    Up = ctx->Usv32.p;
+    Sp = ctx->Ssv32.p;
+    Vp = ctx->Vsv32.p;
+  }
+  if (U_out) *U_out = Up;
+  if (ldu_out) *ldu_out = ldm;
+  if (S_out) *S_out = Sp;
+  if (V_out) *V_out = Vp;
+  if (ldv_out) *ldv_out = ldn;
+  return QB_OK;
 }
 
 qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, double eps, int64_t b, int q,
@@ -961,7 +1200,11 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   ctx->outQ = nullptr;
   ctx->outB = nullptr;
   if (resid_out) *resid_out = std::sqrt(r2_0);
+  ctx->last_k = -1;
   if (r2_0 <= eps2) {
+    ctx->last_m = m;
+    ctx->last_n = n;
+    ctx->last_k = 0;
     QB_TRY(grow_factors(ctx, m, n, 1, std::max<int64_t>(kmax_eff, 1)));
     return publish_outputs(ctx, m, n, 0, Q_out, ldq_out, B_out, ldb_out);
   }
@@ -1031,20 +1274,34 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
+    float* Qbar32 = static_cast<float*>(ctx->Qbar32.p);
+    float* Qi32 = is_f32 ? Qbar32 + ell * ctx->ldq : nullptr;
     if (ell > 0 && !(flags & QB_NO_REPROJ)) {
       QB_TRY(ensure(ctx, ctx->W, sizeof(double) * (size_t)(ell * bp)));
-      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)ell, (int)w, (int)m, Qbar, ctx->ldq, Qi, ctx->ldq, ctx->W.d(), bp,
-                  false, nullptr));
-      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)ell, Qbar, ctx->ldq, ctx->W.d(), bp, Qi, ctx->ldq,
-                  false, nullptr));
+      if (is_f32) {  // on the FP32 copies: W = Q̄^T Q_i, Q_i -= Q̄ W (3xTF32), then orth in FP64
+        QB_TRY(ensure(ctx, ctx->W32, sizeof(float) * (size_t)(ell * bp)));
+        QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Qi32, ctx->ldq));
+        QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)ell, (int)w, (int)m, Qbar32, ctx->ldq, Qi32, ctx->ldq,
+                       ctx->W.d(), bp, false, nullptr));
+        QB_TRY(launch_convert(ctx, ctx->W.d(), bp, w, ell, static_cast<float*>(ctx->W32.p), bp));
+        QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)w, (int)ell, Qbar32, ctx->ldq,
+                       static_cast<const float*>(ctx->W32.p), bp, Qi32, ctx->ldq, false, nullptr));
+        QB_TRY(launch_convert(ctx, static_cast<const float*>(Qi32), ctx->ldq, m, w, Qi, ctx->ldq));
+      } else {
+        QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)ell, (int)w, (int)m, Qbar, ctx->ldq, Qi, ctx->ldq, ctx->W.d(),
+                    bp, false, nullptr));
+        QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)ell, Qbar, ctx->ldq, ctx->W.d(), bp, Qi,
+                    ctx->ldq, false, nullptr));
+      }
       QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w));
     }
+    // FP32 contexts: Q̄32_i = RN_32(Q_i), the factor the caller receives and the residual's GEMMs use
+    if (is_f32) QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Qi32, ctx->ldq));
     // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
     int64_t nb_parts = 0;
     QB_CUDA(cudaEventRecord(ctx->evp[2], ctx->stream));
-    if (is_f32) {  // the residual's GEMMs take Q_i rounded to FP32: the factor the caller receives
-      QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Q32, ldm));
-      QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)w, (int)n, (int)m, Q32, ldm, A32, ldA, Bi, ctx->ldb, true,
+    if (is_f32) {
+      QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)w, (int)n, (int)m, Qi32, ctx->ldq, A32, ldA, Bi, ctx->ldb, true,
                      &nb_parts));
     } else {
       QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)w, (int)n, (int)m, Qi, ctx->ldq, A, ldA, Bi, ctx->ldb, true,
@@ -1057,7 +1314,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_CUDA(cudaEventRecord(ctx->evp[4], ctx->stream));
     if (is_f32) {  // A -= RN32(Q_i) RN32(B_i): the residual of the factors the caller receives
       QB_TRY(launch_convert(ctx, static_cast<const double*>(Bi), ctx->ldb, n, w, B32, ctx->ldb));
-      QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)n, (int)w, Q32, ldm, B32, ctx->ldb, A32, ldA, true,
+      QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)n, (int)w, Qi32, ctx->ldq, B32, ctx->ldb, A32, ldA, true,
                      &na_parts));
     } else {
       QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)n, (int)w, Qi, ctx->ldq, Bi, ctx->ldb, A, ldA, true,
@@ -1097,6 +1354,9 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     if (r2 <= eps2) break;  // line (11): stop test (R1, R4)
   }
   *k_out = ell;
+  ctx->last_m = m;
+  ctx->last_n = n;
+  ctx->last_k = ell;
   QB_TRY(publish_outputs(ctx, m, n, ell, Q_out, ldq_out, B_out, ldb_out));
   if (resid_out) *resid_out = std::sqrt(r2);
   return r2 <= eps2 ? QB_OK : QB_NOT_CONVERGED;
