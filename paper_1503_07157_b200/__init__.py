@@ -13,7 +13,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqb.so")
+LIB_PATH = os.environ.get("QB_LIB_PATH") or os.path.join(_HERE, "libqb.so")  # override: experiments only
 
 QB_OK = 0
 QB_NOT_CONVERGED = 1

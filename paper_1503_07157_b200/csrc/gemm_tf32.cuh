@@ -16,15 +16,19 @@
 // into FP32 registers with IEEE rounding; two TMEM buffers let the MMAs of chunk c+1 run while
 // chunk c is drained.
 //
-// CTA tile 128 x BN, k-tile 32 floats (one 128-byte swizzle row); 10 warps:
+// Persistent CTAs (one per SM) walk the work units (tile x K-split) statically; CTA tile
+// 128 x BN, k-tile 32 floats (one 128-byte swizzle row); 11 warps:
 //   warp 0      TMA producer (one thread): raw FP32 tiles -> the stage's "hi" buffers
 //   warp 1      TMEM allocator + MMA issuer (one thread): 4 k-steps x 3 tcgen05.mma per stage
 //   warps 2..5  split the stage in place (hi = RN_tf32(x), lo = x - hi)
-//   warps 6..9  drain TMEM chunks into register accumulators, then the epilogue
-//               (warp w reads TMEM lanes 32 (w % 4) .. + 31 = tile rows)
+//   warps 6..9  drain TMEM chunks into register accumulators, then the epilogue of the unit
+//               (warp w reads TMEM lanes 32 (w % 4) .. + 31 = tile rows) while the MMAs of the
+//               next unit run in the other TMEM buffer
+//   warp 10     TF_SUB_COL only: TMA-loads the C tile, 128 x 32 at a time, into a ring that
+//               the epilogue updates in place and TMA-stores back
 // Barriers per stage: full (TMA bytes landed), conv (128 splitters done), empty (MMAs done,
-// tcgen05.commit); per TMEM buffer: acc_full (chunk's MMAs done), acc_empty (drained).  One
-// tile per CTA; split-K over blockIdx.y as in the FP64 kernel.
+// tcgen05.commit); per TMEM buffer: acc_full (chunk's MMAs done), acc_empty (drained); per C
+// slot: cfull (loaded), cempty (stored).
 //
 // Operand layouts in shared memory (UMMA canonical 128B-swizzle layouts):
 //   K-major (TN): box {32 k, rows}: row r at r*128 B, 8-row groups at 1024 B (SBO), the k-th
@@ -40,7 +44,12 @@ namespace qbk {
 constexpr int TF_BM = 128;
 constexpr int TF_BK = 32;
 constexpr int TF_PROMO = 4;       // k-tiles (128 k) per TMEM accumulation chunk
-constexpr int TF_THREADS = 320;   // producer, MMA, 4 splitter warps, 4 promoter/epilogue warps
+constexpr int TF_THREADS = 352;   // 11 warps, see the header comment
+constexpr int TF_CSUB = 32;       // TF_SUB_COL: C streams through shared memory 128 x 32 at a time
+#ifndef QB_TF_CSLOTS
+#define QB_TF_CSLOTS 2
+#endif
+constexpr int TF_CSLOTS = QB_TF_CSLOTS;  // ring of C sub-tiles
 
 enum TfEpi { TF_STORE_COL = 0, TF_STORE_ROW = 1, TF_SUB_COL = 2 };
 
@@ -49,11 +58,12 @@ struct TfParams {
   int tiles_m, tiles_n;
   int nkt;            // ceil(K / 32)
   int kt_per_split;
+  int splits;         // work unit u: split u / tiles, tile u % tiles
   int raster_m_fast;
   void* C;            // STORE_*: double output (or split partials); SUB_COL: float C
   int64_t ldc;
   int64_t split_stride;
-  double* norm_partials;  // SUB_COL: per-CTA sum of squares of the new C (FP64)
+  double* norm_partials;  // SUB_COL: per-CTA sum of squares of the new C (FP64), one per CTA
   int a3d, b3d;       // NN: one 3D TMA per operand per stage ({32, K, rows/32} view)
 };
 
@@ -64,15 +74,40 @@ struct TfCfg {
   static constexpr int B_BYTES = BN * TF_BK * 4;
   static constexpr int HI_BYTES = A_BYTES + B_BYTES;   // [A_hi][B_hi], then [A_lo][B_lo]
   static constexpr int STAGE_BYTES = 2 * HI_BYTES;
-  // TF_SUB_COL keeps its whole C tile (128 x BN floats, column-major) in shared memory: TMA-
-  // loaded at tile start, updated in place, TMA-stored back
-  static constexpr int C_BYTES = SUB ? TF_BM * BN * 4 : 0;
-  static constexpr int STAGES = (200 * 1024 - C_BYTES) / STAGE_BYTES;
+  static constexpr int CSUB_BYTES = TF_BM * TF_CSUB * 4;
+  static constexpr int C_BYTES = SUB ? TF_CSLOTS * CSUB_BYTES : 0;
+  static constexpr int STAGES = (224 * 1024 - C_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers (chunk c in buffer c & 1)
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + C_BYTES + (3 * STAGES + 5) * 8 + 64;
+  static constexpr int SMEM_BYTES =
+      1024 + STAGES * STAGE_BYTES + C_BYTES + (3 * STAGES + 4 + 2 * TF_CSLOTS) * 8 + 64;
   static_assert(STAGES >= 2, "at least double buffering");
   static_assert(BN == 64 || BN == 128, "BN: register accumulators of the promoter warps");
 };
+
+// Work unit u of a persistent CTA: tile origin and k-tile range.
+struct TfUnit {
+  int m0, n0, kt0, nk, split;
+};
+
+__device__ __forceinline__ TfUnit tf_unit(const TfParams& p, int u, int bn) {
+  const int tiles = p.tiles_m * p.tiles_n;
+  TfUnit r;
+  r.split = u / tiles;
+  const int t = u - r.split * tiles;
+  int tm, tn;
+  if (p.raster_m_fast) {
+    tm = t % p.tiles_m;
+    tn = t / p.tiles_m;
+  } else {
+    tn = t % p.tiles_n;
+    tm = t / p.tiles_n;
+  }
+  r.m0 = tm * TF_BM;
+  r.n0 = tn * bn;
+  r.kt0 = r.split * p.kt_per_split;
+  r.nk = max(min(p.nkt, r.kt0 + p.kt_per_split) - r.kt0, 0);
+  return r;
+}
 
 // Shared-memory matrix descriptor: layout 2 = SWIZZLE_128B (K-major operands), 1 =
 // SWIZZLE_128B_BASE32B (MN-major 32-bit operands: 32-byte granules of each 128-byte row XORed
@@ -174,30 +209,19 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* sC = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);  // SUB: [BN][128]
+  float* sC = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);  // SUB: ring of [32][128] sub-tiles
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::C_BYTES);
   uint64_t* conv = full + STAGES;
   uint64_t* empty = conv + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
-  uint64_t* cbar = acc_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 1);
+  uint64_t* cfull = acc_empty + 2;      // [TF_CSLOTS]
+  uint64_t* cempty = cfull + TF_CSLOTS; // [TF_CSLOTS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + TF_CSLOTS);
   double* red = reinterpret_cast<double*>(tmem_slot + 2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int tm, tn;
-  if (p.raster_m_fast) {
-    tm = blockIdx.x % p.tiles_m;
-    tn = blockIdx.x / p.tiles_m;
-  } else {
-    tn = blockIdx.x % p.tiles_n;
-    tm = blockIdx.x / p.tiles_n;
-  }
-  const int m0 = tm * TF_BM, n0 = tn * BN;
-  const int kt0 = blockIdx.y * p.kt_per_split;
-  const int kt1 = min(p.nkt, kt0 + p.kt_per_split);
-  const int nk = max(kt1 - kt0, 0);
-  const int nchunks = (nk + TF_PROMO - 1) / TF_PROMO;
+  const int units = p.tiles_m * p.tiles_n * p.splits;
 
   if (tid == 0) {
     tma_prefetch_desc(&tA);
@@ -212,7 +236,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 128);
     }
-    mbar_init(cbar, 1);
+    for (int s = 0; s < TF_CSLOTS; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -226,19 +253,18 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
+    // ---------------------------------------------------------------- operand producer
     if (lane == 0) {
-      if (SUB) {  // the C tile travels beside the operands
-        tma_prefetch_desc(&tC);
-        mbar_arrive_expect_tx(cbar, Cfg::C_BYTES);
-        tma_load_2d(sC, &tC, cbar, m0, n0);
-      }
-      for (int j = 0; j < nk; ++j) {
-        const int slot = j % STAGES;
-        if (j >= STAGES) mbar_wait(&empty[slot], ((j / STAGES) - 1) & 1);
-        uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
-        tf_issue_stage<LAYOUT, BN>(&tA, &tB, st, st + Cfg::A_BYTES, &full[slot], m0, n0, (kt0 + j) * TF_BK, p.a3d,
-                                   p.b3d);
+      int j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const TfUnit w = tf_unit(p, u, BN);
+        for (int kt = 0; kt < w.nk; ++kt, ++j) {
+          const int slot = j % STAGES;
+          if (j >= STAGES) mbar_wait(&empty[slot], ((j / STAGES) - 1) & 1);
+          uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
+          tf_issue_stage<LAYOUT, BN>(&tA, &tB, st, st + Cfg::A_BYTES, &full[slot], w.m0, w.n0, (w.kt0 + kt) * TF_BK,
+                                     p.a3d, p.b3d);
+        }
       }
     }
   } else if (warp == 1) {
@@ -251,156 +277,200 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
       constexpr uint32_t SBO = LAYOUT == 0 ? 512u : 1024u;
       constexpr uint32_t LT = LAYOUT == 0 ? 1u : 2u;
       constexpr uint32_t KSTEP = LAYOUT == 0 ? 64u : 2u;  // descriptor units (16 B) per K=8 slice
-      for (int j = 0; j < nk; ++j) {
-        const int slot = j % STAGES;
-        const int c = j / TF_PROMO, b = c & 1;
-        const bool first = (j % TF_PROMO) == 0;
-        // a chunk starts in accumulator buffer b once the promoters have drained it
-        if (first && c >= 2) mbar_wait(&acc_empty[b], ((c >> 1) - 1) & 1);
-        mbar_wait(&conv[slot], (j / STAGES) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tacc = tmem_base + static_cast<uint32_t>(b * BN);
-        const uint32_t a_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES);
-        const uint32_t b_hi = a_hi + Cfg::A_BYTES;
-        const uint64_t dAh = umma_desc(a_hi, LBO, SBO, LT), dBh = umma_desc(b_hi, LBO, SBO, LT);
-        const uint64_t dAl = umma_desc(a_hi + Cfg::HI_BYTES, LBO, SBO, LT);
-        const uint64_t dBl = umma_desc(b_hi + Cfg::HI_BYTES, LBO, SBO, LT);
+      int j = 0, c = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int nk = tf_unit(p, u, BN).nk;
+        uint32_t tacc = tmem_base;
+        for (int kt = 0; kt < nk; ++kt, ++j) {
+          const int slot = j % STAGES;
+          const bool first = (kt % TF_PROMO) == 0;
+          if (first) {
+            // chunk c goes to accumulator buffer c & 1 once the promoters have drained it
+            const int b = c & 1;
+            if (c >= 2) mbar_wait(&acc_empty[b], ((c >> 1) - 1) & 1);
+            tacc = tmem_base + static_cast<uint32_t>(b * BN);
+          }
+          mbar_wait(&conv[slot], (j / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES);
+          const uint32_t b_hi = a_hi + Cfg::A_BYTES;
+          const uint64_t dAh = umma_desc(a_hi, LBO, SBO, LT), dBh = umma_desc(b_hi, LBO, SBO, LT);
+          const uint64_t dAl = umma_desc(a_hi + Cfg::HI_BYTES, LBO, SBO, LT);
+          const uint64_t dBl = umma_desc(b_hi + Cfg::HI_BYTES, LBO, SBO, LT);
 #pragma unroll
-        for (int kk = 0; kk < TF_BK / 8; ++kk) {
-          const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
-          umma_tf32(tacc, dAh + adv, dBh + adv, idesc, (!first || kk > 0) ? 1u : 0u);
-          umma_tf32(tacc, dAh + adv, dBl + adv, idesc, 1u);
-          umma_tf32(tacc, dAl + adv, dBh + adv, idesc, 1u);
+          for (int kk = 0; kk < TF_BK / 8; ++kk) {
+            const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
+            umma_tf32(tacc, dAh + adv, dBh + adv, idesc, (!first || kk > 0) ? 1u : 0u);
+            umma_tf32(tacc, dAh + adv, dBl + adv, idesc, 1u);
+            umma_tf32(tacc, dAl + adv, dBh + adv, idesc, 1u);
+          }
+          umma_commit(&empty[slot]);
+          if ((kt % TF_PROMO) == TF_PROMO - 1 || kt == nk - 1) {
+            umma_commit(&acc_full[c & 1]);
+            ++c;
+          }
         }
-        umma_commit(&empty[slot]);
-        if ((j % TF_PROMO) == TF_PROMO - 1 || j == nk - 1) umma_commit(&acc_full[b]);
       }
     }
   } else if (warp < 6) {
     // ---------------------------------------------------------------- splitters
     const int t = tid - 64;
-    for (int j = 0; j < nk; ++j) {
-      const int slot = j % STAGES;
-      mbar_wait(&full[slot], (j / STAGES) & 1);
-      uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int nk = tf_unit(p, u, BN).nk;
+      for (int kt = 0; kt < nk; ++kt, ++j) {
+        const int slot = j % STAGES;
+        mbar_wait(&full[slot], (j / STAGES) & 1);
+        uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
 #pragma unroll 4
-      for (int i = t; i < Cfg::HI_BYTES / 16; i += 128) {
-        float4* hp = reinterpret_cast<float4*>(st + i * 16);
-        const float4 v = *hp;
-        float4 h, l;
-        h.x = tf32_rna(v.x);
-        h.y = tf32_rna(v.y);
-        h.z = tf32_rna(v.z);
-        h.w = tf32_rna(v.w);
-        l.x = v.x - h.x;
-        l.y = v.y - h.y;
-        l.z = v.z - h.z;
-        l.w = v.w - h.w;
-        *hp = h;
-        *reinterpret_cast<float4*>(st + Cfg::HI_BYTES + i * 16) = l;
+        for (int i = t; i < Cfg::HI_BYTES / 16; i += 128) {
+          float4* hp = reinterpret_cast<float4*>(st + i * 16);
+          const float4 v = *hp;
+          float4 h, l;
+          h.x = tf32_rna(v.x);
+          h.y = tf32_rna(v.y);
+          h.z = tf32_rna(v.z);
+          h.w = tf32_rna(v.w);
+          l.x = v.x - h.x;
+          l.y = v.y - h.y;
+          l.z = v.z - h.z;
+          l.w = v.w - h.w;
+          *hp = h;
+          *reinterpret_cast<float4*>(st + Cfg::HI_BYTES + i * 16) = l;
+        }
+        // generic-proxy writes -> visible to the tensor core (async proxy) before the MMA reads
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&conv[slot]);
       }
-      // generic-proxy writes -> visible to the tensor core (async proxy) before the MMA reads
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&conv[slot]);
     }
-  } else {
+  } else if (warp < 10) {
     // ---------------------------------------------------------------- promoters + epilogue
     // Each K chunk of TF_PROMO k-tiles is accumulated by the tensor core in TMEM, then added
     // into FP32 registers here (round-to-nearest), which bounds the length of the tensor
-    // core's own accumulation chain (reading R18b).  TMEM lane = tile row.
+    // core's own accumulation chain (reading R18b).  TMEM lane = tile row.  While this
+    // epilogue runs, the MMAs of the next unit proceed in the other TMEM buffer.
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
-    const int m = m0 + row;
     const uint32_t trow = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-    float acc[BN];
-#pragma unroll
-    for (int i = 0; i < BN; ++i) acc[i] = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      const int b = c & 1;
-      mbar_wait(&acc_full[b], (c >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(trow + static_cast<uint32_t>(b * BN + c0), r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[c0 + i] += __uint_as_float(r[i]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&acc_empty[b]);
-    }
-
     double sq = 0.0;
-    if (m < p.M) {
-      const int ncols = min(BN, p.N - n0);
-      // groups of 8 columns, pinned in order so that the compiler does not widen all BN
-      // accumulators to FP64 at once (register pressure)
-      if (EPI == TF_STORE_COL) {
-        double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(blockIdx.y) * p.split_stride + m +
-                      static_cast<int64_t>(n0) * p.ldc;
+    int c = 0, cs = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const TfUnit w = tf_unit(p, u, BN);
+      float acc[BN];
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 8) {
-          float t[8];
+      for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+      const int nchunks = (w.nk + TF_PROMO - 1) / TF_PROMO;
+      for (int ch = 0; ch < nchunks; ++ch, ++c) {
+        const int b = c & 1;
+        mbar_wait(&acc_full[b], (c >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
-          pin8(t);
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(trow + static_cast<uint32_t>(b * BN + c0), r);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (c0 + i < ncols) *dst = static_cast<double>(t[i]);
-            dst += p.ldc;
+          for (int i = 0; i < 32; ++i) acc[c0 + i] += __uint_as_float(r[i]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&acc_empty[b]);
+      }
+
+      const int m = w.m0 + row;
+      if (EPI == TF_STORE_COL || EPI == TF_STORE_ROW) {
+        if (m < p.M) {
+          const int ncols = min(BN, p.N - w.n0);
+          // groups of 8 columns, pinned in order so that the compiler does not widen all BN
+          // accumulators to FP64 at once (register pressure)
+          if (EPI == TF_STORE_COL) {
+            double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(w.split) * p.split_stride + m +
+                          static_cast<int64_t>(w.n0) * p.ldc;
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 8) {
+              float t[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
+              pin8(t);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (c0 + i < ncols) *dst = static_cast<double>(t[i]);
+                dst += p.ldc;
+              }
+            }
+          } else {
+            double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(w.split) * p.split_stride +
+                          static_cast<int64_t>(m) * p.ldc + w.n0;
+            const bool vec = ncols == BN && (p.ldc & 1) == 0;
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 8) {
+              float t[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
+              pin8(t);
+              if (vec) {
+#pragma unroll
+                for (int i = 0; i < 8; i += 2)
+                  *reinterpret_cast<double2*>(dst + c0 + i) = make_double2(t[i], t[i + 1]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  if (c0 + i < ncols) dst[c0 + i] = static_cast<double>(t[i]);
+              }
+            }
           }
         }
-      } else if (EPI == TF_STORE_ROW) {
-        double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(blockIdx.y) * p.split_stride +
-                      static_cast<int64_t>(m) * p.ldc + n0;
-        const bool vec = ncols == BN && (p.ldc & 1) == 0;
+      } else {
+        // TF_SUB_COL: C -= acc, 32 columns at a time through the shared-memory ring (sub-tile:
+        // column n at n*128 floats; a warp touches 32 consecutive floats per column); FP64 sum
+        // of squares of the new C; one thread TMA-stores each sub-tile (clipped to the matrix)
+        const int ncols = m < p.M ? min(BN, p.N - w.n0) : 0;
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 8) {
-          float t[8];
+        for (int sub = 0; sub < BN / TF_CSUB; ++sub, ++cs) {
+          const int slot = cs % TF_CSLOTS;
+          mbar_wait(&cfull[slot], (cs / TF_CSLOTS) & 1);
+          float* cb = sC + slot * (TF_BM * TF_CSUB);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
-          pin8(t);
-          if (vec) {
-#pragma unroll
-            for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(dst + c0 + i) = make_double2(t[i], t[i + 1]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (c0 + i < ncols) dst[c0 + i] = static_cast<double>(t[i]);
+          for (int i = 0; i < TF_CSUB; ++i) {
+            const float r = cb[i * TF_BM + row] - acc[sub * TF_CSUB + i];
+            cb[i * TF_BM + row] = r;
+            if (sub * TF_CSUB + i < ncols) sq = fma(static_cast<double>(r), static_cast<double>(r), sq);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          if (warp == 6 && lane == 0) {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tC)),
+                         "r"(smem_u32(cb)), "r"(w.m0), "r"(w.n0 + sub * TF_CSUB)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            mbar_arrive(&cempty[slot]);
           }
         }
       }
     }
     if (SUB) {
-      // TF_SUB_COL: C -= acc on the shared-memory copy of the tile (column n at n*128 floats:
-      // a warp touches 32 consecutive floats per column), FP64 sum of squares of the new C
-      mbar_wait(cbar, 0);
-      const int ncols = m < p.M ? min(BN, p.N - n0) : 0;
-#pragma unroll
-      for (int i = 0; i < BN; ++i) {
-        const float r = sC[i * TF_BM + row] - acc[i];
-        sC[i * TF_BM + row] = r;
-        if (i < ncols) sq = fma(static_cast<double>(r), static_cast<double>(r), sq);
-      }
-      // generic-proxy writes -> visible to the TMA store (async proxy); one thread stores the
-      // tile (clipped to the matrix by TMA) once all 128 epilogue threads are done
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (warp == 6 && lane == 0) {
-        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                         reinterpret_cast<uint64_t>(&tC)),
-                     "r"(smem_u32(sC)), "r"(m0), "r"(n0)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      if (warp == 6 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (p.norm_partials != nullptr) {
+        sq = warp_sum(sq);
+        if (lane == 0) red[warp - 6] = sq;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 6 && lane == 0) p.norm_partials[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
       }
     }
-    if (EPI == TF_SUB_COL && p.norm_partials != nullptr) {
-      sq = warp_sum(sq);
-      if (lane == 0) red[warp - 6] = sq;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 6 && lane == 0)
-        p.norm_partials[blockIdx.y * gridDim.x + blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+  } else if (SUB) {
+    // ---------------------------------------------------------------- C producer (warp 10)
+    if (lane == 0) {
+      tma_prefetch_desc(&tC);
+      int cs = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const TfUnit w = tf_unit(p, u, BN);
+        for (int sub = 0; sub < BN / TF_CSUB; ++sub, ++cs) {
+          const int slot = cs % TF_CSLOTS;
+          if (cs >= TF_CSLOTS) mbar_wait(&cempty[slot], ((cs / TF_CSLOTS) - 1) & 1);
+          mbar_arrive_expect_tx(&cfull[slot], Cfg::CSUB_BYTES);
+          tma_load_2d(sC + slot * (TF_BM * TF_CSUB), &tC, &cfull[slot], w.m0, w.n0 + sub * TF_CSUB);
+        }
+      }
     }
   }
 

@@ -336,7 +336,7 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   int bn = 64;
   p.tiles_n = (N + bn - 1) / bn;
   int splits = 1;
-  if (allow_split) splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 64);
+  if (allow_split) splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 296);
   const bool subtract = epi == EPI_SUB_COL;
   static const int wide_env = debug_env("QB_WIDE_DOWNDATE");  // experiment: 1 = 128-wide tiles
   if (subtract && splits == 1 && wide_env > 0 && N >= 2048) {
@@ -466,8 +466,8 @@ qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, 
     QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
     attr_done = true;
   }
-  dim3 grid(p.tiles_m * p.tiles_n, splits);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tc, p);
+  const int units = p.tiles_m * p.tiles_n * splits;
+  kern<<<std::min(units, ctx->num_sms), Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tc, p);
   return check_launch(ctx, "gemm_tf32");
 }
 
@@ -503,7 +503,7 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   p.tiles_n = (N + bn - 1) / bn;
   const int tiles = p.tiles_m * p.tiles_n;
   int splits = 1;
-  if (allow_split && epi != TF_SUB_COL) splits = choose_splits(tiles, p.nkt, ctx->num_sms, 64);
+  if (allow_split && epi != TF_SUB_COL) splits = choose_splits(tiles, p.nkt, ctx->num_sms, 148);
   p.kt_per_split = (p.nkt + splits - 1) / splits;
   splits = std::max(1, (p.nkt + p.kt_per_split - 1) / p.kt_per_split);
   p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
@@ -522,7 +522,7 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   }
   CUtensorMap tc = ta;
   if (epi == TF_SUB_COL)
-    QB_TRY(make_map_f32(ctx, &tc, static_cast<const float*>(C), M, N, ldc, TF_BM, bn, CU_TENSOR_MAP_SWIZZLE_NONE));
+    QB_TRY(make_map_f32(ctx, &tc, static_cast<const float*>(C), M, N, ldc, TF_BM, TF_CSUB, CU_TENSOR_MAP_SWIZZLE_NONE));
   auto run = [&](int e, int s) -> qb_status {
     if (bn == 64) return dispatch_tf<64>(ctx, layout, e, ta, tb, tc, p, s);
     if (bn == 128) return dispatch_tf<128>(ctx, layout, e, ta, tb, tc, p, s);
@@ -532,13 +532,16 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   if (epi == TF_SUB_COL) {
     p.C = C;
     p.ldc = ldc;
-    if (want_norm) {
-      QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)tiles));
+    p.splits = 1;
+    if (want_norm) {  // one partial per persistent CTA
+      const int grid = std::min(tiles, ctx->num_sms);
+      QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
       p.norm_partials = ctx->parts.d();
-      if (nparts) *nparts = tiles;
+      if (nparts) *nparts = grid;
     }
     return run(TF_SUB_COL, 1);
   }
+  p.splits = splits;
   const int64_t rows = epi == TF_STORE_ROW ? M : N, cols = epi == TF_STORE_ROW ? N : M;
   if (splits == 1) {
     p.C = C;

@@ -15,6 +15,10 @@ def classify(name, grid):
         m = re.search(r"gemm_f64_kernel<(?:\(int\))?(\d), (?:\(int\))?(\d+), (?:\(int\))?(\d)>", name)
         lay, bn, epi = (int(m.group(1)), int(m.group(2)), int(m.group(3))) if m else (-1, -1, -1)
         return f"gemm_f64<{'NN' if lay == 0 else 'TN'},{bn},{['STORE_COL', 'STORE_ROW', 'SUB_COL'][epi]}>"
+    if "gemm_tf32_kernel" in name:
+        m = re.search(r"gemm_tf32_kernel<(?:\(int\))?(\d), (?:\(int\))?(\d+), (?:\(int\))?(\d)>", name)
+        lay, bn, epi = (int(m.group(1)), int(m.group(2)), int(m.group(3))) if m else (-1, -1, -1)
+        return f"gemm_tf32<{'NN' if lay == 0 else 'TN'},{bn},{['STORE_COL', 'STORE_ROW', 'SUB_COL'][epi]}>"
     m = re.search(r"qbk::(\w+)", name)
     return m.group(1) if m else None
 
