@@ -794,6 +794,10 @@ const char* qb_last_error(qb_ctx ctx) { return ctx ? ctx->err.c_str() : "null co
 
 int64_t qb_kernel_launches(qb_ctx ctx) { return ctx ? ctx->launches : 0; }
 
+#ifdef QB_CHOL_TIMING
+int qb_debug_chol_ts(unsigned long long* out) { return (int)cudaMemcpyFromSymbol(out, qb_chol_ts, 64 * 8); }
+#endif
+
 qb_status qb_create(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream) {
   if (!out) return QB_ERR_INVALID_ARG;
   *out = nullptr;

@@ -139,15 +139,15 @@ __global__ void __launch_bounds__(256) gated_copy_kernel(const double* __restric
 // memory).  Writes T column-major into `Tout` (ld ldt) such that X T has orthonormal columns:
 //   * Newton-Schulz: if ||G - I||_F <= sqrt(ns_tol2), X is orthonormal to first order and
 //     T = I - (G - I)/2 (one step towards the polar factor, error (3/4)||G - I||^2).  status 3.
-//   * Cholesky: right-looking over the 32-column panels.  Step p: CTA p factors its 32 x 32
-//     diagonal block (warp 0), inverts it, and solves its panel below; the CTAs that own later
-//     panels copy the rows they need of panel p over DSMEM and apply the rank-32 update.  Then
-//     CTA J forms block column J of L^-1 by blocked forward substitution
-//     (X_JJ = L_JJ^-1, X_IJ = -L_II^-1 sum_{K=J}^{I-1} L_IK X_KJ), reading L_IK and L_II^-1 from
-//     their owners, and writes it: Tout(row, col) = L^-1(row, col), i.e. read ROW-major Tout is
-//     R^-1 = L^-T (upper triangular).  A pivot that is not > tol * G_jj (or NaN) is a breakdown
-//     (reading R8): the cluster restarts once with the shifted-CholeskyQR shift
-//     s = 11 (m w + w (w+1)) u trace(G).  status[0] = 0 ok / 1 shifted / 2 failed.
+//   * Cholesky: right-looking over the 32-column panels.  Step p: warp 0 of CTA p factors its
+//     32 x 32 diagonal block and inverts it in registers (lane = row, shuffles), the CTA solves
+//     its panel below; the CTAs that own later panels copy the rows they need of panel p over
+//     DSMEM and apply the rank-32 update.  Then CTA J forms block column J of L^-1 right-
+//     looking over K = J.. (X_JJ = L_JJ^-1; X_KJ = -L_KK^-1 acc_K; acc_I += L_IK X_KJ for I > K,
+//     one DSMEM copy of panel K per step) and writes Tout(row, col) = L^-1(row, col), i.e. read
+//     ROW-major Tout is R^-1 = L^-T (upper triangular).  A pivot that is not > tol * G_jj (or
+//     NaN) is a breakdown (reading R8): the cluster restarts once with the shifted-CholeskyQR
+//     shift s = 11 (m w + w (w+1)) u trace(G).  status[0] = 0 ok / 1 shifted / 2 failed.
 // Flags: status[1] = 1 when the shift was used (gates the extra CholeskyQR3 passes),
 // status[2] = 1 when the Cholesky path ran (gates CholeskyQR's second pass; a Newton-Schulz
 // first pass needs none), status[3] += 1 per shifted factorization, status[4] = 1 on failure.
@@ -157,8 +157,83 @@ constexpr int CHOL_NB = 32;
 constexpr int CHOL_CTAS = 8;
 constexpr int CHOL_THREADS = 256;
 constexpr int CHOL_PLD = CHOL_NB + 1;
-constexpr int CHOL_SMEM = (2 * CHOL_MAXW * CHOL_PLD + 3 * CHOL_NB * CHOL_PLD) * 8;
+constexpr int CHOL_SMEM = (3 * CHOL_MAXW * CHOL_PLD + 2 * CHOL_NB * CHOL_PLD) * 8;
 constexpr int CHOL_ST_NS = 3;
+#ifdef QB_CHOL_TIMING  // development instrumentation: phase timestamps of CTA 0 (not in product builds)
+__device__ unsigned long long qb_chol_ts[64];
+#define CHOL_TS(i)                                                                                     \
+  do {                                                                                                 \
+    if (threadIdx.x == 0 && cluster.block_rank() == 0) {                                               \
+      unsigned long long t_;                                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                           \
+      qb_chol_ts[(i)] = t_;                                                                            \
+    }                                                                                                  \
+  } while (0)
+#else
+#define CHOL_TS(i) do { } while (0)
+#endif
+
+// dst[i][k] = src[(r0 + i)][k] for i < n, k < 32 (row stride PLD), src in a peer's shared memory
+// (DSMEM, generic loads): eight loads in flight per thread before the stores.
+__device__ __forceinline__ void chol_copy_rows(double* __restrict__ dst, const double* __restrict__ src, int r0,
+                                               int n) {
+  constexpr int PLD = CHOL_PLD;
+  const int total = n * CHOL_NB;
+  for (int base = threadIdx.x; base < total; base += 8 * CHOL_THREADS) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * CHOL_THREADS;
+      v[u] = idx < total ? src[(r0 + idx / CHOL_NB) * PLD + (idx % CHOL_NB)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * CHOL_THREADS;
+      if (idx < total) dst[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = v[u];
+    }
+  }
+}
+
+// rows [r0, r1) of A (ld PLD) times B^T restricted to 32 columns: out(i, c) = sum_k A(i,k) B(c,k),
+// four rows per warp pass (independent FMA chains); `op` consumes (i, c, value).
+template <typename Op>
+__device__ __forceinline__ void chol_rows_times_bt(const double* A, const double* B, int r0, int r1, int ncols,
+                                                   Op op) {
+  constexpr int PLD = CHOL_PLD;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane;
+  for (int i = r0 + 4 * warp; i < r1; i += 4 * (CHOL_THREADS / 32)) {
+    // 4 rows x 2 halves of k: 8 independent FMA chains (FP64 latency)
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+    const bool v1 = i + 1 < r1, v2 = i + 2 < r1, v3 = i + 3 < r1;
+#pragma unroll 8
+    for (int k = 0; k < CHOL_NB / 2; ++k) {
+      const int kh = k + CHOL_NB / 2;
+      const double b = B[c * PLD + k], bh = B[c * PLD + kh];
+      a0 = fma(A[i * PLD + k], b, a0);
+      e0 = fma(A[i * PLD + kh], bh, e0);
+      if (v1) {
+        a1 = fma(A[(i + 1) * PLD + k], b, a1);
+        e1 = fma(A[(i + 1) * PLD + kh], bh, e1);
+      }
+      if (v2) {
+        a2 = fma(A[(i + 2) * PLD + k], b, a2);
+        e2 = fma(A[(i + 2) * PLD + kh], bh, e2);
+      }
+      if (v3) {
+        a3 = fma(A[(i + 3) * PLD + k], b, a3);
+        e3 = fma(A[(i + 3) * PLD + kh], bh, e3);
+      }
+    }
+    __syncwarp();
+    if (c < ncols) {
+      op(i, c, a0 + e0);
+      if (v1) op(i + 1, c, a1 + e1);
+      if (v2) op(i + 2, c, a2 + e2);
+      if (v3) op(i + 3, c, a3 + e3);
+    }
+  }
+}
 
 __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS)
     chol_cluster_kernel(const double* __restrict__ G, int64_t ldg, int w, int64_t m_rows, double* __restrict__ Tout,
@@ -170,12 +245,12 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
   constexpr int PLD = CHOL_PLD;
   extern __shared__ double sm[];
   double* P = sm;                      // [256][PLD] own panel: rows 32*cta.., columns 32*cta..+31
-  double* R = P + CHOL_MAXW * PLD;     // [256][PLD] staged rows of a peer panel; later X = L^-1 block column
-  double* Dl = R + CHOL_MAXW * PLD;    // [32][PLD] diagonal block L11 (identity-padded) / staging
-  double* Di = Dl + CHOL_NB * PLD;     // [32][PLD] L11^-1 (identity-padded), read by peers
-  double* Tb = Di + CHOL_NB * PLD;     // [32][PLD] scratch
-  __shared__ double red[CHOL_THREADS / 32];
-  __shared__ double s_part, s_tot, s_shift;
+  double* X = P + CHOL_MAXW * PLD;     // [256][PLD] block column of L^-1 (accumulated)
+  double* S = X + CHOL_MAXW * PLD;     // [256][PLD] staged rows of a peer panel
+  double* Di = S + CHOL_MAXW * PLD;    // [32][PLD] L11^-1 (identity-padded), read by peers
+  double* Dt = Di + CHOL_NB * PLD;     // [32][PLD] staged peer L_KK^-1
+  __shared__ double red[2][CHOL_THREADS / 32];
+  __shared__ double s_part[2], s_tot, s_shift;
   __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cta = static_cast<int>(cluster.block_rank());
@@ -183,30 +258,43 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
   const bool active = cta < nbk;
   const int p0 = cta * CHOL_NB;
   const int rows = active ? w - p0 : 0, nb = active ? min(CHOL_NB, w - p0) : 0;
+  CHOL_TS(0);
 
-  // ---- Newton-Schulz test: ||G - I||_F^2 over the own column block, summed in rank order
-  double e2 = 0.0;
+  // ---- Newton-Schulz test ||G - I||_F^2 and trace(G) over the own column block (rank order)
+  double e2 = 0.0, tr = 0.0;
   for (int idx = tid; idx < w * nb; idx += CHOL_THREADS) {
     const int i = idx % w, j = p0 + idx / w;
-    const double d = __ldcg(G + i + static_cast<int64_t>(j) * ldg) - (i == j ? 1.0 : 0.0);
+    const double g = __ldcg(G + i + static_cast<int64_t>(j) * ldg);
+    const double d = g - (i == j ? 1.0 : 0.0);
     e2 = fma(d, d, e2);
+    if (i == j) tr += g;
   }
   e2 = warp_sum(e2);
-  if (lane == 0) red[warp] = e2;
+  tr = warp_sum(tr);
+  if (lane == 0) {
+    red[0][warp] = e2;
+    red[1][warp] = tr;
+  }
   __syncthreads();
   if (tid == 0) {
-    double t = 0.0;
-    for (int k = 0; k < CHOL_THREADS / 32; ++k) t += red[k];
-    s_part = t;
-    double tr = 0.0;
-    for (int j = 0; j < w; ++j) tr += __ldcg(G + j + static_cast<int64_t>(j) * ldg);
-    s_shift = 11.0 * (static_cast<double>(m_rows) * w + static_cast<double>(w) * (w + 1)) * 0x1p-53 * tr;
+    double t0 = 0.0, t1 = 0.0;
+    for (int k = 0; k < CHOL_THREADS / 32; ++k) {
+      t0 += red[0][k];
+      t1 += red[1][k];
+    }
+    s_part[0] = t0;
+    s_part[1] = t1;
   }
   cluster.sync();
   if (tid == 0) {
-    double t = 0.0;
-    for (int r = 0; r < CHOL_CTAS; ++r) t += *cluster.map_shared_rank(&s_part, r);
-    s_tot = t;
+    double t0 = 0.0, t1 = 0.0;
+    for (int r = 0; r < CHOL_CTAS; ++r) {
+      const double* pr = cluster.map_shared_rank(s_part, r);
+      t0 += pr[0];
+      t1 += pr[1];
+    }
+    s_tot = t0;
+    s_shift = 11.0 * (static_cast<double>(m_rows) * w + static_cast<double>(w) * (w + 1)) * 0x1p-53 * t1;
   }
   __syncthreads();
   if (ns_tol2 >= 0.0 && s_tot <= ns_tol2) {
@@ -219,6 +307,8 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
     cluster.sync();  // peers may still read s_part
     return;
   }
+  // tolerance reference of the own diagonal block, lane = row
+  const double gdiag = (lane < nb) ? __ldcg(G + (p0 + lane) + static_cast<int64_t>(p0 + lane) * ldg) : 1.0;
 
   int attempt = 0;
   bool failed = false;
@@ -231,81 +321,85 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
       P[i * PLD + j] = v;
     }
     if (tid == 0) s_fail = 0;
+    CHOL_TS(1);
     cluster.sync();  // panels loaded; no peer still reads the previous attempt's panels
+    CHOL_TS(2);
     failed = false;
     for (int p = 0; p < nbk; ++p) {
       if (cta == p) {
-        // unblocked Cholesky of the nb x nb diagonal block (warp 0, lane = row)
         if (warp == 0) {
+          // Cholesky of the nb x nb diagonal block in registers: lane = row, a[c] = L(lane, c)
+          double a[CHOL_NB];
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c)
+            a[c] = (lane < nb && c < nb && c <= lane) ? P[lane * PLD + c] : (c == lane ? 1.0 : 0.0);
+          // (dependent FP64 latency dominates this single-warp code: reciprocal square roots
+          // instead of divisions, split accumulators in the substitution)
+          if (p == 0) CHOL_TS(3);
           int bad = 0;
-          for (int jj = 0; jj < nb; ++jj) {
-            const double d = P[jj * PLD + jj];
-            const double g0 = __ldcg(G + (p0 + jj) + static_cast<int64_t>(p0 + jj) * ldg);
-            if (!(d > tol * g0) || !(d > 0.0)) {
-              bad = 1;
-              break;
+          double rdiag = 1.0;  // 1 / L(lane, lane)
+#pragma unroll
+          for (int jj = 0; jj < CHOL_NB; ++jj) {
+            const double d = __shfl_sync(0xffffffffu, a[jj], jj);
+            const double gj = __shfl_sync(0xffffffffu, gdiag, jj);
+            if (jj < nb && (!(d > tol * gj) || !(d > 0.0))) bad = 1;
+            const double ri = rsqrt(d);
+            const double l = lane > jj ? a[jj] * ri : (lane == jj ? d * ri : 0.0);
+            if (lane == jj) rdiag = ri;
+            a[jj] = l;
+#pragma unroll
+            for (int c = 0; c < CHOL_NB; ++c) {  // fixed bounds: a[] stays in registers
+              if (c > jj) {
+                const double lc = __shfl_sync(0xffffffffu, l, c);
+                if (lane >= c) a[c] = fma(-l, lc, a[c]);
+              }
             }
-            const double r = sqrt(d);
-            __syncwarp();
-            if (lane == jj) P[jj * PLD + jj] = r;
-            if (lane > jj && lane < nb) P[lane * PLD + jj] /= r;
-            __syncwarp();
-            if (lane > jj && lane < nb) {
-              const double lij = P[lane * PLD + jj];
-              for (int c = jj + 1; c <= lane; ++c) P[lane * PLD + c] -= lij * P[c * PLD + jj];
+          }
+          if (p == 0) CHOL_TS(4);
+          // L11^-1, column `lane`: forward substitution with L(r, k) broadcast from lane r
+          double x[CHOL_NB];
+#pragma unroll
+          for (int r = 0; r < CHOL_NB; ++r) {
+            double v0 = (r == lane) ? 1.0 : 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+            for (int k = 0; k < CHOL_NB; k += 4) {
+              if (k < r) v0 = fma(-__shfl_sync(0xffffffffu, a[k], r), x[k], v0);
+              if (k + 1 < r) v1 = fma(-__shfl_sync(0xffffffffu, a[k + 1], r), x[k + 1], v1);
+              if (k + 2 < r) v2 = fma(-__shfl_sync(0xffffffffu, a[k + 2], r), x[k + 2], v2);
+              if (k + 3 < r) v3 = fma(-__shfl_sync(0xffffffffu, a[k + 3], r), x[k + 3], v3);
             }
-            __syncwarp();
+            x[r] = ((v0 + v1) + (v2 + v3)) * __shfl_sync(0xffffffffu, rdiag, r);
+          }
+          if (p == 0) CHOL_TS(5);
+#pragma unroll
+          for (int r = 0; r < CHOL_NB; ++r) Di[r * PLD + lane] = (r >= lane) ? x[r] : 0.0;
+          if (lane < nb) {
+#pragma unroll
+            for (int c = 0; c < CHOL_NB; ++c)
+              if (c < nb) P[lane * PLD + c] = (c <= lane) ? a[c] : 0.0;
           }
           if (lane == 0) s_fail = bad;
-          if (!bad) {  // L11 -> Dl (identity-padded), L11^-1 -> Di by forward substitution, lane = column
-            for (int r = 0; r < CHOL_NB; ++r)
-              Dl[r * PLD + lane] =
-                  (r < nb && lane < nb && lane <= r) ? P[r * PLD + lane] : (r == lane ? 1.0 : 0.0);
-            __syncwarp();
-            for (int r = 0; r < CHOL_NB; ++r) {
-              double v = (r == lane) ? 1.0 : 0.0;
-              for (int k = lane; k < r; ++k) v -= Dl[r * PLD + k] * Di[k * PLD + lane];
-              Di[r * PLD + lane] = (r >= lane) ? v / Dl[r * PLD + r] : 0.0;
-              __syncwarp();
-            }
-          }
         }
         __syncthreads();
-        if (!s_fail) {  // panel below the diagonal block: L21 = P21 L11^-T
-          const int c = lane;
-          for (int i = nb + warp; i < rows; i += CHOL_THREADS / 32) {
-            double v = 0.0;
-            if (c < nb)
-              for (int k = 0; k <= c; ++k) v = fma(P[i * PLD + k], Di[c * PLD + k], v);
-            __syncwarp();
-            if (c < nb) P[i * PLD + c] = v;
-          }
+        if (!s_fail) {  // panel below the diagonal block: L21 = P21 L11^-T, in place
+          chol_rows_times_bt(P, Di, nb, rows, nb, [&](int i, int c, double v) { P[i * PLD + c] = v; });
         }
       }
+      if (p == 0) CHOL_TS(6);
       cluster.sync();
+      if (p == 0) CHOL_TS(7);
       if (*cluster.map_shared_rank(&s_fail, p)) {
         failed = true;
         break;
       }
       if (active && cta > p) {  // rank-32 update of the own panel with panel p's rows p0.. (over DSMEM)
-        const double* Pp = cluster.map_shared_rank(P, p);
-        const int off = p0 - p * CHOL_NB;
-        for (int idx = tid; idx < rows * CHOL_NB; idx += CHOL_THREADS) {
-          const int i = idx / CHOL_NB, k = idx % CHOL_NB;
-          R[i * PLD + k] = Pp[(off + i) * PLD + k];
-        }
+        chol_copy_rows(S, cluster.map_shared_rank(P, p), p0 - p * CHOL_NB, rows);
         __syncthreads();
-        const int c = lane;
-        for (int i = warp; i < rows; i += CHOL_THREADS / 32) {
-          if (c < nb) {
-            double acc = 0.0;
-#pragma unroll 8
-            for (int k = 0; k < CHOL_NB; ++k) acc = fma(R[i * PLD + k], R[c * PLD + k], acc);
-            P[i * PLD + c] -= acc;
-          }
-        }
+        chol_rows_times_bt(S, S, 0, rows, nb, [&](int i, int c, double v) { P[i * PLD + c] -= v; });
       }
+      CHOL_TS(8 + 2 * p);
       cluster.sync();
+      CHOL_TS(9 + 2 * p);
     }
     if (!failed) break;
   }
@@ -323,63 +417,83 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
     return;
   }
 
-  // ---- block column J = cta of L^-1 (X in R, rows 32J..w-1)
+  CHOL_TS(30);
+  // ---- block column J = cta of L^-1, right-looking over K = J .. nbk-1 (X rows 32J..w-1)
   if (active) {
-    double* X = R;
-    for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
-      X[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = Di[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)];
-    const int r = tid >> 3, c0 = (tid & 7) * 4;  // thread owns T(r, c0..c0+3)
-    for (int I = cta + 1; I < nbk; ++I) {
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-      for (int K = cta; K < I; ++K) {
-        const double* PK = cluster.map_shared_rank(P, K);  // L_IK = rows 32(I-K).. of panel K
-        __syncthreads();
-        for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += CHOL_THREADS) {
-          const int rr = idx / CHOL_NB, kk = idx % CHOL_NB;
-          Dl[rr * PLD + kk] = (I * CHOL_NB + rr < w) ? PK[((I - K) * CHOL_NB + rr) * PLD + kk] : 0.0;
-        }
-        __syncthreads();
-        const double* xb = X + (K - cta) * CHOL_NB * PLD;
-#pragma unroll 4
-        for (int kk = 0; kk < CHOL_NB; ++kk) {
-          const double l = Dl[r * PLD + kk];
-          const double* x = xb + kk * PLD + c0;
-          t0 = fma(l, x[0], t0);
-          t1 = fma(l, x[1], t1);
-          t2 = fma(l, x[2], t2);
-          t3 = fma(l, x[3], t3);
-        }
-      }
-      const double* DI = cluster.map_shared_rank(Di, I);
-      __syncthreads();
-      Tb[r * PLD + c0] = t0;
-      Tb[r * PLD + c0 + 1] = t1;
-      Tb[r * PLD + c0 + 2] = t2;
-      Tb[r * PLD + c0 + 3] = t3;
-      for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
-        Dl[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = DI[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)];
-      __syncthreads();
-      double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-      for (int t = 0; t <= r; ++t) {
-        const double d = Dl[r * PLD + t];
-        v0 = fma(d, Tb[t * PLD + c0], v0);
-        v1 = fma(d, Tb[t * PLD + c0 + 1], v1);
-        v2 = fma(d, Tb[t * PLD + c0 + 2], v2);
-        v3 = fma(d, Tb[t * PLD + c0 + 3], v3);
-      }
-      double* xo = X + ((I - cta) * CHOL_NB + r) * PLD + c0;
-      xo[0] = -v0;
-      xo[1] = -v1;
-      xo[2] = -v2;
-      xo[3] = -v3;
-    }
+    for (int idx = tid; idx < rows * CHOL_NB; idx += CHOL_THREADS) X[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = 0.0;
     __syncthreads();
+    const int r = tid >> 3, c0 = (tid & 7) * 4;  // thread owns X_KJ(r, c0..c0+3) when finalising
+    for (int K = cta; K < nbk; ++K) {
+      double* XK = X + (K - cta) * CHOL_NB * PLD;
+      if (K == cta) {
+        for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
+          XK[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = Di[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)];
+      } else {  // X_KJ = -L_KK^-1 acc_K
+        chol_copy_rows(Dt, cluster.map_shared_rank(Di, K), 0, CHOL_NB);
+        __syncthreads();
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+#pragma unroll 8
+        for (int t = 0; t < CHOL_NB / 2; ++t) {
+          const int th = t + CHOL_NB / 2;
+          const double d = Dt[r * PLD + t], dh = Dt[r * PLD + th];
+          v0 = fma(d, XK[t * PLD + c0], v0);
+          v1 = fma(d, XK[t * PLD + c0 + 1], v1);
+          v2 = fma(d, XK[t * PLD + c0 + 2], v2);
+          v3 = fma(d, XK[t * PLD + c0 + 3], v3);
+          u0 = fma(dh, XK[th * PLD + c0], u0);
+          u1 = fma(dh, XK[th * PLD + c0 + 1], u1);
+          u2 = fma(dh, XK[th * PLD + c0 + 2], u2);
+          u3 = fma(dh, XK[th * PLD + c0 + 3], u3);
+        }
+        __syncthreads();
+        XK[r * PLD + c0] = -(v0 + u0);
+        XK[r * PLD + c0 + 1] = -(v1 + u1);
+        XK[r * PLD + c0 + 2] = -(v2 + u2);
+        XK[r * PLD + c0 + 3] = -(v3 + u3);
+      }
+      const int below = w - (K + 1) * CHOL_NB;  // rows of panel K under its diagonal block
+      if (below <= 0) break;
+      chol_copy_rows(S, cluster.map_shared_rank(P, K), CHOL_NB, below);
+      __syncthreads();
+      // acc_I += L_IK X_KJ for the rows below block K: out(i, c) = sum_k S(i, k) XK(k, c)
+      double* acc = X + (K + 1 - cta) * CHOL_NB * PLD;
+      for (int i = 4 * warp; i < below; i += 4 * (CHOL_THREADS / 32)) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+        const bool q1 = i + 1 < below, q2 = i + 2 < below, q3 = i + 3 < below;
+#pragma unroll 8
+        for (int k = 0; k < CHOL_NB / 2; ++k) {
+          const int kh = k + CHOL_NB / 2;
+          const double xk = XK[k * PLD + lane], xh = XK[kh * PLD + lane];
+          a0 = fma(S[i * PLD + k], xk, a0);
+          e0 = fma(S[i * PLD + kh], xh, e0);
+          if (q1) {
+            a1 = fma(S[(i + 1) * PLD + k], xk, a1);
+            e1 = fma(S[(i + 1) * PLD + kh], xh, e1);
+          }
+          if (q2) {
+            a2 = fma(S[(i + 2) * PLD + k], xk, a2);
+            e2 = fma(S[(i + 2) * PLD + kh], xh, e2);
+          }
+          if (q3) {
+            a3 = fma(S[(i + 3) * PLD + k], xk, a3);
+            e3 = fma(S[(i + 3) * PLD + kh], xh, e3);
+          }
+        }
+        acc[i * PLD + lane] += a0 + e0;
+        if (q1) acc[(i + 1) * PLD + lane] += a1 + e1;
+        if (q2) acc[(i + 2) * PLD + lane] += a2 + e2;
+        if (q3) acc[(i + 3) * PLD + lane] += a3 + e3;
+      }
+      __syncthreads();
+    }
     for (int idx = tid; idx < w * nb; idx += CHOL_THREADS) {
       const int row = idx % w, c = idx / w;
       Tout[row + static_cast<int64_t>(p0 + c) * ldt] = row >= p0 ? X[(row - p0) * PLD + c] : 0.0;
     }
   }
+  CHOL_TS(31);
   cluster.sync();  // keep this CTA's shared memory alive while peers read it
+  CHOL_TS(32);
 }
 
 }  // namespace qbk
