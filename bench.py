@@ -243,7 +243,7 @@ def run_ours(args, cfg):
     t_down = statistics.mean(s["ms_down"] for s in full) * 1e-3
     achieved = 2.0 * m * n_local * b / t_down * 1e-12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01c.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("downdate_dram_bytes_per_launch")
