@@ -120,6 +120,23 @@ qb_status qb_factor(qb_ctx ctx, void* A, int64_t m, int64_t n, int64_t lda, doub
                     int64_t* k, const void** Q, int64_t* ldq, const void** B, int64_t* ldb,
                     double* resid);
 
+/* Fixed-rank schemes (NEXT-4): randQB (Fig. 1) for P = 0 and randQB_p (Fig. 3,
+ * P:826-849) for P >= 1, unblocked: Omega = randn(n, l) (columns 0..l-1 of the same generator
+ * as qb_factor, so its Omega_i are slices of this one, eq. (OmegaBlock));
+ * Q = orth(A Omega); P times { Q = orth(A^* Q); Q = orth(A Q) }; B = Q^* A.  With
+ * QB_SKIP_POWER_ORTH: Y = A Omega; P times Y = A (A^* Y); Q = orth(Y).
+ * orth of the m x l panel: 256 columns at a time, two block Gram-Schmidt projections against the
+ * finished columns and CholeskyQR2 (shifted fallback, R8).
+ *   A     device, column-major m x n (lda); read-only unless QB_OVERWRITE_A.  1 <= l <= min(m, n).
+ *   *resid (optional) = ||A - QB||_F, computed directly (one more rank-l update, of A itself
+ *          under QB_OVERWRITE_A, else of a context-owned copy).
+ * Outputs Q (column-major m x l, *ldq) and B (ROW-major l x n, *ldb) are context-owned as for
+ * qb_factor; rqb_svd afterwards converts this factorization.  Distributed contexts:
+ * QB_ERR_UNSUPPORTED.  Blocking.                                                            */
+qb_status qb_fixed_rank(qb_ctx ctx, void* A, int64_t m, int64_t n, int64_t lda, int64_t l, int P,
+                        uint64_t seed, unsigned flags, const void** Q, int64_t* ldq, const void** B,
+                        int64_t* ldb, double* resid);
+
 /* qb_factor with HOST buffers (end-to-end entry point): A_host (column-major, lda_host) is
  * copied to the device on the context stream (pinned memory makes this a DMA at full PCIe /
  * C2C rate), factored with the device path, and Q (column-major m x k, ldq_host) and B

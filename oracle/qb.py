@@ -124,27 +124,28 @@ def randqb_pb(A, eps, b, q=0, seed=1, kmax=None, reproj=True, omega_dtype=np.flo
     return res
 
 
-def randqb(A, ell, seed=1):
+def randqb(A, ell, seed=1, omega_dtype=np.float64):
     """randQB (Fig. 1), the unblocked fixed-rank scheme:
     Ω = randn(n, ℓ); Q = orth(AΩ); B = Q^* A.  Ω is columns 0..ℓ-1 of the same generator,
-    so its slices are the Ω_i of the blocked scheme (eq. (OmegaBlock), :479-484)."""
+    so its slices are the Ω_i of the blocked scheme (eq. (OmegaBlock), :479-484).
+    omega_dtype=np.float32: Ω = RN_32(Ω) (reading R18), arithmetic still FP64."""
     A = np.asarray(A, dtype=np.float64)
-    Q = orth(A @ omega(seed, A.shape[1], 0, ell))
+    Q = orth(A @ omega(seed, A.shape[1], 0, ell, omega_dtype))
     return Q, Q.T @ A
 
 
-def randqb_p(A, ell, P, seed=1, skip_power_orth=False):
+def randqb_p(A, ell, P, seed=1, skip_power_orth=False, omega_dtype=np.float64):
     """randQB_p (Fig. 3, PAPER.md:826-849): Q = orth(AΩ); P times {Q = orth(A^*Q);
     Q = orth(AQ)}; B = Q^* A.  skip_power_orth: Y = AΩ; P times Y = A(A^*Y); Q = orth(Y)
-    (PAPER.md:919-927)."""
+    (PAPER.md:919-927).  omega_dtype as in randqb."""
     A = np.asarray(A, dtype=np.float64)
     if skip_power_orth:
-        Y = A @ omega(seed, A.shape[1], 0, ell)
+        Y = A @ omega(seed, A.shape[1], 0, ell, omega_dtype)
         for _ in range(P):
             Y = A @ (A.T @ Y)
         Q = orth(Y)
         return Q, Q.T @ A
-    Q = orth(A @ omega(seed, A.shape[1], 0, ell))
+    Q = orth(A @ omega(seed, A.shape[1], 0, ell, omega_dtype))
     for _ in range(P):
         Q = orth(A.T @ Q)
         Q = orth(A @ Q)

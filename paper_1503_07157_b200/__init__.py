@@ -74,6 +74,8 @@ def lib():
         L.qb_omega.argtypes = [c_ctx, u64, i64, i64, i64, i64, vp, i64]
         L.qb_orth.argtypes = [c_ctx, vp, i64, i64, i64]
         L.rqb_svd.argtypes = [c_ctx, i64, P(vp), P(i64), P(vp), P(vp), P(i64)]
+        L.qb_fixed_rank.argtypes = [c_ctx, vp, i64, i64, i64, i64, ctypes.c_int, u64, ctypes.c_uint, P(vp), P(i64),
+                                    P(vp), P(i64), P(dbl)]
         L.qb_kernel_launches.argtypes = [c_ctx]
         L.qb_kernel_launches.restype = i64
         L.qb_destroy.argtypes = [c_ctx]
@@ -83,7 +85,7 @@ def lib():
         L.qb_last_error.argtypes = [c_ctx]
         L.qb_last_error.restype = ctypes.c_char_p
         for f in ("qb_create", "qb_create_dist", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_gemm", "qb_chol_rinv", "qb_stats", "qb_omega",
-                  "qb_orth", "rqb_svd"):
+                  "qb_orth", "rqb_svd", "qb_fixed_rank"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -165,6 +167,18 @@ def qb_factor(ctx, A_ptr, m, n, lda, eps, b, q=0, seed=1, kmax=0, flags=0):
                         ctypes.byref(resid))
     _check(ctx, s, ok=(QB_OK, QB_NOT_CONVERGED))
     return dict(status=s, k=k.value, Q=Q.value, ldq=ldq.value, B=B.value, ldb=ldb.value, resid=resid.value)
+
+
+def qb_fixed_rank(ctx, A_ptr, m, n, lda, l, P=0, seed=1, flags=0, want_resid=True):
+    """Raw call of the fixed-rank schemes randQB / randQB_p (see include/qb.h).
+    Returns dict(Q, ldq, B, ldb, resid) with device pointers (resid None unless requested)."""
+    Q, B = ctypes.c_void_p(), ctypes.c_void_p()
+    ldq, ldb = ctypes.c_int64(), ctypes.c_int64()
+    resid = ctypes.c_double()
+    _check(ctx, lib().qb_fixed_rank(ctx, ctypes.c_void_p(A_ptr), m, n, lda, l, P, seed, flags, ctypes.byref(Q),
+                                    ctypes.byref(ldq), ctypes.byref(B), ctypes.byref(ldb),
+                                    ctypes.byref(resid) if want_resid else None))
+    return dict(Q=Q.value, ldq=ldq.value, B=B.value, ldb=ldb.value, resid=resid.value if want_resid else None)
 
 
 def qb_factor_host(ctx, A_host_ptr, m, n, lda, eps, b, q, seed, kmax, Q_host_ptr, ldq, B_host_ptr, ldb, kcap):
@@ -287,6 +301,21 @@ class QB:
             Q, B = Q.clone(), B.clone()
         self._last = (m, n, k, A.dtype)
         return dict(status=r["status"], k=k, Q=Q, B=B, resid=r["resid"], stats=qb_stats(self.ctx))
+
+    def fixed_rank(self, A, l, P=0, seed=1, overwrite=False, flags=0, want_resid=True, copy_out=True):
+        """randQB (P = 0, Fig. 1) / randQB_p (Fig. 3): Q (m x l), B (l x n) for a fixed rank l."""
+        import torch
+        assert A.is_cuda and A.dtype in (torch.float64, torch.float32) and A.dim() == 2 and A.stride(0) == 1
+        m, n = A.shape
+        r = qb_fixed_rank(self.ctx, A.data_ptr(), m, n, A.stride(1) if n > 1 else m, l, P, seed,
+                          (QB_OVERWRITE_A if overwrite else 0) | flags, want_resid)
+        ts = "<f8" if A.dtype == torch.float64 else "<f4"
+        Q = view_colmajor(r["Q"], m, l, r["ldq"], ts)
+        B = view_rowmajor(r["B"], l, n, r["ldb"], ts)
+        if copy_out:
+            Q, B = Q.clone(), B.clone()
+        self._last = (m, n, l, A.dtype)
+        return dict(Q=Q, B=B, resid=r["resid"])
 
     def svd(self, kkeep=0, copy_out=True):
         """Partial SVD A ~ U diag(S) V^T from the last ``factor`` (rqb_svd):

@@ -636,6 +636,26 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
   return QB_OK;
 }
 
+// Orthonormalise the m x l column-major panel X (ld ldx) in place for any l: 256 columns at a
+// time, two block Gram-Schmidt projections against the finished columns, then CholeskyQR2.
+// Uses ctx->Wsv (l x 256 row-major coefficients).
+qb_status orth_blocked(qb_ctx ctx, double* X, int64_t ldx, int64_t m, int64_t l) {
+  const int64_t bp = round_up(kMaxB, 16);
+  QB_TRY(ensure(ctx, ctx->Wsv, sizeof(double) * (size_t)(round_up(l, 16) * bp)));
+  for (int64_t j0 = 0; j0 < l; j0 += kMaxB) {
+    const int64_t w = std::min<int64_t>(kMaxB, l - j0);
+    double* Xj = X + j0 * ldx;
+    for (int pass = 0; pass < 2 && j0 > 0; ++pass) {  // Xj -= X (X^T Xj), twice
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)j0, (int)w, (int)m, X, ldx, Xj, ldx, ctx->Wsv.d(), bp, false,
+                  nullptr));
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)j0, X, ldx, ctx->Wsv.d(), bp, Xj, ldx, false,
+                  nullptr));
+    }
+    QB_TRY(cholqr2(ctx, Xj, ldx, Xj, ldx, m, (int)w));
+  }
+  return QB_OK;
+}
+
 bool skip_orth_flag(unsigned flags) { return (flags & QB_SKIP_POWER_ORTH) != 0; }
 
 qb_status reset_flags(qb_ctx ctx) {
@@ -998,19 +1018,8 @@ qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_ou
   QB_TRY(reset_flags(ctx));
 
   // 1. Q_B = orth(B̄^T), 256 columns at a time
-  for (int64_t j0 = 0; j0 < k; j0 += kMaxB) {
-    const int64_t w = std::min<int64_t>(kMaxB, k - j0);
-    double* X = QBm + j0 * ldn;
-    QB_CUDA(cudaMemcpy2DAsync(X, ldn * 8, Bbar + j0 * ctx->ldb, ctx->ldb * 8, n * 8, w, cudaMemcpyDeviceToDevice,
-                              ctx->stream));
-    for (int pass = 0; pass < 2 && j0 > 0; ++pass) {  // X -= Q_B (Q_B^T X), twice
-      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)j0, (int)w, (int)n, QBm, ldn, X, ldn, ctx->Wsv.d(), bp, false,
-                  nullptr));
-      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)n, (int)w, (int)j0, QBm, ldn, ctx->Wsv.d(), bp, X, ldn, false,
-                  nullptr));
-    }
-    QB_TRY(cholqr2(ctx, X, ldn, X, ldn, n, (int)w));
-  }
+  QB_CUDA(cudaMemcpy2DAsync(QBm, ldn * 8, Bbar, ctx->ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, ctx->stream));
+  QB_TRY(orth_blocked(ctx, QBm, ldn, n, k));
   // 2. R = Q_B^T B̄^T (k x k, column-major)
   QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)k, (int)k, (int)n, QBm, ldn, Bbar, ctx->ldb, ctx->R.d(), ldk, false,
               nullptr));
@@ -1125,6 +1134,139 @@ qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_ou
   if (V_out) *V_out = Vp;
   if (ldv_out) *ldv_out = ldn;
   return QB_OK;
+}
+
+qb_status qb_fixed_rank(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, int64_t l, int P, uint64_t seed,
+                        unsigned flags, const void** Q_out, int64_t* ldq_out, const void** B_out, int64_t* ldb_out,
+                        double* resid_out) {
+  // randQB (Fig. 1) / randQB_p (Fig. 3), unblocked; the skip
+  // variant of PAPER.md:919-927 under QB_SKIP_POWER_ORTH.
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  ctx->stats.clear();
+  ctx->last_k = -1;
+  if (ctx->nranks > 1) return fail(ctx, QB_ERR_UNSUPPORTED, "qb_fixed_rank: distributed contexts not supported");
+  const bool is_f32 = ctx->dtype == QB_F32;
+  if (!Ain || m < 1 || n < 1 || lda < m || m > INT32_MAX || n > INT32_MAX || l < 1 || l > std::min(m, n) || P < 0)
+    return fail(ctx, QB_ERR_INVALID_ARG, "qb_fixed_rank: bad arguments (m=%lld n=%lld lda=%lld l=%lld P=%d)",
+                (long long)m, (long long)n, (long long)lda, (long long)l, P);
+  QB_CUDA(cudaSetDevice(ctx->device));
+  const size_t es = is_f32 ? 4 : 8;
+  // A is only read, except for the optional residual: then it is updated in place (OVERWRITE)
+  // or in a context-owned copy
+  void* Av = Ain;
+  int64_t ldA = lda;
+  const bool aligned = (lda % (is_f32 ? 4 : 2) == 0) && ((reinterpret_cast<uintptr_t>(Ain) & 15) == 0);
+  if (!aligned || (resid_out && !(flags & QB_OVERWRITE_A))) {
+    ldA = round_up(m, 16);
+    QB_TRY(ensure(ctx, ctx->Awork, es * (size_t)(ldA * n)));
+    QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * es, Ain, lda * es, m * es, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    Av = ctx->Awork.p;
+  }
+  double* A = static_cast<double*>(Av);
+  float* A32 = static_cast<float*>(Av);
+  const int64_t ldn = round_up(n, 16), lp = round_up(l, 16), ldm = round_up(m, 16);
+  QB_TRY(grow_factors(ctx, m, n, l, l));
+  double* Qd = ctx->Qbar.d();
+  const int64_t ldq = ctx->ldq;
+  double* Bd = ctx->Bbar.d();
+  QB_TRY(ensure(ctx, ctx->Om, es * (size_t)(n * lp)));
+  QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(std::max(m, n), 16) * kMaxB)));
+  const int64_t bp = round_up(kMaxB, 16);
+  QB_TRY(ensure(ctx, ctx->G, sizeof(double) * bp * bp));
+  QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (bp * bp + 8 * 32 * 32)));
+  QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * bp * bp));
+  QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)std::max<int64_t>(
+                                     ((m + GEMM_BM - 1) / GEMM_BM) * ((n + kBN - 1) / kBN), 16 * ctx->num_sms)));
+  if (P > 0) {
+    QB_TRY(ensure(ctx, ctx->Z, sizeof(double) * (size_t)(ldn * l)));
+    QB_TRY(ensure(ctx, ctx->Zt, es * (size_t)(n * lp)));
+  }
+  if (is_f32) QB_TRY(ensure(ctx, ctx->Q32, sizeof(float) * (size_t)(ldm * l)));
+  float* X32 = static_cast<float*>(ctx->Q32.p);
+  QB_TRY(reset_flags(ctx));
+
+  // Y (into Q̄'s storage) = A X for the row-major n x l operand X (ld lp)
+  auto sketch = [&](const void* X) -> qb_status {
+    if (is_f32)
+      return gemm_tf(ctx, GEMM_NN, TF_STORE_COL, (int)m, (int)l, (int)n, A32, ldA, static_cast<const float*>(X), lp,
+                     Qd, ldq, false, nullptr);
+    return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)l, (int)n, A, ldA, static_cast<const double*>(X), lp, Qd,
+                ldq, false, nullptr);
+  };
+  // Z = A^T Q̄ (n x l, ld ldn)
+  auto adjoint = [&]() -> qb_status {
+    if (!is_f32)
+      return gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)n, (int)l, (int)m, A, ldA, Qd, ldq, ctx->Z.d(), ldn, false,
+                  nullptr);
+    QB_TRY(launch_convert(ctx, static_cast<const double*>(Qd), ldq, m, l, X32, ldm));
+    return gemm_tf(ctx, GEMM_TN, TF_STORE_COL, (int)n, (int)l, (int)m, A32, ldA, X32, ldm, ctx->Z.d(), ldn, false,
+                   nullptr);
+  };
+  auto transpose_z = [&]() -> qb_status {
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((l + 31) / 32));
+    if (is_f32)
+      transpose_kernel<float><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, l,
+                                                                      static_cast<float*>(ctx->Zt.p), lp);
+    else
+      transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Z.d(), ldn, n, l, ctx->Zt.d(), lp);
+    return check_launch(ctx, "transpose");
+  };
+
+  // Omega = randn(n, l): global columns 0..l-1, row-major (ld lp); FP32 contexts draw RN_32(Omega)
+  QB_TRY(launch_omega(ctx, seed, 0, n, 0, l, ctx->Om.p, lp, is_f32 ? 1 : 0));
+  QB_TRY(sketch(ctx->Om.p));  // Y = A Omega
+  const bool skip_orth = skip_orth_flag(flags);
+  if (skip_orth) {
+    for (int j = 0; j < P; ++j) {  // Y = A (A^* Y)
+      QB_TRY(adjoint());
+      QB_TRY(transpose_z());
+      QB_TRY(sketch(ctx->Zt.p));
+    }
+    QB_TRY(orth_blocked(ctx, Qd, ldq, m, l));
+  } else {
+    QB_TRY(orth_blocked(ctx, Qd, ldq, m, l));  // Q = orth(A Omega)
+    for (int j = 0; j < P; ++j) {
+      QB_TRY(adjoint());                                   // Z = A^* Q
+      QB_TRY(orth_blocked(ctx, ctx->Z.d(), ldn, n, l));    // Z = orth(Z)
+      QB_TRY(transpose_z());
+      QB_TRY(sketch(ctx->Zt.p));                           // Q = A Z
+      QB_TRY(orth_blocked(ctx, Qd, ldq, m, l));            // Q = orth(Q)
+    }
+  }
+  // B = Q^* A (row-major l x n); FP32 contexts use RN_32(Q), the factor the caller receives
+  int64_t nparts = 0;
+  if (is_f32) {
+    QB_TRY(launch_convert(ctx, static_cast<const double*>(Qd), ldq, m, l, static_cast<float*>(ctx->Qbar32.p), ldq));
+    QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)l, (int)n, (int)m, static_cast<const float*>(ctx->Qbar32.p), ldq,
+                   A32, ldA, Bd, ctx->ldb, false, nullptr));
+  } else {
+    QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)l, (int)n, (int)m, Qd, ldq, A, ldA, Bd, ctx->ldb, false, nullptr));
+  }
+  double r = 0.0;
+  if (resid_out) {  // ||A - QB||_F, directly: A -= Q B with the fused sum of squares
+    if (is_f32) {
+      QB_TRY(ensure(ctx, ctx->B32, sizeof(float) * (size_t)(ctx->ldb * l)));
+      QB_TRY(launch_convert(ctx, static_cast<const double*>(Bd), ctx->ldb, n, l, static_cast<float*>(ctx->B32.p),
+                            ctx->ldb));
+      QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)n, (int)l, static_cast<const float*>(ctx->Qbar32.p), ldq,
+                     static_cast<const float*>(ctx->B32.p), ctx->ldb, A32, ldA, true, &nparts));
+    } else {
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)n, (int)l, Qd, ldq, Bd, ctx->ldb, A, ldA, true, &nparts));
+    }
+    QB_TRY(reduce_to_scal(ctx, nparts, 0));
+    QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->h_status[4]) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "qb_fixed_rank: CholeskyQR failed even with the shift");
+  if (resid_out) {
+    r = std::sqrt(ctx->h_scal[0]);
+    *resid_out = r;
+  }
+  ctx->last_m = m;
+  ctx->last_n = n;
+  ctx->last_k = l;
+  return publish_outputs(ctx, m, n, l, Q_out, ldq_out, B_out, ldb_out);
 }
 
 qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, double eps, int64_t b, int q,

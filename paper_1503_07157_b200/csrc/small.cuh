@@ -314,9 +314,11 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
   bool failed = false;
   for (; attempt < 2; ++attempt) {
     const double shift = attempt == 0 ? 0.0 : s_shift;
-    for (int idx = tid; idx < rows * nb; idx += CHOL_THREADS) {
+    // columns nb..31 of a narrow last panel are zero: the 32-wide products below multiply them
+    // by the zero upper triangle of L11^-1, and stale shared memory could hold NaN patterns
+    for (int idx = tid; idx < rows * CHOL_NB; idx += CHOL_THREADS) {
       const int i = idx % rows, j = idx / rows;
-      double v = __ldcg(G + (p0 + i) + static_cast<int64_t>(p0 + j) * ldg);
+      double v = j < nb ? __ldcg(G + (p0 + i) + static_cast<int64_t>(p0 + j) * ldg) : 0.0;
       if (i == j) v += shift;
       P[i * PLD + j] = v;
     }
@@ -420,7 +422,10 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
   CHOL_TS(30);
   // ---- block column J = cta of L^-1, right-looking over K = J .. nbk-1 (X rows 32J..w-1)
   if (active) {
-    for (int idx = tid; idx < rows * CHOL_NB; idx += CHOL_THREADS) X[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = 0.0;
+    // every 32-row block up to the last panel's, padding rows of a narrow last block included
+    // (their zeros meet the identity padding of L_KK^-1 in the finalisation)
+    for (int idx = tid; idx < (nbk - cta) * CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
+      X[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = 0.0;
     __syncthreads();
     const int r = tid >> 3, c0 = (tid & 7) * 4;  // thread owns X_KJ(r, c0..c0+3) when finalising
     for (int K = cta; K < nbk; ++K) {

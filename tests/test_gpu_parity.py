@@ -76,7 +76,8 @@ def test_omega_bitwise(qbmod, ctx, seed, n, row0, row1, col0, w):
 
 
 # ------------------------------------------------------------------------- orth
-@pytest.mark.parametrize("m,w", [(1000, 1), (1000, 7), (333, 64), (5000, 256), (2048, 128)])
+@pytest.mark.parametrize("m,w", [(1000, 1), (1000, 7), (333, 64), (5000, 256), (2048, 128), (3000, 97), (3000, 100),
+                                 (3000, 130), (3000, 200), (3000, 250)])
 def test_orth_parity(qbmod, ctx, m, w):
     X = np.random.default_rng(m + w).standard_normal((m, w))
     Xd = to_dev(X)
