@@ -98,6 +98,16 @@ qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_str
                          int rank, int nranks, const void* nccl_unique_id,
                          int64_t col_offset, int64_t n_global);
 
+/* Row-sharded distributed context (NEXT-2, tall-skinny A): this rank holds rows
+ * row_offset .. row_offset + m_local - 1 of an m_global x n matrix and passes that block to
+ * qb_factor with m = m_local.  Omega is replicated (all n rows), Y_i and Q_i stay local; the
+ * CholeskyQR Grams, the re-projection coefficients W, the power step's Z and B_i are summed
+ * with NCCL, so B is REPLICATED and Q is this rank's rows of Q.  rqb_svd works on it (U is
+ * this rank's rows).  Collective.  Errors as for qb_create_dist.                            */
+qb_status qb_create_dist_rows(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream,
+                              int rank, int nranks, const void* nccl_unique_id,
+                              int64_t row_offset, int64_t m_global);
+
 /* Write a fresh ncclUniqueId (128 bytes) to `out128`.  QB_ERR_NCCL if NCCL is absent.      */
 qb_status qb_nccl_unique_id(void* out128);
 

@@ -62,6 +62,8 @@ def lib():
         L.qb_create.argtypes = [P(c_ctx), ctypes.c_int, ctypes.c_int, vp]
         L.qb_create_dist.argtypes = [P(c_ctx), ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
                                      i64, i64]
+        L.qb_create_dist_rows.argtypes = [P(c_ctx), ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
+                                          i64, i64]
         L.qb_nccl_unique_id.argtypes = [vp]
         L.qb_factor.argtypes = [c_ctx, vp, i64, i64, i64, dbl, i64, ctypes.c_int, u64, i64, ctypes.c_uint,
                                 P(i64), P(vp), P(i64), P(vp), P(i64), P(dbl)]
@@ -84,7 +86,7 @@ def lib():
         L.qb_status_string.restype = ctypes.c_char_p
         L.qb_last_error.argtypes = [c_ctx]
         L.qb_last_error.restype = ctypes.c_char_p
-        for f in ("qb_create", "qb_create_dist", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_gemm", "qb_chol_rinv", "qb_stats", "qb_omega",
+        for f in ("qb_create", "qb_create_dist", "qb_create_dist_rows", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_gemm", "qb_chol_rinv", "qb_stats", "qb_omega",
                   "qb_orth", "rqb_svd", "qb_fixed_rank"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -132,11 +134,14 @@ def qb_nccl_unique_id():
     return buf.raw
 
 
-def qb_create_dist(device, rank, nranks, unique_id, col_offset, n_global, dtype=QB_F64, stream=None):
+def qb_create_dist(device, rank, nranks, unique_id, col_offset, n_global, dtype=QB_F64, stream=None, rows=False):
+    """Column-sharded context (rows=False: col_offset / n_global) or row-sharded context
+    (rows=True: the same two arguments are row_offset / m_global)."""
     ctx = ctypes.c_void_p()
     uid = ctypes.create_string_buffer(bytes(unique_id), 128)
-    s = lib().qb_create_dist(ctypes.byref(ctx), int(device), int(dtype), stream, int(rank), int(nranks), uid,
-                             int(col_offset), int(n_global))
+    fn = lib().qb_create_dist_rows if rows else lib().qb_create_dist
+    s = fn(ctypes.byref(ctx), int(device), int(dtype), stream, int(rank), int(nranks), uid, int(col_offset),
+           int(n_global))
     if s != QB_OK:
         msg = qb_last_error(ctx) if ctx.value else ""
         if ctx.value:
@@ -263,8 +268,9 @@ class QB:
     (``A.stride(0) == 1``)."""
 
     def __init__(self, device=0, dtype=QB_F64, stream=None, dist=None):
-        """dist: None, or dict(rank, nranks, unique_id, col_offset, n_global) for a
-        column-sharded context (see paper_1503_07157_b200.dist)."""
+        """dist: None, dict(rank, nranks, unique_id, col_offset, n_global) for a column-sharded
+        context, or dict(shard="rows", rank, nranks, unique_id, row_offset, m_global) for a
+        row-sharded one (see paper_1503_07157_b200.dist)."""
         # Default to torch's current stream on `device` so that the library's kernels are
         # stream-ordered after the torch work that produced their inputs.
         if stream is None:
@@ -274,8 +280,12 @@ class QB:
         if dist is None:
             self.ctx = qb_create(device, dtype, stream)
         else:
-            self.ctx = qb_create_dist(device, dist["rank"], dist["nranks"], dist["unique_id"], dist["col_offset"],
-                                      dist["n_global"], dtype, stream)
+            if dist.get("shard", "cols") == "rows":
+                self.ctx = qb_create_dist(device, dist["rank"], dist["nranks"], dist["unique_id"], dist["row_offset"],
+                                          dist["m_global"], dtype, stream, rows=True)
+            else:
+                self.ctx = qb_create_dist(device, dist["rank"], dist["nranks"], dist["unique_id"],
+                                          dist["col_offset"], dist["n_global"], dtype, stream)
 
     def close(self):
         qb_destroy(self.ctx)

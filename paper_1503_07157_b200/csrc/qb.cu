@@ -145,6 +145,9 @@ struct qb_ctx_s {
   // distributed (column sharding); nranks == 1 on a plain context
   int rank = 0, nranks = 1;
   int64_t col_offset = 0, n_global = 0;
+  // row sharding (NEXT-2, tall-skinny A): this rank holds rows row_offset .. of an m_global-row A
+  bool shard_rows = false;
+  int64_t row_offset = 0, m_global = 0;
   ncclComm_t comm = nullptr;  // set on distributed contexts (any nranks >= 1)
 
   DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status, Qf, Bf, Astage, Q32, B32,
@@ -773,6 +776,22 @@ qb_status init_ctx(qb_ctx ctx, int device, qb_dtype dtype, void* stream) {
 
 // Hand out Q̄ (column-major, ld ldq) and B̄ (row-major, ld ldb): the FP64 factors, or for an
 // FP32 context their RN_32 copies in context-owned FP32 buffers with the same layouts.
+// NCCL communicator of a distributed context (rank `rank` of `nranks`).
+qb_status init_comm(qb_ctx ctx, int rank, int nranks, const void* nccl_unique_id) {
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  if (!nccl().ok) return fail(ctx, QB_ERR_NCCL, "libnccl.so.2 not found (set QB_NCCL_LIB)");
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  QB_CUDA(cudaSetDevice(ctx->device));
+  ncclResult_t r = nccl().commInitRank(&ctx->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    ctx->comm = nullptr;
+    return fail(ctx, QB_ERR_NCCL, "ncclCommInitRank: %s", nccl().errorString(r));
+  }
+  return QB_OK;
+}
+
 qb_status publish_outputs(qb_ctx ctx, int64_t m, int64_t n, int64_t k, const void** Q_out, int64_t* ldq_out,
                           const void** B_out, int64_t* ldb_out) {
   const void* Qp = ctx->Qbar.p;
@@ -843,20 +862,22 @@ qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_str
   qb_ctx ctx = *out;
   if (nranks < 1 || rank < 0 || rank >= nranks || col_offset < 0 || n_global < 1 || !nccl_unique_id)
     return fail(ctx, QB_ERR_INVALID_ARG, "bad distributed arguments");
-  ctx->rank = rank;
-  ctx->nranks = nranks;
   ctx->col_offset = col_offset;
   ctx->n_global = n_global;
-  if (!nccl().ok) return fail(ctx, QB_ERR_NCCL, "libnccl.so.2 not found (set QB_NCCL_LIB)");
-  ncclUniqueId id;
-  std::memcpy(&id, nccl_unique_id, sizeof(id));
-  QB_CUDA(cudaSetDevice(device));
-  ncclResult_t r = nccl().commInitRank(&ctx->comm, nranks, id, rank);
-  if (r != ncclSuccess) {
-    ctx->comm = nullptr;
-    return fail(ctx, QB_ERR_NCCL, "ncclCommInitRank: %s", nccl().errorString(r));
-  }
-  return QB_OK;
+  return init_comm(ctx, rank, nranks, nccl_unique_id);
+}
+
+qb_status qb_create_dist_rows(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, int rank, int nranks,
+                              const void* nccl_unique_id, int64_t row_offset, int64_t m_global) {
+  qb_status s = qb_create(out, device, dtype, cuda_stream);
+  if (s != QB_OK) return s;
+  qb_ctx ctx = *out;
+  if (nranks < 1 || rank < 0 || rank >= nranks || row_offset < 0 || m_global < 1 || !nccl_unique_id)
+    return fail(ctx, QB_ERR_INVALID_ARG, "bad distributed arguments");
+  ctx->shard_rows = true;
+  ctx->row_offset = row_offset;
+  ctx->m_global = m_global;
+  return init_comm(ctx, rank, nranks, nccl_unique_id);
 }
 
 void qb_destroy(qb_ctx ctx) {
@@ -985,7 +1006,9 @@ qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_ou
   // k x k R = Ũ D Ṽ^T; then B̄ = R^T Q_B^T = Ṽ D (Q_B Ũ)^T, so Û = Ṽ, V = Q_B Ũ, U = Q̄ Ṽ.
   if (!ctx) return QB_ERR_INVALID_ARG;
   if (ctx->last_k < 0) return fail(ctx, QB_ERR_INVALID_ARG, "rqb_svd: no factorization to convert");
-  if (ctx->nranks > 1) return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: column-sharded B̄ (distributed) not supported");
+  // row shards: B̄ is replicated and U = Q̄ Ṽ is this rank's rows of U; column shards hold B̄ split
+  if (ctx->nranks > 1 && !ctx->shard_rows)
+    return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: column-sharded B̄ (distributed) not supported");
   if (!solver().ok) return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: libcusolver.so.11 not loadable");
   const int64_t m = ctx->last_m, n = ctx->last_n, k = ctx->last_k;
   const int64_t kk = (kkeep > 0 && kkeep < k) ? kkeep : k;
@@ -1283,8 +1306,13 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   if (b < 1 || b > kMaxB) return fail(ctx, QB_ERR_INVALID_ARG, "block size b=%lld outside [1, %lld]", (long long)b, (long long)kMaxB);
   if (q < 0) return fail(ctx, QB_ERR_INVALID_ARG, "q=%d < 0", q);
   if (!(eps >= 0.0)) return fail(ctx, QB_ERR_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
-  const int64_t n_glob = ctx->nranks > 1 ? ctx->n_global : n;
-  const int64_t kmax_eff = (kmax <= 0) ? std::min(m, n_glob) : std::min(kmax, std::min(m, n_glob));
+  // sharding: column shards allreduce Y (and the row-distributed Z's Gram);
+  // row shards (NEXT-2) allreduce Grams, W, Z and B_i instead, and keep Y, Q_i local
+  const bool rowsh = ctx->comm != nullptr && ctx->shard_rows;
+  const bool colsh = ctx->comm != nullptr && !ctx->shard_rows;
+  const int64_t n_glob = (colsh && ctx->nranks > 1) ? ctx->n_global : n;
+  const int64_t m_glob = (rowsh && ctx->nranks > 1) ? ctx->m_global : m;
+  const int64_t kmax_eff = (kmax <= 0) ? std::min(m_glob, n_glob) : std::min(kmax, std::min(m_glob, n_glob));
   QB_CUDA(cudaSetDevice(ctx->device));
 
   // ---- residual workspace A^(0) = A (A^(j) overwrites A^(j-1), :112)
@@ -1402,25 +1430,27 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp, is_f32 ? 1 : 0));
     // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
     QB_TRY(sketch(ctx->Om.p));
-    QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));  // Y = sum_p A_p Omega_p (column shards)
+    if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));  // Y = sum_p A_p Omega_p (column shards)
     QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
-    if (!(skip_orth_flag(flags) && q > 0)) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
+    if (!(skip_orth_flag(flags) && q > 0)) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     const bool skip_orth = (flags & QB_SKIP_POWER_ORTH) != 0;
     for (int j = 0; j < q && skip_orth; ++j) {  // NEXT-3: Y = A (A^* Y), orth once
       QB_TRY(adjoint(ctx->Y.d(), ldm));
+      if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->Z.d(), (size_t)(ldn * w)));  // Z = sum_p A_p^T Y_p
       QB_TRY(transpose_z());
       QB_TRY(sketch(ctx->Zt.p));
-      QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
+      if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
     }
-    if (skip_orth && q > 0) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
+    if (skip_orth && q > 0) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
     for (int j = 0; j < q && !skip_orth; ++j) {
       QB_TRY(adjoint(Qi, ctx->ldq));
-      QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, ctx->comm != nullptr));
+      if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->Z.d(), (size_t)(ldn * w)));  // Z = sum_p A_p^T Q_p
+      QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, colsh));
       QB_TRY(transpose_z());
       QB_TRY(sketch(ctx->Zt.p));
-      QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
-      QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w));
+      if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
+      QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
     float* Qbar32 = static_cast<float*>(ctx->Qbar32.p);
@@ -1432,6 +1462,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
         QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Qi32, ctx->ldq));
         QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)ell, (int)w, (int)m, Qbar32, ctx->ldq, Qi32, ctx->ldq,
                        ctx->W.d(), bp, false, nullptr));
+        if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->W.d(), (size_t)(ell * bp)));  // W = sum_p Q̄_p^T Q_p
         QB_TRY(launch_convert(ctx, ctx->W.d(), bp, w, ell, static_cast<float*>(ctx->W32.p), bp));
         QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)w, (int)ell, Qbar32, ctx->ldq,
                        static_cast<const float*>(ctx->W32.p), bp, Qi32, ctx->ldq, false, nullptr));
@@ -1439,10 +1470,11 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       } else {
         QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)ell, (int)w, (int)m, Qbar, ctx->ldq, Qi, ctx->ldq, ctx->W.d(),
                     bp, false, nullptr));
+        if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->W.d(), (size_t)(ell * bp)));  // W = sum_p Q̄_p^T Q_p
         QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)ell, Qbar, ctx->ldq, ctx->W.d(), bp, Qi,
                     ctx->ldq, false, nullptr));
       }
-      QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w));
+      QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, rowsh));
     }
     // FP32 contexts: Q̄32_i = RN_32(Q_i), the factor the caller receives and the residual's GEMMs use
     if (is_f32) QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Qi32, ctx->ldq));
@@ -1450,11 +1482,18 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     int64_t nb_parts = 0;
     QB_CUDA(cudaEventRecord(ctx->evp[2], ctx->stream));
     if (is_f32) {
-      QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)w, (int)n, (int)m, Qi32, ctx->ldq, A32, ldA, Bi, ctx->ldb, true,
-                     &nb_parts));
+      QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)w, (int)n, (int)m, Qi32, ctx->ldq, A32, ldA, Bi, ctx->ldb,
+                     !rowsh, &nb_parts));
     } else {
-      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)w, (int)n, (int)m, Qi, ctx->ldq, A, ldA, Bi, ctx->ldb, true,
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)w, (int)n, (int)m, Qi, ctx->ldq, A, ldA, Bi, ctx->ldb, !rowsh,
                   &nb_parts));
+    }
+    if (rowsh) {  // B_i = sum_p Q_p^T A_p, replicated; its norm from the reduced rows
+      QB_TRY(allreduce_sum(ctx, Bi, (size_t)(w * ctx->ldb)));
+      const int grid = (int)std::min<int64_t>(w, 4 * ctx->num_sms);
+      sumsq_kernel<double><<<grid, RED_THREADS, 0, ctx->stream>>>(Bi, n, w, ctx->ldb, ctx->parts.d());
+      QB_TRY(check_launch(ctx, "sumsq"));
+      nb_parts = grid;
     }
     QB_CUDA(cudaEventRecord(ctx->evp[3], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, nb_parts, 1));
@@ -1471,7 +1510,8 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     }
     QB_CUDA(cudaEventRecord(ctx->evp[5], ctx->stream));
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
-    QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 2));  // ||A^(i)||_F^2 and ||B_i||_F^2 over the shards
+    // ||A^(i)||_F^2 (and, on column shards, ||B_i||_F^2) summed over the shards
+    QB_TRY(allreduce_sum(ctx, ctx->scal.d(), rowsh ? 1 : 2));
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));

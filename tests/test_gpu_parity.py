@@ -278,6 +278,40 @@ def test_distributed_context_single_rank_bitwise(qbmod, q):
     assert torch.equal(g0["Q"], g1["Q"]) and torch.equal(g0["B"], g1["B"])
 
 
+@pytest.mark.parametrize("q", [0, 1])
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_row_sharded_context_single_rank(qbmod, q, dt):
+    """A row-sharded context (NEXT-2; NCCL communicator of one rank) runs the Gram / W / Z / B_i
+    allreduce code path; against the oracle like a plain context (FP32: FP32 tolerances)."""
+    try:
+        uid = qbmod.qb_nccl_unique_id()
+    except qbmod.QBError:
+        pytest.skip("NCCL not loadable")
+    A, _ = make(3000, 200, "exp_100", 19)
+    eps = 1e-3 if dt == "f32" else 1e-8
+    d = qbmod.QB(0, dtype=qbmod.QB_F32 if dt == "f32" else qbmod.QB_F64,
+                 dist=dict(shard="rows", rank=0, nranks=1, unique_id=uid, row_offset=0, m_global=3000))
+    if dt == "f32":
+        A32 = A.astype(np.float32)
+        Aw = A32.astype(np.float64)
+        o = oqb.randqb_pb(Aw, eps, 32, q, seed=4, omega_dtype=np.float32)
+        g = d.factor(torch.from_numpy(np.asfortranarray(A32)).cuda(), eps, 32, q, seed=4)
+        assert g["k"] == o.k
+        Qg, Bg = g["Q"].double().cpu().numpy(), g["B"].double().cpu().numpy()
+        nA = np.linalg.norm(Aw)
+        assert np.abs(Qg.T @ Qg - np.eye(g["k"])).max() <= 1e-5
+        assert np.linalg.norm(np.hstack([Qg, o.Q]) @ np.vstack([Bg, -o.B])) / nA <= 1e-4
+        assert np.linalg.norm(Aw - Qg @ Bg) <= eps * (1 + 1e-4) + 1e-6 * nA
+    else:
+        o = oqb.randqb_pb(A, eps, 32, q, seed=4)
+        g = d.factor(to_dev(A), eps, 32, q, seed=4)
+        check_parity(A, g, o, eps)
+        s = d.svd()   # rqb_svd on a row-sharded context (B replicated)
+        np.testing.assert_allclose(s["S"].cpu().numpy(), np.linalg.svd(o.B, compute_uv=False),
+                                   rtol=0, atol=1e-10 * np.linalg.norm(A))
+    d.close()
+
+
 @pytest.mark.parametrize("case", [(400, 300, "exp10_20", 1e-4, 10, 0), (3000, 200, "exp_100", 1e-3, 32, 0),
                                   (1000, 260, "poly2", 1e-4, 64, 1)])
 def test_fp32_path_parity(qbmod, case):
