@@ -105,8 +105,18 @@ def dist_env():
 
 
 def make_A(cfg, device):
+    import torch
     import synth
-    return synth.make_matrix_torch(cfg.m, cfg.n, synth.config_sigma(cfg), cfg.seed_matrix, device=device)
+    dt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    return synth.make_matrix_torch(cfg.m, cfg.n, synth.config_sigma(cfg), cfg.seed_matrix, device=device, dtype=dt)
+
+
+def hbm_peak():
+    """Measured copy bandwidth (driver-written MEASURED_PEAKS.json), else the guide's figure."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 7700.0, "B200_PROFILING.md nominal HBM3e 7.7 TB/s"
 
 
 def oracle_sample(A_np, cfg, blocks):
@@ -180,16 +190,37 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     dspec = None
     sig = synth.config_sigma(cfg)
+    f32 = cfg.dtype == "f32"
+    tdt = torch.float32 if f32 else torch.float64
+    es = 4 if f32 else 8
+    # tall-skinny workloads shard rows (NEXT-2), square ones columns; --shard overrides
+    rows = (args.shard == "rows") or (args.shard == "auto" and cfg.m >= 8 * cfg.n)
+    m_global, m_local = cfg.m, cfg.m
     if ws > 1:
-        from paper_1503_07157_b200.dist import dist_spec, shard_columns
+        from paper_1503_07157_b200.dist import dist_spec, dist_spec_rows
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        n_global = cfg.n if args.strong else cfg.n * ws
-        dspec = dist_spec(n_global)
+        if rows:
+            m_global = cfg.m if args.strong else cfg.m * ws
+            dspec = dist_spec_rows(m_global)
+        else:
+            n_global = cfg.n if args.strong else cfg.n * ws
+            dspec = dist_spec(n_global)
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream(dev)
     if dspec is None:
         A0 = make_A(cfg, dev)
         n_global, n_local = cfg.n, cfg.n
+    elif rows:
+        n_global, n_local = cfg.n, cfg.n
+        if args.strong:
+            Af = make_A(cfg, dev)
+            off, m_local = dspec["row_offset"], dspec["m_local"]
+            A0 = Af[off:off + m_local].t().contiguous().t()
+            del Af
+        else:
+            m_local = cfg.m
+            dspec["row_offset"], dspec["m_local"] = rank * m_local, m_local
+            A0 = synth.make_row_shard_torch(m_local, cfg.n, sig, cfg.seed_matrix, rank, ws, device=dev, dtype=tdt)
     elif args.strong:
         Af = make_A(cfg, dev)
         off, n_local = dspec["col_offset"], dspec["n_local"]
@@ -200,10 +231,10 @@ def run_ours(args, cfg):
         n_local = cfg.n
         n_global = cfg.n * ws
         dspec["col_offset"], dspec["n_local"] = rank * n_local, n_local
-        A0 = synth.make_shard_torch(cfg.m, n_local, sig, cfg.seed_matrix, rank, ws, device=dev)
+        A0 = synth.make_shard_torch(cfg.m, n_local, sig, cfg.seed_matrix, rank, ws, device=dev, dtype=tdt)
     torch.cuda.synchronize()
-    ctx = qbp.QB(local, stream=ctypes_stream(stream), dist=dspec)
-    m, b, q = cfg.m, cfg.b, cfg.q
+    ctx = qbp.QB(local, dtype=qbp.QB_F32 if f32 else qbp.QB_F64, stream=ctypes_stream(stream), dist=dspec)
+    m, b, q = m_local, cfg.b, cfg.q
 
     def step():
         return ctx.factor(A0, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=False)
@@ -234,35 +265,46 @@ def run_ours(args, cfg):
         ms = float(t.item())
         dist.barrier()
     k, stats = g["k"], g["stats"]
-    F = falg(m, n_global, k, b, q, len(stats))
+    F = falg(m_global, n_global, k, b, q, len(stats))
     value = F / (ms * 1e-3) * 1e-9
     peak, peak_src, cublas = fp64_peak()
 
     # roofline of the dominant kernel: the downdate GEMM A -= Q_i B_i (fused norm epilogue)
-    full = [s for s in stats if s["w"] == b]
+    full = [s for s in stats if s["w"] == b] or stats
     t_down = statistics.mean(s["ms_down"] for s in full) * 1e-3
-    achieved = 2.0 * m * n_local * b / t_down * 1e-12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01c.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("downdate_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "gemm_f64_kernel<NN,64,SUB_COL> (A -= Q_i B_i, fused ||A||_F^2)",
-                "peak_source": peak_src,
-                "algorithmic_per_launch": f"2*m*n_local*b = {2.0 * m * n_local * b:.4g} flop",
-                "share_of_step": sum(s["ms_down"] for s in stats) / ms}
+    if not f32:
+        achieved = 2.0 * m * n_local * b / t_down * 1e-12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_summary_r01c.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("downdate_dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "kernel": "gemm_f64_kernel<NN,64,SUB_COL> (A -= Q_i B_i, fused ||A||_F^2)",
+                    "peak_source": peak_src,
+                    "algorithmic_per_launch": f"2*m*n_local*b = {2.0 * m * n_local * b:.4g} flop",
+                    "share_of_step": sum(s["ms_down"] for s in stats) / ms}
+    else:  # FP32: the 3xTF32 subtract-update streams A in and out of HBM (K = b is short)
+        hbm, hbm_src = hbm_peak()
+        achieved = 2.0 * m * n_local * 4 / t_down * 1e-9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "traffic": None,
+                    "kernel": "gemm_tf32_kernel<NN,128,SUB_COL> (A -= Q_i B_i, 3xTF32, fused ||A||_F^2)",
+                    "peak_source": hbm_src,
+                    "algorithmic_per_launch": f"2*m*n_local*4 = {2.0 * m * n_local * 4:.4g} bytes (A read + write)",
+                    "share_of_step": sum(s["ms_down"] for s in stats) / ms}
 
     # end to end through the host-buffer entry point: H2D of A, D2H of Q and B per step
     e2e = None
     if not args.no_e2e:
-        A_h = torch.empty((n_local, m), dtype=torch.float64, pin_memory=True).t()   # column-major host A
+        A_h = torch.empty((n_local, m), dtype=tdt, pin_memory=True).t()   # column-major host A
         A_h.copy_(A0)
         kcap = k + b
-        Q_h = torch.empty((kcap, m), dtype=torch.float64, pin_memory=True)
-        B_h = torch.empty((kcap, n_local), dtype=torch.float64, pin_memory=True)
+        Q_h = torch.empty((kcap, m), dtype=tdt, pin_memory=True)
+        B_h = torch.empty((kcap, n_local), dtype=tdt, pin_memory=True)
         res = qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n_local, m, cfg.eps, b, q, cfg.seed_omega, 0,
                                  Q_h.data_ptr(), m, B_h.data_ptr(), n_local, kcap)
         torch.cuda.synchronize()
@@ -283,10 +325,10 @@ def run_ours(args, cfg):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         ke = res["k"]
-        e2e = {"value": falg(m, n_global, ke, b, q, -(-ke // b)) / (ems * 1e-3) * 1e-9, "unit": "GFLOP/s",
-               "ms_per_step": ems, "h2d_bytes_per_step": ws * m * n_local * 8,
-               "d2h_bytes_per_step": ws * ke * (m + n_local) * 8 + 16,
-               "entry_point": "qb_factor_host (pinned host A, Q, B; every rank its column block)"}
+        e2e = {"value": falg(m_global, n_global, ke, b, q, -(-ke // b)) / (ems * 1e-3) * 1e-9, "unit": "GFLOP/s",
+               "ms_per_step": ems, "h2d_bytes_per_step": ws * m * n_local * es,
+               "d2h_bytes_per_step": ws * ke * (m + n_local) * es + 16,
+               "entry_point": "qb_factor_host (pinned host A, Q, B; every rank its shard)"}
         del A_h, Q_h, B_h
 
     cpu = None
@@ -300,17 +342,21 @@ def run_ours(args, cfg):
 
     if rank == 0:
         scaling = "strong" if (ws > 1 and args.strong) else "weak"
-        par = "single" if ws == 1 else f"column-sharded x{ws} (NCCL allreduce of Y_i, Gram, norms)"
+        par = "single" if ws == 1 else (
+            f"row-sharded x{ws} (NCCL allreduce of Grams, W, Z, B_i, norms)" if rows else
+            f"column-sharded x{ws} (NCCL allreduce of Y_i, Gram, norms)")
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
                 "config": {"workload": workload_desc(cfg) + ("" if ws == 1 else
-                           f"; {'one matrix sharded' if args.strong else 'weak: m x %d global' % n_global}"),
-                           "m": m, "n": n_global, "n_per_gpu": n_local, "b": b, "q": q, "eps": cfg.eps,
-                           "k": k, "blocks": len(stats), "parallelism": par,
-                           "l2": "inputs larger than L2 (A is 3.2 GB; every step reads it >= 3 times)"},
-                "seconds_to_eps": ms * 1e-3, "frac_fp64_peak": value / ws / (peak * 1e3),
-                "frac_cublas_dgemm": (value / ws / (cublas * 1e3)) if cublas else None,
+                           f"; {'one matrix sharded' if args.strong else 'weak: %d x %d global' % (m_global, n_global)}"),
+                           "m": m_global, "n": n_global, "m_per_gpu": m, "n_per_gpu": n_local, "b": b, "q": q,
+                           "eps": cfg.eps, "k": k, "blocks": len(stats), "parallelism": par,
+                           "l2": f"inputs larger than L2 (A is {m * n_local * es / 1e9:.1f} GB per GPU; every step "
+                                 "reads it >= 3 times)"},
+                "seconds_to_eps": ms * 1e-3,
+                "frac_fp64_peak": None if f32 else value / ws / (peak * 1e3),
+                "frac_cublas_dgemm": (value / ws / (cublas * 1e3)) if (cublas and not f32) else None,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk}
         print(json.dumps(line), flush=True)
@@ -336,6 +382,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--strong", action="store_true", help="N > 1: shard one matrix (strong scaling)")
+    ap.add_argument("--shard", default="auto", choices=["auto", "cols", "rows"],
+                    help="N > 1: shard columns (square A) or rows (tall-skinny A, NEXT-2); auto picks rows "
+                         "when m >= 8 n")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -131,6 +131,27 @@ def make_shard_torch(m, n_local, sig, seed, rank, nranks, device="cuda", dtype=N
     return At.to(dtype).t()
 
 
+def make_row_shard_torch(m_local, n, sig, seed, rank, nranks, device="cuda", dtype=None):
+    """Row block `rank` of the (nranks * m_local) x n matrix
+    A = [U_0; ...; U_{P-1}] diag(σ) V^T / sqrt(P), each U_p an m_local x r orthonormal factor:
+    the stacked left factor has orthonormal columns, so A has exactly the singular values σ for
+    every P (the row-sharded analogue of make_shard_torch, for tall-skinny weak scaling)."""
+    import torch
+    dtype = dtype or torch.float64
+    r = len(sig)
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    s = torch.as_tensor(np.asarray(sig), dtype=torch.float64, device=device) / np.sqrt(nranks)
+    V, _ = torch.linalg.qr(torch.randn(n, r, generator=g, dtype=torch.float64, device=device))
+    if rank > 0:
+        g = torch.Generator(device=device)
+        g.manual_seed(int(seed) * 1000003 + int(rank))
+    U, _ = torch.linalg.qr(torch.randn(m_local, r, generator=g, dtype=torch.float64, device=device))
+    At = (V * s[None, :]) @ U.T          # n x m_local contiguous = A_p^T
+    del U, V
+    return At.to(dtype).t()
+
+
 def config_sigma(cfg):
     return sigma(cfg.spectrum, cfg.rank)
 
