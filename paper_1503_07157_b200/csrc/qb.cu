@@ -621,22 +621,33 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
 // row_distributed: src holds this rank's rows of a matrix whose rows are spread over the
 // ranks (the power step's Z = A^T Q on column shards); the Gram is summed with NCCL and the
 // replicated T applied to the local rows.
+// single = true (cholqr1 below): the second pass runs only after a SHIFTED first factorization
+// (then the whole shifted CholeskyQR3 runs); otherwise a factorized first pass is final.
 qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
-                  bool row_distributed = false) {
+                  bool row_distributed = false, bool single = false) {
   const int64_t ldt = round_up(m, 16);
   double* T = ctx->T1.d();
   QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, 2 * sizeof(int), ctx->stream));
   QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr, row_distributed));
   // second pass only after a factorization (status[2]); a Newton-Schulz first pass is final
-  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 2, row_distributed));
+  const int* gate2 = status_dev(ctx) + (single ? 1 : 2);
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, gate2, row_distributed));
   {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
-    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, status_dev(ctx) + 2);
+    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, gate2);
     QB_TRY(check_launch(ctx, "gated_copy"));
   }
   QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed));
   QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed));
   return QB_OK;
+}
+
+// One CholeskyQR pass (reading R11b): used for the orth of line (3)/(6) when the re-projection
+// and its CholeskyQR2 follow in the same block; the orth after the projection restores full
+// orthogonality.  A first pass that needed the shift still runs the whole shifted CholeskyQR3.
+qb_status cholqr1(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
+                  bool row_distributed = false) {
+  return cholqr2(ctx, src, lds, dst, ldd, m, w, row_distributed, true);
 }
 
 // Orthonormalise the m x l column-major panel X (ld ldx) in place for any l: 256 columns at a
@@ -1432,7 +1443,17 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(sketch(ctx->Om.p));
     if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));  // Y = sum_p A_p Omega_p (column shards)
     QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
-    if (!(skip_orth_flag(flags) && q > 0)) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
+    // orth of line (3); a single CholeskyQR pass when the re-projection's orth follows (R11b)
+    static const int full_first_orth = debug_env("QB_FULL_FIRST_ORTH");  // experiment: 1 = CholeskyQR2 always
+    const bool reproj_follows = ell > 0 && !(flags & QB_NO_REPROJ) && !full_first_orth;
+    auto orth_y = [&]() -> qb_status {
+      return reproj_follows ? cholqr1(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh)
+                            : cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh);
+    };
+    if (!(skip_orth_flag(flags) && q > 0)) {
+      if (q == 0) QB_TRY(orth_y());
+      else QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
+    }
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     const bool skip_orth = (flags & QB_SKIP_POWER_ORTH) != 0;
     for (int j = 0; j < q && skip_orth; ++j) {  // NEXT-3: Y = A (A^* Y), orth once
@@ -1442,7 +1463,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       QB_TRY(sketch(ctx->Zt.p));
       if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
     }
-    if (skip_orth && q > 0) QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
+    if (skip_orth && q > 0) QB_TRY(orth_y());
     for (int j = 0; j < q && !skip_orth; ++j) {
       QB_TRY(adjoint(Qi, ctx->ldq));
       if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->Z.d(), (size_t)(ldn * w)));  // Z = sum_p A_p^T Q_p
@@ -1450,7 +1471,8 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       QB_TRY(transpose_z());
       QB_TRY(sketch(ctx->Zt.p));
       if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
-      QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
+      if (j == q - 1) QB_TRY(orth_y());  // the last orth of the power scheme, line (6)
+      else QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
     float* Qbar32 = static_cast<float*>(ctx->Qbar32.p);
