@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
     }
     } else {  // EPI_SUB_COL: C -= acc with C read from the prefetched smem tile, sum of squares
     mbar_wait(cbar, 0);
-    double sq = 0.0;
+    double sq = 0.0, sq2 = 0.0;  // two independent FP64 chains (latency)
 #pragma unroll
     for (int mi = 0; mi < 8; ++mi) {
       const int ml = wm * 64 + mi * 8 + (lane >> 2);
@@ -298,12 +298,13 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
           if (m < p.M && n < p.N) {
             const double v = c - acc[mi][ni][e];
             __stcg(p.C + m + static_cast<int64_t>(n) * p.ldc, v);
-            sq = fma(v, v, sq);
+            if (e == 0) sq = fma(v, v, sq);
+            else sq2 = fma(v, v, sq2);
           }
         }
     }
     if (p.norm_partials != nullptr) {
-      sq = warp_sum(sq);
+      sq = warp_sum(sq + sq2);
       if (lane == 0) red[warp] = sq;
       __syncthreads();
       if (tid == 0) {

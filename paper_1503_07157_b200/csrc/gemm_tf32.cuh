@@ -428,12 +428,15 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           const int slot = cs % TF_CSLOTS;
           mbar_wait(&cfull[slot], (cs / TF_CSLOTS) & 1);
           float* cb = sC + slot * (TF_BM * TF_CSUB);
+          double s4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent FP64 chains (latency)
 #pragma unroll
           for (int i = 0; i < TF_CSUB; ++i) {
             const float r = cb[i * TF_BM + row] - acc[sub * TF_CSUB + i];
             cb[i * TF_BM + row] = r;
-            if (sub * TF_CSUB + i < ncols) sq = fma(static_cast<double>(r), static_cast<double>(r), sq);
+            const double rd = sub * TF_CSUB + i < ncols ? static_cast<double>(r) : 0.0;
+            s4[i & 3] = fma(rd, rd, s4[i & 3]);
           }
+          sq += (s4[0] + s4[1]) + (s4[2] + s4[3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("bar.sync 2, 128;" ::: "memory");
           if (warp == 6 && lane == 0) {

@@ -159,6 +159,15 @@ struct qb_ctx_s {
   cudaEvent_t evp[6] = {};  // phase events: sketch, B, downdate (begin/end)
   std::vector<qb_block_stats> stats;
   int64_t last_m = 0, last_n = 0, last_k = -1;  // the last qb_factor (for rqb_svd); -1: none
+  // qb_factor_host: each finished block's Q_i / B_i is copied to these pinned host buffers on a
+  // copy stream while the next block computes
+  struct {
+    void* Q = nullptr;
+    void* B = nullptr;
+    int64_t ldq = 0, ldb = 0, kcap = 0;
+  } hout;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy = nullptr;
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
   cusolverDnHandle_t solver = nullptr;
   int block_fallbacks = 0;
@@ -733,6 +742,7 @@ qb_status grow_factors(qb_ctx ctx, int64_t m, int64_t n, int64_t need, int64_t k
     if (ctx->Qbar32.p) QB_CUDA(cudaFree(ctx->Qbar32.p));
     ctx->Qbar32 = nq32;
   }
+  if (ctx->copy_stream) QB_CUDA(cudaStreamSynchronize(ctx->copy_stream));  // block copies read the old factors
   if (ctx->Qbar.p) QB_CUDA(cudaFree(ctx->Qbar.p));
   if (ctx->Bbar.p) QB_CUDA(cudaFree(ctx->Bbar.p));
   ctx->Qbar = nq;
@@ -910,6 +920,11 @@ void qb_destroy(qb_ctx ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->comm) nccl().commDestroy(ctx->comm);
   if (ctx->solver) solver().destroy(ctx->solver);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1561,6 +1576,22 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     st.ms_down = ms;
     st.fallback = ctx->block_fallbacks;
     ctx->stats.push_back(st);
+    if (ctx->hout.Q && ell - w < ctx->hout.kcap) {
+      // the block is final (host-synchronised above): its Q_i columns and B_i rows go to the
+      // host on the copy stream while the next block computes
+      const int64_t c0 = ell - w, wc = std::min(w, ctx->hout.kcap - c0);
+      const size_t es = is_f32 ? 4 : 8;
+      const void* qsrc = is_f32 ? static_cast<const void*>(static_cast<const float*>(ctx->Qbar32.p) + c0 * ctx->ldq)
+                                : static_cast<const void*>(ctx->Qbar.d() + c0 * ctx->ldq);
+      const void* bsrc = is_f32 ? ctx->B32.p : static_cast<const void*>(ctx->Bbar.d() + c0 * ctx->ldb);
+      QB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->hout.Q) + c0 * ctx->hout.ldq * es, ctx->hout.ldq * es, qsrc,
+                                ctx->ldq * es, m * es, wc, cudaMemcpyDeviceToHost, ctx->copy_stream));
+      QB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->hout.B) + c0 * ctx->hout.ldb * es, ctx->hout.ldb * es, bsrc,
+                                ctx->ldb * es, n * es, wc, cudaMemcpyDeviceToHost, ctx->copy_stream));
+      // FP32: B32 is rewritten by the next block; the main stream waits for this copy first
+      QB_CUDA(cudaEventRecord(ctx->ev_copy, ctx->copy_stream));
+      QB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
+    }
     if (!std::isfinite(r2)) return fail(ctx, QB_ERR_CUDA, "non-finite residual after block ending at %lld", (long long)ell);
     if (r2 <= eps2) break;  // line (11): stop test (R1, R4)
   }
@@ -1589,13 +1620,22 @@ qb_status qb_factor_host(qb_ctx ctx, const void* A_host, int64_t m, int64_t n, i
   const void* Qd = nullptr;
   const void* Bd = nullptr;
   int64_t ldq = 0, ldb = 0;
-  qb_status s = qb_factor(ctx, dst.p, m, n, ldA, eps, b, q, seed, kmax, QB_OVERWRITE_A, k, &Qd, &ldq, &Bd, &ldb, resid);
-  if (s != QB_OK && s != QB_NOT_CONVERGED) return s;
-  const int64_t kc = std::min(*k, kcap_host);
-  if (kc > 0) {
-    QB_CUDA(cudaMemcpy2DAsync(Q_host, ldq_host * es, Qd, ldq * es, m * es, kc, cudaMemcpyDeviceToHost, ctx->stream));
-    QB_CUDA(cudaMemcpy2DAsync(B_host, ldb_host * es, Bd, ldb * es, n * es, kc, cudaMemcpyDeviceToHost, ctx->stream));
+  if (!ctx->copy_stream) {
+    QB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    QB_CUDA(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
   }
+  // Q_i / B_i stream to the host block by block inside qb_factor (overlapping the next block)
+  ctx->hout.Q = kcap_host > 0 ? Q_host : nullptr;
+  ctx->hout.B = B_host;
+  ctx->hout.ldq = ldq_host;
+  ctx->hout.ldb = ldb_host;
+  ctx->hout.kcap = kcap_host;
+  qb_status s = qb_factor(ctx, dst.p, m, n, ldA, eps, b, q, seed, kmax, QB_OVERWRITE_A, k, &Qd, &ldq, &Bd, &ldb, resid);
+  ctx->hout.Q = nullptr;
+  ctx->hout.B = nullptr;
+  const cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+  if (s != QB_OK && s != QB_NOT_CONVERGED) return s;
+  if (ce != cudaSuccess) return fail(ctx, QB_ERR_CUDA, "qb_factor_host copies: %s", cudaGetErrorString(ce));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
   return s;
 }

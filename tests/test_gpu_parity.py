@@ -345,3 +345,27 @@ def test_skip_power_orth_parity(qbmod, ctx, q):
     o = oqb.randqb_pb(A, eps, 20, q, seed=1, skip_power_orth=True)
     g = ctx.factor(to_dev(A), eps, 20, q, seed=1, flags=qbmod.QB_SKIP_POWER_ORTH)
     check_parity(A, g, o, eps)
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_factor_host_entry_point(qbmod, dt):
+    """qb_factor_host (the end-to-end entry point): host A in, Q / B streamed to host buffers block
+    by block (overlapping the next block); equal to the device entry point's factors, and kcap
+    truncates the copy."""
+    A, _ = make(900, 700, "exp10_25", 23)
+    npdt = np.float32 if dt == "f32" else np.float64
+    Ah = np.asfortranarray(A.astype(npdt))
+    c = qbmod.QB(0, dtype=qbmod.QB_F32 if dt == "f32" else qbmod.QB_F64)
+    g = c.factor(torch.from_numpy(Ah).cuda(), 1e-5, 32, 0, seed=3)
+    k = g["k"]
+    for kcap in (k + 5, k - 40):
+        Qh = np.full((kcap, 900), np.nan, dtype=npdt)      # column-major 900 x kcap
+        Bh = np.full((kcap, 700), np.nan, dtype=npdt)      # row-major kcap x 700
+        r = qbmod.qb_factor_host(c.ctx, Ah.ctypes.data, 900, 700, 900, 1e-5, 32, 0, 3, 0, Qh.ctypes.data, 900,
+                                 Bh.ctypes.data, 700, kcap)
+        assert r["k"] == k and abs(r["resid"] - g["resid"]) <= 1e-12 * np.linalg.norm(A)
+        kc = min(k, kcap)
+        assert np.array_equal(Qh[:kc].T, g["Q"][:, :kc].cpu().numpy())
+        assert np.array_equal(Bh[:kc], g["B"][:kc].cpu().numpy())
+        assert np.isnan(Qh[kc:]).all() and np.isnan(Bh[kc:]).all()
+    c.close()
