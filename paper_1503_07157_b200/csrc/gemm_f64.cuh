@@ -43,11 +43,19 @@ struct GemmParams {
   int a3d, b3d;          // NN: operand maps are 3D {16, K, rows/16} -> one TMA per operand per stage
 };
 
-template <int BN>
+#ifndef QB_SUB_CTAS
+#define QB_SUB_CTAS 3
+#endif
+#ifndef QB_ALL_CTAS
+#define QB_ALL_CTAS 2
+#endif
+template <int BN, int EPI = 0>
 struct GemmCfg {
   static constexpr int WARPS = (GEMM_BM / 64) * (BN / 32);
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int STAGES = BN == 64 ? 4 : 5;
+  // subtract-updates (short K = b, epilogue-heavy) may run QB_SUB_CTAS CTAs per SM
+  static constexpr bool SUB3 = BN == 64 && ((EPI == 2 && QB_SUB_CTAS == 3) || QB_ALL_CTAS == 3);
+  static constexpr int STAGES = SUB3 ? 3 : (BN == 64 ? 4 : 5);
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 8;
   static constexpr int B_BYTES = BN * GEMM_BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -58,14 +66,14 @@ struct GemmCfg {
   static constexpr int C_PER_SLOT = STAGE_BYTES / C_BOX_BYTES;
   static constexpr int C_GROUPS = (GEMM_BM / 16 + C_PER_SLOT - 1) / C_PER_SLOT;
   static_assert(C_PER_SLOT >= 1 && C_GROUPS <= STAGES, "C tile must fit in the drained pipeline slots");
-  static constexpr int MIN_BLOCKS = BN == 64 ? 2 : 1;
+  static constexpr int MIN_BLOCKS = SUB3 ? 3 : (BN == 64 ? 2 : 1);
 };
 
-template <int LAYOUT, int BN>
+template <int LAYOUT, int BN, int EPI>
 __device__ __forceinline__ void gemm_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, uint8_t* sA,
                                                  uint8_t* sB, uint64_t* bar, int m0, int n0, int k0, int a3d,
                                                  int b3d) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   mbar_arrive_expect_tx(bar, Cfg::STAGE_BYTES);
   if (LAYOUT == GEMM_NN) {
     // the 16-row chunks of an MN-contiguous tile land at c * 2048 either way; a 3D map
@@ -89,10 +97,10 @@ __device__ __forceinline__ void gemm_issue_stage(const CUtensorMap* tA, const CU
 }
 
 // Issue the TMA loads of C-tile box group g (EPI_SUB_COL prefetch) into pipeline slot `slot`.
-template <int BN>
+template <int BN, int EPI>
 __device__ __forceinline__ void gemm_issue_c_group(const CUtensorMap* tC, uint8_t* smem, uint64_t* cbar, int g, int slot,
                                                    int m0, int n0) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
 #pragma unroll
   for (int j = 0; j < Cfg::C_PER_SLOT; ++j) {
     const int b = g * Cfg::C_PER_SLOT + j;
@@ -101,10 +109,10 @@ __device__ __forceinline__ void gemm_issue_c_group(const CUtensorMap* tC, uint8_
 }
 
 template <int LAYOUT, int BN, int EPI>
-__global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
+__global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, GemmCfg<BN, EPI>::MIN_BLOCKS)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                     const __grid_constant__ CUtensorMap tC, const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   constexpr int STAGES = Cfg::STAGES;
   if (p.gate != nullptr && __ldcg(p.gate) == 0) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -154,11 +162,11 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
       // groups whose slot no k-tile ever uses go out right away
       for (int g = 0; g < Cfg::C_GROUPS; ++g) {
         const int t = nk - Cfg::C_GROUPS + g;
-        if (t < 0) gemm_issue_c_group<BN>(&tC, smem, cbar, g, ((t % STAGES) + STAGES) % STAGES, m0, n0);
+        if (t < 0) gemm_issue_c_group<BN, EPI>(&tC, smem, cbar, g, ((t % STAGES) + STAGES) % STAGES, m0, n0);
       }
     }
       for (int s = 0; s < STAGES && s < nk; ++s)
-      gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + s * Cfg::STAGE_BYTES, smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES,
+      gemm_issue_stage<LAYOUT, BN, EPI>(&tA, &tB, smem + s * Cfg::STAGE_BYTES, smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES,
                                    &full[s], m0, n0, (kt0 + s) * GEMM_BK, p.a3d, p.b3d);
   }
 
@@ -199,12 +207,12 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, GemmCfg<BN>::MIN_BLOCKS)
     const uint32_t par = (j / STAGES) & 1;
     if (j + STAGES < nk) {
       mbar_wait(&empty[slot], par);
-      gemm_issue_stage<LAYOUT, BN>(&tA, &tB, smem + slot * Cfg::STAGE_BYTES,
+      gemm_issue_stage<LAYOUT, BN, EPI>(&tA, &tB, smem + slot * Cfg::STAGE_BYTES,
                                    smem + slot * Cfg::STAGE_BYTES + Cfg::A_BYTES, &full[slot], m0, n0,
                                    (kt0 + j + STAGES) * GEMM_BK, p.a3d, p.b3d);
     } else if (kPrefetchC && j >= nk - Cfg::C_GROUPS) {
       mbar_wait(&empty[slot], par);
-      gemm_issue_c_group<BN>(&tC, smem, cbar, j - (nk - Cfg::C_GROUPS), slot, m0, n0);
+      gemm_issue_c_group<BN, EPI>(&tC, smem, cbar, j - (nk - Cfg::C_GROUPS), slot, m0, n0);
     }
   };
 

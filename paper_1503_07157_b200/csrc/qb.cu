@@ -277,7 +277,7 @@ qb_status make_map(qb_ctx ctx, CUtensorMap* map, const double* ptr, uint64_t inn
 template <int LAYOUT, int BN, int EPI>
 qb_status launch_gemm_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                         const GemmParams& p, int splits) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   auto kern = gemm_f64_kernel<LAYOUT, BN, EPI>;
   static bool attr_done = false;
   if (!attr_done) {
