@@ -275,7 +275,7 @@ def run_ours(args, cfg):
     if not f32:
         achieved = 2.0 * m * n_local * b / t_down * 1e-12
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_summary_r01c.json")
+        prof = os.path.join(ROOT, "profiles", "ncu_summary_r01d.json")
         if os.path.exists(prof):
             try:
                 traffic = json.load(open(prof)).get("downdate_dram_bytes_per_launch")
