@@ -206,6 +206,18 @@ qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_
 qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U, int64_t* ldu, const void** S,
                   const void** V, int64_t* ldv);
 
+/* Partial pivoted QR from the context's last factorization (NEXT-4):
+ * B P = Q~ R by Householder QR with column pivoting of the k x n factor B (LAPACK dlaqp2
+ * order: first column of largest partial norm, norms downdated and recomputed on cancellation),
+ * Q^ = Q Q~, so that A P ~ Q^ R.  FP64 internally.
+ * Outputs: perm (HOST, n entries, caller-owned): column j of A P is column perm[j] of A;
+ * Q^ device column-major m x k (*ldqh); R device ROW-major k x n upper trapezoidal (*ldr);
+ * both context-owned, in the context's dtype, valid until the next call.  k = 0 gives the
+ * identity permutation and NULL factors.  Errors: QB_ERR_INVALID_ARG without a factorization,
+ * QB_ERR_UNSUPPORTED on column-sharded contexts.  Blocking.                                */
+qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm, const void** Qh, int64_t* ldqh, const void** R,
+                        int64_t* ldr);
+
 /* Number of the library's own kernel launches since the context was created.              */
 int64_t qb_kernel_launches(qb_ctx ctx);
 

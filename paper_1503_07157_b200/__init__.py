@@ -76,6 +76,7 @@ def lib():
         L.qb_omega.argtypes = [c_ctx, u64, i64, i64, i64, i64, vp, i64]
         L.qb_orth.argtypes = [c_ctx, vp, i64, i64, i64]
         L.rqb_svd.argtypes = [c_ctx, i64, P(vp), P(i64), P(vp), P(vp), P(i64)]
+        L.qb_pivoted_qr.argtypes = [c_ctx, vp, P(vp), P(i64), P(vp), P(i64)]
         L.qb_fixed_rank.argtypes = [c_ctx, vp, i64, i64, i64, i64, ctypes.c_int, u64, ctypes.c_uint, P(vp), P(i64),
                                     P(vp), P(i64), P(dbl)]
         L.qb_kernel_launches.argtypes = [c_ctx]
@@ -87,7 +88,7 @@ def lib():
         L.qb_last_error.argtypes = [c_ctx]
         L.qb_last_error.restype = ctypes.c_char_p
         for f in ("qb_create", "qb_create_dist", "qb_create_dist_rows", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_gemm", "qb_chol_rinv", "qb_stats", "qb_omega",
-                  "qb_orth", "rqb_svd", "qb_fixed_rank"):
+                  "qb_orth", "rqb_svd", "qb_fixed_rank", "qb_pivoted_qr"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -216,6 +217,18 @@ def rqb_svd(ctx, kkeep=0):
     return dict(U=U.value or 0, ldu=ldu.value, S=S.value or 0, V=V.value or 0, ldv=ldv.value)
 
 
+def qb_pivoted_qr(ctx, n):
+    """QB -> partial pivoted QR of the context's last factorization (see include/qb.h).
+    Returns dict(perm (numpy int64, n), Qh, ldqh, R, ldr) with device pointers."""
+    import numpy as np
+    perm = np.empty(n, dtype=np.int64)
+    Qh, R = ctypes.c_void_p(), ctypes.c_void_p()
+    ldq, ldr = ctypes.c_int64(), ctypes.c_int64()
+    _check(ctx, lib().qb_pivoted_qr(ctx, ctypes.c_void_p(perm.ctypes.data), ctypes.byref(Qh), ctypes.byref(ldq),
+                                    ctypes.byref(R), ctypes.byref(ldr)))
+    return dict(perm=perm, Qh=Qh.value or 0, ldqh=ldq.value, R=R.value or 0, ldr=ldr.value)
+
+
 def qb_omega(ctx, seed, row0, row1, col0, w, out_ptr, ldo):
     _check(ctx, lib().qb_omega(ctx, seed, row0, row1, col0, w, ctypes.c_void_p(out_ptr), ldo))
 
@@ -326,6 +339,24 @@ class QB:
             Q, B = Q.clone(), B.clone()
         self._last = (m, n, l, A.dtype)
         return dict(Q=Q, B=B, resid=r["resid"])
+
+    def pivoted_qr(self, copy_out=True):
+        """A P ~ Qh R from the last ``factor`` / ``fixed_rank``: returns
+        dict(perm, Qh (m x k), R (k x n upper trapezoidal)); column j of A P is column perm[j] of A."""
+        import torch
+        if getattr(self, "_last", None) is None:
+            qb_pivoted_qr(self.ctx, 0)  # raises QBError: no factorization yet
+        m, n, k, dt = self._last
+        r = qb_pivoted_qr(self.ctx, n)
+        ts = "<f8" if dt == torch.float64 else "<f4"
+        if k == 0:
+            return dict(perm=r["perm"], Qh=torch.zeros(m, 0, dtype=dt, device="cuda"),
+                        R=torch.zeros(0, n, dtype=dt, device="cuda"))
+        Qh = view_colmajor(r["Qh"], m, k, r["ldqh"], ts)
+        R = view_rowmajor(r["R"], k, n, r["ldr"], ts)
+        if copy_out:
+            Qh, R = Qh.clone(), R.clone()
+        return dict(perm=r["perm"], Qh=Qh, R=R)
 
     def svd(self, kkeep=0, copy_out=True):
         """Partial SVD A ~ U diag(S) V^T from the last ``factor`` (rqb_svd):

@@ -27,6 +27,7 @@
 #include "gemm_f64.cuh"
 #include "gemm_tf32.cuh"
 #include "omega.cuh"
+#include "qrcp.cuh"
 #include "small.cuh"
 
 namespace {
@@ -169,6 +170,7 @@ struct qb_ctx_s {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy = nullptr;
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
+  DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32;     // qb_pivoted_qr
   cusolverDnHandle_t solver = nullptr;
   int block_fallbacks = 0;
   const double* outQ = nullptr;
@@ -909,7 +911,9 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->G,     &ctx->L,    &ctx->Rinv, &ctx->W,  &ctx->P,     &ctx->parts, &ctx->scal, &ctx->status,
                     &ctx->Qf,    &ctx->Bf,   &ctx->Astage, &ctx->Q32,  &ctx->B32, &ctx->Qbar32, &ctx->W32,
                     &ctx->QB,    &ctx->R,    &ctx->Usv,    &ctx->Vsv,  &ctx->Ssv, &ctx->Wsv,    &ctx->Ut,
-                    &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork};
+                    &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
+                    &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
+                    &ctx->Rq32,  &ctx->Qh32};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -1182,6 +1186,106 @@ qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_ou
   if (S_out) *S_out = Sp;
   if (V_out) *V_out = Vp;
   if (ldv_out) *ldv_out = ldn;
+  return QB_OK;
+}
+
+qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int64_t* ldqh_out, const void** R_out,
+                        int64_t* ldr_out) {
+  // QB -> partial pivoted QR: B P = Q~ R (Householder QR with column pivoting
+  // of the l x n factor B), Q^ = Q Q~, so that A P ~ Q^ R.  FP64 internally.
+  if (!ctx) return QB_ERR_INVALID_ARG;
+  if (ctx->last_k < 0) return fail(ctx, QB_ERR_INVALID_ARG, "qb_pivoted_qr: no factorization to convert");
+  if (ctx->nranks > 1 && !ctx->shard_rows)
+    return fail(ctx, QB_ERR_UNSUPPORTED, "qb_pivoted_qr: column-sharded B̄ (distributed) not supported");
+  const int64_t m = ctx->last_m, n = ctx->last_n, l = ctx->last_k;
+  QB_CUDA(cudaSetDevice(ctx->device));
+  if (l == 0) {
+    if (perm_out)
+      for (int64_t j = 0; j < n; ++j) perm_out[j] = j;
+    if (Qh_out) *Qh_out = nullptr;
+    if (R_out) *R_out = nullptr;
+    if (ldqh_out) *ldqh_out = round_up(m, 16);
+    if (ldr_out) *ldr_out = ctx->ldb;
+    return QB_OK;
+  }
+  const int64_t ldr = ctx->ldb, ldm = round_up(m, 16), ldqt = round_up(l, 16);
+  const int nchunks = (int)((l + QRCP_ROWS - 1) / QRCP_ROWS);
+  const int64_t ldp = round_up(n, 16);
+  QB_TRY(ensure(ctx, ctx->Rq, sizeof(double) * (size_t)(ldr * l)));
+  QB_TRY(ensure(ctx, ctx->Qt, sizeof(double) * (size_t)(ldqt * l)));
+  QB_TRY(ensure(ctx, ctx->Qh, sizeof(double) * (size_t)(ldm * l)));
+  QB_TRY(ensure(ctx, ctx->qvn1, sizeof(double) * (size_t)n));
+  QB_TRY(ensure(ctx, ctx->qvn2, sizeof(double) * (size_t)n));
+  QB_TRY(ensure(ctx, ctx->qperm, sizeof(int) * (size_t)n));
+  QB_TRY(ensure(ctx, ctx->qtau, sizeof(double) * (size_t)l));
+  QB_TRY(ensure(ctx, ctx->qv, sizeof(double) * (size_t)l));
+  QB_TRY(ensure(ctx, ctx->qparts, sizeof(double) * (size_t)(nchunks * ldp)));
+  double* R = ctx->Rq.d();
+  QB_CUDA(cudaMemcpyAsync(R, ctx->Bbar.p, sizeof(double) * (size_t)(ldr * l), cudaMemcpyDeviceToDevice, ctx->stream));
+  double* vn1 = ctx->qvn1.d();
+  double* vn2 = ctx->qvn2.d();
+  int* perm = static_cast<int*>(ctx->qperm.p);
+  double* tau = ctx->qtau.d();
+  double* vb = ctx->qv.d();
+  double* parts = ctx->qparts.d();
+  const double tol3z = std::sqrt(0x1p-52);
+  qrcp_init_kernel<<<(int)((n + QRCP_THREADS - 1) / QRCP_THREADS), QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l,
+                                                                                                 (int)n, vn1, vn2, perm);
+  QB_TRY(check_launch(ctx, "qrcp_init"));
+  for (int i = 0; i < (int)l; ++i) {
+    qrcp_pivot_kernel<<<1, 1024, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2, perm, tau, vb);
+    QB_TRY(check_launch(ctx, "qrcp_pivot"));
+    if (i + 1 >= n) continue;
+    const int ncol = (int)(n - i - 1);
+    const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
+    dim3 grid((unsigned)((ncol + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
+    qrcp_w_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vb, parts, ldp);
+    QB_TRY(check_launch(ctx, "qrcp_w"));
+    qrcp_update_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vb, tau, parts, ldp, rch,
+                                                               vn1, vn2, tol3z);
+    QB_TRY(check_launch(ctx, "qrcp_update"));
+    qrcp_renorm_kernel<<<grid.x, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2);
+    QB_TRY(check_launch(ctx, "qrcp_renorm"));
+  }
+  // Q~ = H_0 ... H_{l-1} (backward accumulation on the identity), then Q^ = Q̄ Q~
+  double* Qt = ctx->Qt.d();
+  qrcp_identity_kernel<<<(int)std::min<int64_t>((l * l + 255) / 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
+      Qt, ldqt, (int)l);
+  QB_TRY(check_launch(ctx, "qrcp_identity"));
+  for (int i = (int)l - 1; i >= 0; --i) {
+    const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
+    dim3 grid((unsigned)((l + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
+    qrcp_q_w_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, parts, ldp);
+    QB_TRY(check_launch(ctx, "qrcp_q_w"));
+    qrcp_q_update_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, tau, parts, ldp, rch);
+    QB_TRY(check_launch(ctx, "qrcp_q_update"));
+  }
+  qrcp_zero_lower_kernel<<<(int)std::min<int64_t>((l * l + 255) / 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
+      R, ldr, (int)l);
+  QB_TRY(check_launch(ctx, "qrcp_zero_lower"));
+  QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)(16 * ctx->num_sms)));
+  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)l, (int)l, ctx->Qbar.d(), ctx->ldq, Qt, ldqt, ctx->Qh.d(), ldm,
+              false, nullptr));
+  std::vector<int> hperm((size_t)n);
+  QB_CUDA(cudaMemcpyAsync(hperm.data(), perm, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (perm_out)
+    for (int64_t j = 0; j < n; ++j) perm_out[j] = hperm[(size_t)j];
+  const void* Qp = ctx->Qh.p;
+  const void* Rp = R;
+  if (ctx->dtype == QB_F32) {
+    QB_TRY(ensure(ctx, ctx->Qh32, sizeof(float) * (size_t)(ldm * l)));
+    QB_TRY(ensure(ctx, ctx->Rq32, sizeof(float) * (size_t)(ldr * l)));
+    QB_TRY(launch_convert(ctx, ctx->Qh.d(), ldm, m, l, static_cast<float*>(ctx->Qh32.p), ldm));
+    QB_TRY(launch_convert(ctx, static_cast<const double*>(R), ldr, n, l, static_cast<float*>(ctx->Rq32.p), ldr));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    Qp = ctx->Qh32.p;
+    Rp = ctx->Rq32.p;
+  }
+  if (Qh_out) *Qh_out = Qp;
+  if (ldqh_out) *ldqh_out = ldm;
+  if (R_out) *R_out = Rp;
+  if (ldr_out) *ldr_out = ldr;
   return QB_OK;
 }
 
