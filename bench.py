@@ -331,6 +331,27 @@ def run_ours(args, cfg):
                "entry_point": "qb_factor_host (pinned host A, Q, B; every rank its shard)"}
         del A_h, Q_h, B_h
 
+    # the NEXT rows timed once each after the main measurement (warm, CUDA events, not in `value`):
+    # QB -> SVD (rqb_svd) and QB -> pivoted QR (qb_pivoted_qr) of the last factorization, and the
+    # fixed-rank randQB at l = k (one wide GEMM per product instead of s narrow ones)
+    post = None
+    if ws == 1 and not args.no_post:
+        post = {}
+        for name, fn in (("rqb_svd", lambda: ctx.svd(copy_out=False)),
+                         ("pivoted_qr", lambda: ctx.pivoted_qr(copy_out=False)),
+                         ("fixed_rank_randQB_l_eq_k", lambda: ctx.fixed_rank(A0, k, 0, seed=cfg.seed_omega,
+                                                                            want_resid=False, copy_out=False))):
+            fn()  # warm (svd and pivoted QR read the last factorization; fixed_rank runs last)
+            torch.cuda.synchronize()
+            p0 = torch.cuda.Event(enable_timing=True)
+            p1 = torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            fn()
+            p1.record(stream)
+            torch.cuda.synchronize()
+            post[name + "_ms"] = p0.elapsed_time(p1)
+        post["k"] = k
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         A_np = np.asfortranarray(A0.cpu().numpy())
@@ -357,7 +378,7 @@ def run_ours(args, cfg):
                 "seconds_to_eps": ms * 1e-3,
                 "frac_fp64_peak": None if f32 else value / ws / (peak * 1e3),
                 "frac_cublas_dgemm": (value / ws / (cublas * 1e3)) if (cublas and not f32) else None,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "post": post,
                 "clocks": clk}
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -381,6 +402,7 @@ def main():
     ap.add_argument("--cpu-sample-blocks", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-post", action="store_true", help="skip timing rqb_svd / pivoted QR / fixed-rank")
     ap.add_argument("--strong", action="store_true", help="N > 1: shard one matrix (strong scaling)")
     ap.add_argument("--shard", default="auto", choices=["auto", "cols", "rows"],
                     help="N > 1: shard columns (square A) or rows (tall-skinny A, NEXT-2); auto picks rows "

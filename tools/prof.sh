@@ -1,9 +1,9 @@
 # ncu evidence for one round: launch list of the bench command + full sections of the 3 big GEMMs.
 # usage (on the GPU box): bash tools/prof.sh r01
 R=${1:-r01}
-python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_$R.log 2>&1 && \
+python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-post > gpurun_out/plain_$R.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv \
-    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_$R.log 2>&1
+    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-post > gpurun_out/ncu_launch_$R.log 2>&1
 echo launches_rc=$?
 PYTHONPATH=. python tools/quick_run.py T 1 > gpurun_out/plain2_$R.log 2>&1 && \
 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
