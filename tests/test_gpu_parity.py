@@ -313,9 +313,11 @@ def test_row_sharded_context_single_rank(qbmod, q, dt):
 
 
 @pytest.mark.parametrize("case", [(400, 300, "exp10_20", 1e-4, 10, 0), (3000, 200, "exp_100", 1e-3, 32, 0),
-                                  (1000, 260, "poly2", 1e-4, 64, 1)])
+                                  (1000, 260, "poly2", 1e-4, 64, 1), (5000, 700, "exp_100", 1e-3, 100, 0),
+                                  (2000, 1500, "exp_150", 1e-3, 256, 0), (3000, 500, "exp_100", 1e-3, 96, 2)])
 def test_fp32_path_parity(qbmod, case):
-    """FP32 path (BASELINE configs[3] family): float A in, float Q, B out.  The oracle runs in
+    """FP32 path (BASELINE configs[3] family): float A in, float Q, B out, ragged block widths
+    (b = 10, 96, 100) and b = 256 through the 3xTF32 GEMMs, q = 0..2.  The oracle runs in
     FP64 on the same FP32 input with Ω = RN_32(Ω) (reading R18); north_star FP32 tolerances
     1e-5 (orthogonality) and 1e-4 (QB parity)."""
     m, n, kind, eps, b, q = case
