@@ -340,37 +340,50 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
           if (p == 0) CHOL_TS(3);
           int bad = 0;
           double rdiag = 1.0;  // 1 / L(lane, lane)
+          // pivot j: lane j checks its pivot against tol * G_jj; the column is scaled by 1/sqrt(d)
+          auto pivot = [&](int j) -> double {
+            const double d = __shfl_sync(0xffffffffu, a[j], j);
+            if (lane == j && j < nb && (!(d > tol * gdiag) || !(d > 0.0))) bad = 1;
+            const double ri = rsqrt(d);
+            const double l = lane > j ? a[j] * ri : (lane == j ? d * ri : 0.0);
+            if (lane == j) rdiag = ri;
+            a[j] = l;
+            return l;
+          };
+          // right-looking with a one-column lookahead: column jj+1 gets pivot jj's update first and
+          // pivot jj+1 is formed before the rest of pivot jj's updates, so the dependent
+          // pivot chain overlaps the independent column updates
+          double l = pivot(0);
 #pragma unroll
           for (int jj = 0; jj < CHOL_NB; ++jj) {
-            const double d = __shfl_sync(0xffffffffu, a[jj], jj);
-            const double gj = __shfl_sync(0xffffffffu, gdiag, jj);
-            if (jj < nb && (!(d > tol * gj) || !(d > 0.0))) bad = 1;
-            const double ri = rsqrt(d);
-            const double l = lane > jj ? a[jj] * ri : (lane == jj ? d * ri : 0.0);
-            if (lane == jj) rdiag = ri;
-            a[jj] = l;
+            double lnext = 0.0;
+            if (jj + 1 < CHOL_NB) {
+              const double lc = __shfl_sync(0xffffffffu, l, jj + 1);
+              if (lane >= jj + 1) a[jj + 1] = fma(-l, lc, a[jj + 1]);
+              lnext = pivot(jj + 1);
+            }
 #pragma unroll
             for (int c = 0; c < CHOL_NB; ++c) {  // fixed bounds: a[] stays in registers
-              if (c > jj) {
+              if (c > jj + 1) {
                 const double lc = __shfl_sync(0xffffffffu, l, c);
                 if (lane >= c) a[c] = fma(-l, lc, a[c]);
               }
             }
+            l = lnext;
           }
+          bad = __any_sync(0xffffffffu, bad);
           if (p == 0) CHOL_TS(4);
-          // L11^-1, column `lane`: forward substitution with L(r, k) broadcast from lane r
+          // L11^-1, column `lane`, right-looking: x_r = v_r / L(r, r), then v_r2 -= L(r2, r) x_r for
+          // r2 > r (L(r2, r) broadcast from lane r2); the dependent chain is two operations per row
           double x[CHOL_NB];
 #pragma unroll
-          for (int r = 0; r < CHOL_NB; ++r) {
-            double v0 = (r == lane) ? 1.0 : 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+          for (int r = 0; r < CHOL_NB; ++r) x[r] = (r == lane) ? 1.0 : 0.0;
 #pragma unroll
-            for (int k = 0; k < CHOL_NB; k += 4) {
-              if (k < r) v0 = fma(-__shfl_sync(0xffffffffu, a[k], r), x[k], v0);
-              if (k + 1 < r) v1 = fma(-__shfl_sync(0xffffffffu, a[k + 1], r), x[k + 1], v1);
-              if (k + 2 < r) v2 = fma(-__shfl_sync(0xffffffffu, a[k + 2], r), x[k + 2], v2);
-              if (k + 3 < r) v3 = fma(-__shfl_sync(0xffffffffu, a[k + 3], r), x[k + 3], v3);
-            }
-            x[r] = ((v0 + v1) + (v2 + v3)) * __shfl_sync(0xffffffffu, rdiag, r);
+          for (int r = 0; r < CHOL_NB; ++r) {
+            x[r] *= __shfl_sync(0xffffffffu, rdiag, r);
+#pragma unroll
+            for (int r2 = 0; r2 < CHOL_NB; ++r2)
+              if (r2 > r) x[r2] = fma(-__shfl_sync(0xffffffffu, a[r], r2), x[r], x[r2]);
           }
           if (p == 0) CHOL_TS(5);
 #pragma unroll
