@@ -21,7 +21,7 @@
  *     context takes float A and returns float Q, B: the residual A^(i) is kept in FP32 and its
  *     products run on the tensor cores as 3xTF32 with FP32 accumulation (reading R18b), with
  *     Omega = RN32(Omega); orth, re-projection and all norms are FP64.  Its
- *     results meet FP32 tolerances.  qb_orth is FP64-only.
+ *     results meet FP32 tolerances.
  *   - "device" pointers are CUDA device pointers on the context's device; the caller owns
  *     everything it passes in; the context owns everything it hands out.
  *   - Column-major means element (i, j) at ptr[i + j*ld]; row-major means ptr[i*ld + j].
@@ -169,9 +169,10 @@ qb_status qb_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_
                    int64_t w, void* out, int64_t ldo);
 
 /* orth(X) by CholeskyQR2 with the shifted-CholeskyQR3 fallback (R8): X is
- * device, column-major m x w (ldx), overwritten by Q with orthonormal columns spanning
- * ran(X); diag(R) > 0.  w <= 256.  Returns QB_ERR_ORTH_BREAKDOWN if even the shifted
- * variant fails.  Blocking.                                                               */
+ * device, column-major m x w (ldx), in the context's dtype, overwritten by Q with orthonormal
+ * columns spanning ran(X); diag(R) > 0.  w <= 256.  FP32 contexts orthonormalise the exactly
+ * widened panel in FP64 and round the result.  Returns QB_ERR_ORTH_BREAKDOWN if even the
+ * shifted variant fails.  Blocking.                                                       */
 qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx);
 
 /* Test hook: one product with the library's FP64 GEMM (the kernel behind every contraction of

@@ -3,8 +3,11 @@
 //
 // One context owns a CUDA stream, the residual workspace, Q̄ / B̄ and all scratch.  The
 // block loop below is the paper's loop; every arithmetic step runs in this library's
-// kernels (omega.cuh, gemm_f64.cuh, small.cuh).  The host only sequences launches and
-// reads two scalars per block (the stop test) plus the CholeskyQR status words.
+// kernels (omega.cuh; gemm_f64.cuh for FP64 and gemm_tf32.cuh for the FP32 residual's products;
+// small.cuh for CholeskyQR and reductions; qrcp.cuh for QB -> pivoted QR).  The host only
+// sequences launches and reads two scalars per block (the stop test) plus the CholeskyQR status
+// words.  The post-processing entry points (rqb_svd, qb_pivoted_qr) and the fixed-rank schemes
+// (qb_fixed_rank) reuse the same kernels; the k x k SVD core of rqb_svd is cuSOLVER (dlopen).
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
@@ -953,7 +956,6 @@ qb_status qb_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, int64_
 
 qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
   if (!ctx) return QB_ERR_INVALID_ARG;
-  if (ctx->dtype != QB_F64) return fail(ctx, QB_ERR_UNSUPPORTED, "qb_orth: FP32 not built yet");
   if (!X || m < 1 || w < 1 || w > kMaxB || w > m || ldx < m || m > INT32_MAX)
     return fail(ctx, QB_ERR_INVALID_ARG, "qb_orth: bad arguments (m=%lld w=%lld ldx=%lld)", (long long)m,
                 (long long)w, (long long)ldx);
@@ -965,7 +967,13 @@ qb_status qb_orth(qb_ctx ctx, void* X, int64_t m, int64_t w, int64_t ldx) {
   QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(m, 16) * kMaxB)));
   QB_TRY(reset_flags(ctx));
   const bool aligned = (ldx % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-  if (aligned) {
+  if (ctx->dtype == QB_F32) {  // FP32 panel: CholeskyQR2 in FP64 on the exactly widened copy
+    const int64_t ldy = round_up(m, 16);
+    QB_TRY(ensure(ctx, ctx->Y, sizeof(double) * (size_t)(ldy * w)));
+    QB_TRY(launch_convert(ctx, static_cast<const float*>(X), ldx, m, w, ctx->Y.d(), ldy));
+    QB_TRY(cholqr2(ctx, ctx->Y.d(), ldy, ctx->Y.d(), ldy, m, (int)w));
+    QB_TRY(launch_convert(ctx, static_cast<const double*>(ctx->Y.d()), ldy, m, w, static_cast<float*>(X), ldx));
+  } else if (aligned) {
     QB_TRY(cholqr2(ctx, static_cast<double*>(X), ldx, static_cast<double*>(X), ldx, m, (int)w));
   } else {  // TMA needs 16-byte aligned columns: stage through an aligned copy
     const int64_t ldy = round_up(m, 16);

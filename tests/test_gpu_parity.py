@@ -371,3 +371,16 @@ def test_factor_host_entry_point(qbmod, dt):
         assert np.array_equal(Bh[:kc], g["B"][:kc].cpu().numpy())
         assert np.isnan(Qh[kc:]).all() and np.isnan(Bh[kc:]).all()
     c.close()
+
+
+def test_orth_fp32_context(qbmod):
+    """qb_orth on an FP32 context: FP64 CholeskyQR2 of the widened panel, rounded to FP32."""
+    X = np.random.default_rng(4).standard_normal((3000, 100)).astype(np.float32)
+    Xd = torch.from_numpy(np.asfortranarray(X)).cuda()
+    c = qbmod.QB(0, dtype=qbmod.QB_F32)
+    qbmod.qb_orth(c.ctx, Xd.data_ptr(), 3000, 100, 3000)
+    c.close()
+    Q = Xd.double().cpu().numpy()
+    Qo = oqb.orth(X.astype(np.float64))
+    assert np.abs(Q.T @ Q - np.eye(100)).max() <= 1e-6
+    assert np.abs(Q - Qo).max() <= 1e-6
