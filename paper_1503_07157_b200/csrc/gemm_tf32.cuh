@@ -67,17 +67,22 @@ struct TfParams {
   int a3d, b3d;       // NN: one 3D TMA per operand per stage ({32, K, rows/32} view)
 };
 
-template <int BN, bool SUB = false>
+// TS = true: the A operand goes to TMEM (hi and lo, 64 columns per stage, written by the
+// splitters with tcgen05.st), so a stage's shared memory is [A raw][B_hi][B_lo] and more stages fit.
+template <int BN, bool SUB = false, bool TS = false>
 struct TfCfg {
   static constexpr int THREADS = TF_THREADS;
   static constexpr int A_BYTES = TF_BM * TF_BK * 4;
   static constexpr int B_BYTES = BN * TF_BK * 4;
-  static constexpr int HI_BYTES = A_BYTES + B_BYTES;   // [A_hi][B_hi], then [A_lo][B_lo]
-  static constexpr int STAGE_BYTES = 2 * HI_BYTES;
+  static constexpr int HI_BYTES = A_BYTES + B_BYTES;   // SS: [A_hi][B_hi], then [A_lo][B_lo]
+  static constexpr int STAGE_BYTES = TS ? A_BYTES + 2 * B_BYTES : 2 * HI_BYTES;
   static constexpr int CSUB_BYTES = TF_BM * TF_CSUB * 4;
   static constexpr int C_BYTES = SUB ? TF_CSLOTS * CSUB_BYTES : 0;
-  static constexpr int STAGES = (224 * 1024 - C_BYTES) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers (chunk c in buffer c & 1)
+  static constexpr int SMEM_STAGES = (224 * 1024 - C_BYTES) / STAGE_BYTES;
+  static constexpr int TMEM_A_STAGES = (512 - 2 * BN) / 64;
+  static constexpr int STAGES = TS ? (SMEM_STAGES < TMEM_A_STAGES ? SMEM_STAGES : TMEM_A_STAGES) : SMEM_STAGES;
+  static constexpr int A_TMEM_COL = 2 * BN;  // TS: stage s holds A_hi at A_TMEM_COL + 64 s, A_lo 32 further
+  static constexpr int TMEM_COLS = TS ? 512 : 2 * BN;  // two accumulator buffers (chunk c in buffer c & 1)
   static constexpr int SMEM_BYTES =
       1024 + STAGES * STAGE_BYTES + C_BYTES + (3 * STAGES + 4 + 2 * TF_CSLOTS) * 8 + 64;
   static_assert(STAGES >= 2, "at least double buffering");
@@ -166,6 +171,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
                : "memory");
 }
 
+// 32 consecutive TMEM columns of this thread's lane <- r (tcgen05.st 32x32b.x32)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] B[smem] (A K-major in TMEM: row = lane, one K element per column)
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void pin8(float (&t)[8]) {
   asm volatile("" : "+f"(t[0]), "+f"(t[1]), "+f"(t[2]), "+f"(t[3]), "+f"(t[4]), "+f"(t[5]), "+f"(t[6]), "+f"(t[7]));
 }
@@ -179,7 +207,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
 template <int LAYOUT, int BN>
 __device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, uint8_t* sA, uint8_t* sB,
                                                uint64_t* bar, int m0, int n0, int k0, int a3d, int b3d) {
-  using Cfg = TfCfg<BN>;  // operand stage sizes do not depend on the epilogue
+  using Cfg = TfCfg<BN>;  // raw operand bytes do not depend on the epilogue or on TS
   mbar_arrive_expect_tx(bar, Cfg::HI_BYTES);
   if (LAYOUT == 0) {  // NN: MN-major chunks of 32 rows x 32 k
     if (a3d) {
@@ -200,12 +228,12 @@ __device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUte
   }
 }
 
-template <int LAYOUT, int BN, int EPI>
+template <int LAYOUT, int BN, int EPI, bool TS>
 __global__ void __launch_bounds__(TF_THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      const __grid_constant__ CUtensorMap tC, const TfParams p) {
   constexpr bool SUB = EPI == TF_SUB_COL;
-  using Cfg = TfCfg<BN, SUB>;
+  using Cfg = TfCfg<BN, SUB, TS>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -292,17 +320,33 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           }
           mbar_wait(&conv[slot], (j / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES);
-          const uint32_t b_hi = a_hi + Cfg::A_BYTES;
-          const uint64_t dAh = umma_desc(a_hi, LBO, SBO, LT), dBh = umma_desc(b_hi, LBO, SBO, LT);
-          const uint64_t dAl = umma_desc(a_hi + Cfg::HI_BYTES, LBO, SBO, LT);
-          const uint64_t dBl = umma_desc(b_hi + Cfg::HI_BYTES, LBO, SBO, LT);
+          if (TS) {
+            // A (hi, lo) in TMEM, K-major; B (hi, lo) in shared memory after the raw A
+            constexpr uint32_t idesc_ts = tf32_idesc<BN>(0, LAYOUT == 0 ? 1 : 0);
+            const uint32_t b_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES) + Cfg::A_BYTES;
+            const uint64_t dBh = umma_desc(b_hi, LBO, SBO, LT), dBl = umma_desc(b_hi + Cfg::B_BYTES, LBO, SBO, LT);
+            const uint32_t ta = tmem_base + static_cast<uint32_t>(Cfg::A_TMEM_COL + 64 * slot);
 #pragma unroll
-          for (int kk = 0; kk < TF_BK / 8; ++kk) {
-            const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
-            umma_tf32(tacc, dAh + adv, dBh + adv, idesc, (!first || kk > 0) ? 1u : 0u);
-            umma_tf32(tacc, dAh + adv, dBl + adv, idesc, 1u);
-            umma_tf32(tacc, dAl + adv, dBh + adv, idesc, 1u);
+            for (int kk = 0; kk < TF_BK / 8; ++kk) {
+              const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
+              const uint32_t tah = ta + 8 * kk, tal = ta + 32 + 8 * kk;
+              umma_tf32_ts(tacc, tah, dBh + adv, idesc_ts, (!first || kk > 0) ? 1u : 0u);
+              umma_tf32_ts(tacc, tah, dBl + adv, idesc_ts, 1u);
+              umma_tf32_ts(tacc, tal, dBh + adv, idesc_ts, 1u);
+            }
+          } else {
+            const uint32_t a_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES);
+            const uint32_t b_hi = a_hi + Cfg::A_BYTES;
+            const uint64_t dAh = umma_desc(a_hi, LBO, SBO, LT), dBh = umma_desc(b_hi, LBO, SBO, LT);
+            const uint64_t dAl = umma_desc(a_hi + Cfg::HI_BYTES, LBO, SBO, LT);
+            const uint64_t dBl = umma_desc(b_hi + Cfg::HI_BYTES, LBO, SBO, LT);
+#pragma unroll
+            for (int kk = 0; kk < TF_BK / 8; ++kk) {
+              const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
+              umma_tf32(tacc, dAh + adv, dBh + adv, idesc, (!first || kk > 0) ? 1u : 0u);
+              umma_tf32(tacc, dAh + adv, dBl + adv, idesc, 1u);
+              umma_tf32(tacc, dAl + adv, dBh + adv, idesc, 1u);
+            }
           }
           umma_commit(&empty[slot]);
           if ((kt % TF_PROMO) == TF_PROMO - 1 || kt == nk - 1) {
@@ -322,24 +366,66 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
         const int slot = j % STAGES;
         mbar_wait(&full[slot], (j / STAGES) & 1);
         uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
+        if (TS) {
+          // A row r of the tile (TMEM lane r, this warp's quadrant): read its 32 k from the swizzled
+          // raw stage, split, store hi / lo to the stage's TMEM columns
+          const int quad = warp & 3, r = quad * 32 + lane;
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int k = 0; k < TF_BK; ++k) {
+            const uint32_t off = LAYOUT == 0
+                                     ? (r >> 5) * 4096 + k * 128 + ((((r & 31) >> 3) ^ (k & 3)) << 5) + ((r & 7) << 2)
+                                     : r * 128 + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2);
+            const float x = *reinterpret_cast<const float*>(st + off);
+            const float h = tf32_rna(x);
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(x - h);
+          }
+          const uint32_t ta = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                              static_cast<uint32_t>(Cfg::A_TMEM_COL + 64 * slot);
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          // B: hi in place, lo after it
+          uint8_t* sb = st + Cfg::A_BYTES;
 #pragma unroll 4
-        for (int i = t; i < Cfg::HI_BYTES / 16; i += 128) {
-          float4* hp = reinterpret_cast<float4*>(st + i * 16);
-          const float4 v = *hp;
-          float4 h, l;
-          h.x = tf32_rna(v.x);
-          h.y = tf32_rna(v.y);
-          h.z = tf32_rna(v.z);
-          h.w = tf32_rna(v.w);
-          l.x = v.x - h.x;
-          l.y = v.y - h.y;
-          l.z = v.z - h.z;
-          l.w = v.w - h.w;
-          *hp = h;
-          *reinterpret_cast<float4*>(st + Cfg::HI_BYTES + i * 16) = l;
+          for (int i = t; i < Cfg::B_BYTES / 16; i += 128) {
+            float4* hp = reinterpret_cast<float4*>(sb + i * 16);
+            const float4 v = *hp;
+            float4 h, l;
+            h.x = tf32_rna(v.x);
+            h.y = tf32_rna(v.y);
+            h.z = tf32_rna(v.z);
+            h.w = tf32_rna(v.w);
+            l.x = v.x - h.x;
+            l.y = v.y - h.y;
+            l.z = v.z - h.z;
+            l.w = v.w - h.w;
+            *hp = h;
+            *reinterpret_cast<float4*>(sb + Cfg::B_BYTES + i * 16) = l;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        } else {
+#pragma unroll 4
+          for (int i = t; i < Cfg::HI_BYTES / 16; i += 128) {
+            float4* hp = reinterpret_cast<float4*>(st + i * 16);
+            const float4 v = *hp;
+            float4 h, l;
+            h.x = tf32_rna(v.x);
+            h.y = tf32_rna(v.y);
+            h.z = tf32_rna(v.z);
+            h.w = tf32_rna(v.w);
+            l.x = v.x - h.x;
+            l.y = v.y - h.y;
+            l.z = v.z - h.z;
+            l.w = v.w - h.w;
+            *hp = h;
+            *reinterpret_cast<float4*>(st + Cfg::HI_BYTES + i * 16) = l;
+          }
+          // generic-proxy writes -> visible to the tensor core (async proxy) before the MMA reads
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        // generic-proxy writes -> visible to the tensor core (async proxy) before the MMA reads
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[slot]);
       }
     }

@@ -473,11 +473,11 @@ qb_status make_map3d_f32(qb_ctx ctx, CUtensorMap* map, const float* ptr, uint64_
   return QB_OK;
 }
 
-template <int LAYOUT, int BN, int EPI>
-qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                      const TfParams& p, int splits) {
-  using Cfg = TfCfg<BN, EPI == TF_SUB_COL>;
-  auto kern = gemm_tf32_kernel<LAYOUT, BN, EPI>;
+template <int LAYOUT, int BN, int EPI, bool TS>
+qb_status launch_tf_ts(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                       const TfParams& p, int splits) {
+  using Cfg = TfCfg<BN, EPI == TF_SUB_COL, TS>;
+  auto kern = gemm_tf32_kernel<LAYOUT, BN, EPI, TS>;
   static bool attr_done = false;
   if (!attr_done) {
     QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -486,6 +486,15 @@ qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, 
   const int units = p.tiles_m * p.tiles_n * splits;
   kern<<<std::min(units, ctx->num_sms), Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tc, p);
   return check_launch(ctx, "gemm_tf32");
+}
+
+// A operand in TMEM (TS, more pipeline stages) unless QB_TF_SS=1 (both operands in shared memory)
+template <int LAYOUT, int BN, int EPI>
+qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                      const TfParams& p, int splits) {
+  static const int ss = debug_env("QB_TF_SS");
+  if (ss) return launch_tf_ts<LAYOUT, BN, EPI, false>(ctx, ta, tb, tc, p, splits);
+  return launch_tf_ts<LAYOUT, BN, EPI, true>(ctx, ta, tb, tc, p, splits);
 }
 
 template <int BN>
