@@ -245,6 +245,30 @@ def test_target_config_properties(qbmod, ctx):
         assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
 
 
+def test_c4_config_properties_fp32(qbmod):
+    """BASELINE configs[3] (C4: 200000 x 2000 FP32, b = 128) at full size on the FP32 tensor-core
+    path: properties that hold at any size, at the north_star's FP32 tolerances."""
+    cfg = synth.CONFIGS["C4"]
+    sig = synth.config_sigma(cfg)
+    A32 = synth.make_matrix_torch(cfg.m, cfg.n, sig, cfg.seed_matrix, dtype=torch.float32)
+    c = qbmod.QB(0, dtype=qbmod.QB_F32)
+    g = c.factor(A32, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=True)
+    c.close()
+    k = g["k"]
+    assert g["status"] == 0 and k % cfg.b == 0 and k >= synth.eps_rank(sig, cfg.eps)
+    Q, B = g["Q"].double(), g["B"].double()
+    A = A32.double()
+    nA = float(torch.linalg.norm(A))
+    orth = (Q.T @ Q - torch.eye(k, dtype=torch.float64, device="cuda")).abs().max().item()
+    assert orth <= 1e-5
+    true = torch.linalg.norm(torch.addmm(A, Q, B, alpha=-1.0)).item()
+    assert true <= cfg.eps * (1 + 1e-4) + 1e-6 * nA
+    assert abs(g["resid"] - true) <= 1e-6 * nA
+    assert true >= synth.optimal_error(sig, k) * (1 - 1e-3)
+    st = g["stats"]
+    assert st[-1]["r2"] <= cfg.eps ** 2 < st[-2]["r2"]
+
+
 def test_fresh_context_reproducible_across_growth(qbmod):
     """k > 1024 forces the Q̄/B̄ capacity to grow inside the first call; a fresh context and a
     reused one must give bitwise identical factors (fixed-order reductions)."""
