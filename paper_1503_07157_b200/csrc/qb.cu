@@ -173,7 +173,7 @@ struct qb_ctx_s {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy = nullptr;
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
-  DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32;     // qb_pivoted_qr
+  DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw;  // qb_pivoted_qr
   cusolverDnHandle_t solver = nullptr;
   int block_fallbacks = 0;
   const double* outQ = nullptr;
@@ -925,7 +925,7 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->QB,    &ctx->R,    &ctx->Usv,    &ctx->Vsv,  &ctx->Ssv, &ctx->Wsv,    &ctx->Ut,
                     &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
-                    &ctx->Rq32,  &ctx->Qh32};
+                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -1249,20 +1249,46 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
   qrcp_init_kernel<<<(int)((n + QRCP_THREADS - 1) / QRCP_THREADS), QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l,
                                                                                                  (int)n, vn1, vn2, perm);
   QB_TRY(check_launch(ctx, "qrcp_init"));
-  for (int i = 0; i < (int)l; ++i) {
-    qrcp_pivot_kernel<<<1, 1024, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2, perm, tau, vb);
-    QB_TRY(check_launch(ctx, "qrcp_pivot"));
-    if (i + 1 >= n) continue;
-    const int ncol = (int)(n - i - 1);
-    const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
-    dim3 grid((unsigned)((ncol + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
-    qrcp_w_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vb, parts, ldp);
-    QB_TRY(check_launch(ctx, "qrcp_w"));
-    qrcp_update_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vb, tau, parts, ldp, rch,
-                                                               vn1, vn2, tol3z);
-    QB_TRY(check_launch(ctx, "qrcp_update"));
-    qrcp_renorm_kernel<<<grid.x, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2);
-    QB_TRY(check_launch(ctx, "qrcp_renorm"));
+  static const int unfused = debug_env("QB_QRCP_UNFUSED");
+  if (unfused) {  // reference schedule: reflector, w, rank-1 update, renorm per step
+    for (int i = 0; i < (int)l; ++i) {
+      qrcp_pivot_kernel<<<1, 1024, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2, perm, tau, vb);
+      QB_TRY(check_launch(ctx, "qrcp_pivot"));
+      if (i + 1 >= n) continue;
+      const int ncol = (int)(n - i - 1);
+      const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
+      dim3 grid((unsigned)((ncol + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
+      qrcp_w_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vb, parts, ldp);
+      QB_TRY(check_launch(ctx, "qrcp_w"));
+      qrcp_update_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vb, tau, parts, ldp, rch,
+                                                                 vn1, vn2, tol3z);
+      QB_TRY(check_launch(ctx, "qrcp_update"));
+      qrcp_renorm_kernel<<<grid.x, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2);
+      QB_TRY(check_launch(ctx, "qrcp_renorm"));
+    }
+  } else {  // one-step lookahead: the trailing block is read and written once per step
+    QB_TRY(ensure(ctx, ctx->qw, sizeof(double) * (size_t)(n + 2 * l + 64)));
+    double* wprev = ctx->qw.d();
+    double* vbs[2] = {vb, wprev + n};  // v_i alternates between two buffers (v_{i-1} still needed)
+    QB_CUDA(cudaMemsetAsync(wprev, 0, sizeof(double) * (size_t)n, ctx->stream));
+    for (int i = 0; i < (int)l; ++i) {
+      double* vcur = vbs[i & 1];
+      const double* vprev = vbs[(i + 1) & 1];
+      qrcp_la_pivot_kernel<<<1, 1024, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2, perm, tau, vprev, wprev,
+                                                         vcur);
+      QB_TRY(check_launch(ctx, "qrcp_la_pivot"));
+      if (i + 1 >= n) continue;
+      const int ncol = (int)(n - i - 1);
+      const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
+      dim3 grid((unsigned)((ncol + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
+      qrcp_la_fw_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, tau, vprev, wprev, vcur,
+                                                                parts, ldp);
+      QB_TRY(check_launch(ctx, "qrcp_la_fw"));
+      qrcp_la_row_kernel<<<grid.x, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, tau, vcur, parts, ldp,
+                                                                   rch, wprev, vn1, vn2, tol3z);
+      QB_TRY(check_launch(ctx, "qrcp_la_row"));
+    }
+    // the last deferred update reaches rows below l only: nothing left to apply
   }
   // Q~ = H_0 ... H_{l-1} (backward accumulation on the identity), then Q^ = Q̄ Q~
   double* Qt = ctx->Qt.d();
@@ -1271,7 +1297,7 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
   QB_TRY(check_launch(ctx, "qrcp_identity"));
   for (int i = (int)l - 1; i >= 0; --i) {
     const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
-    dim3 grid((unsigned)((l + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
+    dim3 grid((unsigned)((l - i + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
     qrcp_q_w_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, parts, ldp);
     QB_TRY(check_launch(ctx, "qrcp_q_w"));
     qrcp_q_update_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, tau, parts, ldp, rch);

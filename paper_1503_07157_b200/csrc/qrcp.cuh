@@ -6,8 +6,11 @@
 // maps B(i:l, i) to (beta, 0, ..), beta = -sign(alpha) ||x||; the trailing columns get
 // B(i:l, j) -= tau v (v^T B(i:l, j)); the partial norms are downdated with R(i, j) and
 // recomputed from scratch when cancellation makes the downdate inaccurate (sqrt(eps) test).
-// Row-major B makes the two heavy passes (w = B(i:l, :)^T v and the rank-1 update) coalesced
-// over columns; both are fixed-order (per-row-chunk partials summed in chunk order).
+// Row-major B makes the heavy pass coalesced over columns.  The rank-1 update of step i is
+// deferred (one-step lookahead): the next step's fused pass applies it while it forms
+// w_{i+1} = B(i+1:l, :)^T v_{i+1}, so every step reads and writes the trailing block once; row i
+// (for the norm downdate) and the two swapped columns get the update first.  Reductions are
+// fixed-order (per-row-chunk partials summed in chunk order).
 #pragma once
 #include "common.cuh"
 
@@ -222,18 +225,30 @@ __global__ void __launch_bounds__(QRCP_THREADS) qrcp_renorm_kernel(const double*
 
 // Q~ (l x l, row-major, ld ldq) <- H_i Q~ = Q~ - tau v (v^T Q~) restricted to rows i.. (backward
 // accumulation of Q~ = H_0 ... H_{l-1} I); v is read from below the diagonal of B (column i).
+// Before H_i is applied, Q~(i:, 0:i) = 0, so only the columns j >= i change.
 __global__ void __launch_bounds__(QRCP_THREADS) qrcp_q_w_kernel(const double* __restrict__ Qt, int64_t ldq, int l,
                                                               int i, const double* __restrict__ B, int64_t ldb,
                                                               double* __restrict__ partials, int64_t ldp) {
-  const int j = blockIdx.x * QRCP_THREADS + threadIdx.x;
+  const int j = i + blockIdx.x * QRCP_THREADS + threadIdx.x;
   const int r0 = i + blockIdx.y * QRCP_ROWS, r1 = min(l, r0 + QRCP_ROWS);
   if (j >= l) return;
-  double s = 0.0;
-  for (int r = r0; r < r1; ++r) {
-    const double v = r == i ? 1.0 : B[static_cast<int64_t>(r) * ldb + i];
-    s = fma(v, Qt[static_cast<int64_t>(r) * ldq + j], s);
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int r = r0;
+  for (; r + 3 < r1; r += 4) {
+    double q[4], v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      q[u] = Qt[static_cast<int64_t>(r + u) * ldq + j];
+      v[u] = r + u == i ? 1.0 : B[static_cast<int64_t>(r + u) * ldb + i];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = fma(v[u], q[u], s[u]);
   }
-  partials[blockIdx.y * ldp + j] = s;
+  for (; r < r1; ++r) {
+    const double v = r == i ? 1.0 : B[static_cast<int64_t>(r) * ldb + i];
+    s[0] = fma(v, Qt[static_cast<int64_t>(r) * ldq + j], s[0]);
+  }
+  partials[blockIdx.y * ldp + j] = (s[0] + s[2]) + (s[1] + s[3]);
 }
 
 __global__ void __launch_bounds__(QRCP_THREADS) qrcp_q_update_kernel(double* __restrict__ Qt, int64_t ldq, int l,
@@ -241,7 +256,7 @@ __global__ void __launch_bounds__(QRCP_THREADS) qrcp_q_update_kernel(double* __r
                                                                    const double* __restrict__ tau,
                                                                    const double* __restrict__ partials, int64_t ldp,
                                                                    int nchunks) {
-  const int j = blockIdx.x * QRCP_THREADS + threadIdx.x;
+  const int j = i + blockIdx.x * QRCP_THREADS + threadIdx.x;
   if (j >= l) return;
   double w = 0.0;
   for (int c = 0; c < nchunks; ++c) w += partials[c * ldp + j];
@@ -270,6 +285,210 @@ __global__ void qrcp_zero_lower_kernel(double* __restrict__ B, int64_t ldb, int 
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = idx / l, c = idx - r * l;
     if (c < r) B[r * ldb + c] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- lookahead (fused) variant
+// Step i: qrcp_la_pivot (apply the deferred U_{i-1} to the pivot column and column i, swap,
+// reflector v_i), qrcp_la_fw (trailing rows >= i, columns > i: apply U_{i-1}, accumulate the
+// partials of w_i), qrcp_la_row (w_i from the partials, row i += U_i -> R(i, :), norm downdate).
+
+__global__ void __launch_bounds__(1024) qrcp_la_pivot_kernel(double* __restrict__ B, int64_t ldb, int l, int n, int i,
+                                                             double* __restrict__ vn1, double* __restrict__ vn2,
+                                                             int* __restrict__ perm, double* __restrict__ tau,
+                                                             const double* __restrict__ vprev, double* __restrict__ wprev,
+                                                             double* __restrict__ vbuf) {
+  __shared__ double s_val[32];
+  __shared__ int s_idx[32];
+  __shared__ int s_p;
+  __shared__ double s_red[32];
+  __shared__ double s_beta, s_scale;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double best = -1.0;
+  int bi = n;
+  for (int j = i + tid; j < n; j += blockDim.x) {
+    const double v = vn1[j];
+    if (v > best) {
+      best = v;
+      bi = j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_val[warp] = best;
+    s_idx[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double b = s_val[0];
+    int x = s_idx[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x) / 32; ++w)
+      if (s_val[w] > b || (s_val[w] == b && s_idx[w] < x)) {
+        b = s_val[w];
+        x = s_idx[w];
+      }
+    s_p = x;
+  }
+  __syncthreads();
+  const int p = s_p;
+  // the deferred update of step i-1 on the two columns that move (rows >= i)
+  if (i > 0) {
+    const double tp = tau[i - 1];
+    const double wi = wprev[i], wp = wprev[p];
+    for (int r = i + tid; r < l; r += blockDim.x) {
+      double* a = B + static_cast<int64_t>(r) * ldb;
+      const double tv = tp * vprev[r - (i - 1)];
+      a[i] = fma(-tv, wi, a[i]);
+      if (p != i) a[p] = fma(-tv, wp, a[p]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      wprev[i] = 0.0;
+      wprev[p] = 0.0;
+    }
+  }
+  if (p != i) {
+    for (int r = tid; r < l; r += blockDim.x) {
+      double* a = B + static_cast<int64_t>(r) * ldb;
+      const double t = a[i];
+      a[i] = a[p];
+      a[p] = t;
+    }
+    if (tid == 0) {
+      double t = vn1[i];
+      vn1[i] = vn1[p];
+      vn1[p] = t;
+      t = vn2[i];
+      vn2[i] = vn2[p];
+      vn2[p] = t;
+      const int q = perm[i];
+      perm[i] = perm[p];
+      perm[p] = q;
+    }
+  }
+  __syncthreads();
+  double ss = 0.0;
+  for (int r = i + 1 + tid; r < l; r += blockDim.x) {
+    const double x = B[static_cast<int64_t>(r) * ldb + i];
+    ss = fma(x, x, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) s_red[warp] = ss;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x) / 32; ++w) t += s_red[w];
+    const double alpha = B[static_cast<int64_t>(i) * ldb + i];
+    if (t == 0.0) {
+      tau[i] = 0.0;
+      s_beta = alpha;
+      s_scale = 0.0;
+    } else {
+      const double nrm = sqrt(fma(alpha, alpha, t));
+      const double beta = alpha >= 0.0 ? -nrm : nrm;
+      tau[i] = (beta - alpha) / beta;
+      s_beta = beta;
+      s_scale = 1.0 / (alpha - beta);
+    }
+  }
+  __syncthreads();
+  const double scale = s_scale;
+  for (int r = i + tid; r < l; r += blockDim.x) {
+    double* a = B + static_cast<int64_t>(r) * ldb + i;
+    if (r == i) {
+      *a = s_beta;
+      vbuf[0] = 1.0;
+    } else {
+      const double v = *a * scale;
+      *a = v;
+      vbuf[r - i] = v;
+    }
+  }
+}
+
+// rows [r0, r1) of the trailing block (r >= i, columns j > i): B -= tau_{i-1} v_{i-1} w_{i-1}^T, then
+// partials[c][j] = sum_r v_i[r - i] B(r, j)
+__global__ void __launch_bounds__(QRCP_THREADS) qrcp_la_fw_kernel(double* __restrict__ B, int64_t ldb, int l, int n,
+                                                                int i, const double* __restrict__ tau,
+                                                                const double* __restrict__ vprev,
+                                                                const double* __restrict__ wprev,
+                                                                const double* __restrict__ vcur,
+                                                                double* __restrict__ partials, int64_t ldp) {
+  const int j = i + 1 + blockIdx.x * QRCP_THREADS + threadIdx.x;
+  const int r0 = i + blockIdx.y * QRCP_ROWS, r1 = min(l, r0 + QRCP_ROWS);
+  if (j >= n) return;
+  const double tw = i > 0 ? tau[i - 1] * wprev[j] : 0.0;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int r = r0;
+  for (; r + 3 < r1; r += 4) {  // four rows in flight (memory-level parallelism)
+    double* a = B + static_cast<int64_t>(r) * ldb + j;
+    double b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) b[u] = a[u * ldb];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i > 0) {
+        b[u] = fma(-vprev[r + u - (i - 1)], tw, b[u]);
+        a[u * ldb] = b[u];
+      }
+      s[u] = fma(vcur[r + u - i], b[u], s[u]);
+    }
+  }
+  for (; r < r1; ++r) {
+    double* a0 = B + static_cast<int64_t>(r) * ldb + j;
+    double b0 = *a0;
+    if (i > 0) {
+      b0 = fma(-vprev[r - (i - 1)], tw, b0);
+      *a0 = b0;
+    }
+    s[0] = fma(vcur[r - i], b0, s[0]);
+  }
+  const double s0 = s[0] + s[2], s1 = s[1] + s[3];
+  partials[blockIdx.y * ldp + j] = s0 + s1;
+}
+
+// w_i[j] (chunk partials in order) -> wprev; row i: R(i, j) = B(i, j) - tau_i w_i[j]; partial-norm
+// downdate (dlaqp2), recomputed from rows > i (with the deferred update applied) on cancellation.
+__global__ void __launch_bounds__(QRCP_THREADS) qrcp_la_row_kernel(double* __restrict__ B, int64_t ldb, int l, int n,
+                                                                 int i, const double* __restrict__ tau,
+                                                                 const double* __restrict__ vcur,
+                                                                 const double* __restrict__ partials, int64_t ldp,
+                                                                 int nchunks, double* __restrict__ wprev,
+                                                                 double* __restrict__ vn1, double* __restrict__ vn2,
+                                                                 double tol3z) {
+  const int j = i + 1 + blockIdx.x * QRCP_THREADS + threadIdx.x;
+  if (j >= n) return;
+  double w = 0.0;
+  for (int c = 0; c < nchunks; ++c) w += partials[c * ldp + j];
+  wprev[j] = w;
+  const double tw = tau[i] * w;
+  double* bij = B + static_cast<int64_t>(i) * ldb + j;
+  const double rij = *bij - tw;
+  *bij = rij;
+  const double n1 = vn1[j];
+  if (n1 != 0.0) {
+    double temp = fabs(rij) / n1;
+    temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+    const double ratio = n1 / vn2[j];
+    if (temp * ratio * ratio <= tol3z) {
+      double s = 0.0;
+      for (int r = i + 1; r < l; ++r) {
+        const double a = fma(-vcur[r - i], tw, B[static_cast<int64_t>(r) * ldb + j]);
+        s = fma(a, a, s);
+      }
+      vn1[j] = sqrt(s);
+      vn2[j] = vn1[j];
+    } else {
+      vn1[j] = n1 * sqrt(temp);
+    }
   }
 }
 
