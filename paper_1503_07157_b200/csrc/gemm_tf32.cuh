@@ -65,6 +65,7 @@ struct TfParams {
   int64_t split_stride;
   double* norm_partials;  // SUB_COL: per-CTA sum of squares of the new C (FP64), one per CTA
   int a3d, b3d;       // NN: one 3D TMA per operand per stage ({32, K, rows/32} view)
+  const int* gate;    // optional: the kernel does nothing unless *gate != 0
 };
 
 // TS = true: the A operand goes to TMEM (hi and lo, 64 columns per stage, written by the
@@ -232,6 +233,7 @@ template <int LAYOUT, int BN, int EPI, bool TS>
 __global__ void __launch_bounds__(TF_THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                      const __grid_constant__ CUtensorMap tC, const TfParams p) {
+  if (p.gate != nullptr && __ldcg(p.gate) == 0) return;
   constexpr bool SUB = EPI == TF_SUB_COL;
   using Cfg = TfCfg<BN, SUB, TS>;
   constexpr int STAGES = Cfg::STAGES;

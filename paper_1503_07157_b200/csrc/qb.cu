@@ -174,6 +174,7 @@ struct qb_ctx_s {
   cudaEvent_t ev_copy = nullptr;
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
   DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw;  // qb_pivoted_qr
+  DevBuf X32, T32;  // FP32 contexts: FP32 copies of a CholeskyQR pass's X and T
   cusolverDnHandle_t solver = nullptr;
   int block_fallbacks = 0;
   const double* outQ = nullptr;
@@ -437,6 +438,10 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   return check_launch(ctx, "splitk_reduce");
 }
 
+template <typename Tin, typename Tout>
+qb_status launch_convert(qb_ctx ctx, const Tin* in, int64_t ldi, int64_t rows, int64_t cols, Tout* out, int64_t ldo,
+                         const int* gate = nullptr);
+
 // ---------------------------------------------------------------- FP32 (3xTF32 tcgen05) GEMM
 // K-major operand boxes use the plain 128-byte swizzle (SWIZZLE_128B), MN-major ones the
 // 32-byte-atom variant that the MN-major TF32 descriptor expects (SWIZZLE_128B_ATOM_32B); the
@@ -515,10 +520,12 @@ qb_status dispatch_tf(qb_ctx ctx, int layout, int epi, const CUtensorMap& ta, co
 // with the per-CTA FP64 sum of squares of the new C in ctx->parts (want_norm).  Split-K
 // partials (STORE only) are FP64 and reduced in a fixed order as in gemm().
 qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const float* A, int64_t lda, const float* B,
-                  int64_t ldb, void* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true) {
+                  int64_t ldb, void* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true,
+                  const int* gate = nullptr) {
   if (nparts) *nparts = 0;
   if (M <= 0 || N <= 0) return QB_OK;
   TfParams p{};
+  p.gate = gate;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -598,7 +605,7 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
     if (nparts) *nparts = grid;
   }
   splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp,
-                                                               static_cast<double*>(C), ldc, sq, nullptr, 0);
+                                                               static_cast<double*>(C), ldc, sq, gate, 0);
   return check_launch(ctx, "splitk_reduce");
 }
 
@@ -619,8 +626,11 @@ qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) 
     attr_done = true;
   }
   const int64_t ld = round_up(kMaxB, 16);
+  // Newton-Schulz when ||G - I||_F <= 1e-8 (FP64: step error <= 1e-16), <= 1e-4 on FP32 contexts
+  // (step error <= 7.5e-9, below FP32 rounding; reading R18c)
+  const double ns_tol2 = !ns ? -1.0 : (ctx->dtype == QB_F32 ? 1e-8 : 1e-16);
   chol_cluster_kernel<<<CHOL_CTAS, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(
-      ctx->G.d(), ld, w, m_rows, ctx->Rinv.d(), ld, status_dev(ctx), 1e-13, ns ? 1e-16 : -1.0, gate);
+      ctx->G.d(), ld, w, m_rows, ctx->Rinv.d(), ld, status_dev(ctx), 1e-13, ns_tol2, gate);
   return check_launch(ctx, "chol");
 }
 
@@ -632,6 +642,19 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
               gate));
   if (row_distributed) QB_TRY(allreduce_sum(ctx, ctx->G.d(), (size_t)(ldgb * w)));  // G = sum_p src_p^T src_p
   QB_TRY(chol_inv(ctx, w, m, true, gate));
+  static const int orth64 = debug_env("QB_ORTH64");
+  if (ctx->dtype == QB_F32 && !orth64) {
+    // FP32 contexts (reading R18c): X T on the 3xTF32 tensor cores from FP32 copies of X and T;
+    // the Gram stays FP64
+    const int64_t ldx = round_up(m, 16);
+    QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(ldx * w)));
+    QB_TRY(ensure(ctx, ctx->T32, sizeof(float) * (size_t)(ldgb * ldgb)));
+    float* X32 = static_cast<float*>(ctx->X32.p);
+    float* T32 = static_cast<float*>(ctx->T32.p);
+    QB_TRY(launch_convert(ctx, src, lds, m, w, X32, ldx, gate));
+    QB_TRY(launch_convert(ctx, static_cast<const double*>(ctx->Rinv.d()), ldgb, w, w, T32, ldgb, gate));
+    return gemm_tf(ctx, GEMM_NN, TF_STORE_COL, (int)m, w, w, X32, ldx, T32, ldgb, dst, ldd, false, nullptr, true, gate);
+  }
   return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr, true,
               gate);
 }
@@ -719,11 +742,12 @@ qb_status launch_omega(qb_ctx ctx, uint64_t seed, int64_t row0, int64_t row1, in
 }
 
 template <typename Tin, typename Tout>
-qb_status launch_convert(qb_ctx ctx, const Tin* in, int64_t ldi, int64_t rows, int64_t cols, Tout* out, int64_t ldo) {
+qb_status launch_convert(qb_ctx ctx, const Tin* in, int64_t ldi, int64_t rows, int64_t cols, Tout* out, int64_t ldo,
+                         const int* gate) {
   if (rows <= 0 || cols <= 0) return QB_OK;
   const int64_t total = rows * cols;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16 * ctx->num_sms));
-  convert_kernel<Tin, Tout><<<grid, 256, 0, ctx->stream>>>(in, ldi, rows, cols, out, ldo);
+  convert_kernel<Tin, Tout><<<grid, 256, 0, ctx->stream>>>(in, ldi, rows, cols, out, ldo, gate);
   return check_launch(ctx, "convert");
 }
 
@@ -925,7 +949,7 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->QB,    &ctx->R,    &ctx->Usv,    &ctx->Vsv,  &ctx->Ssv, &ctx->Wsv,    &ctx->Ut,
                     &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
-                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw};
+                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);

@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
 // the FP32 path).
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in, int64_t ldi, int64_t rows,
-                                                      int64_t cols, Tout* __restrict__ out, int64_t ldo) {
+                                                      int64_t cols, Tout* __restrict__ out, int64_t ldo,
+                                                      const int* __restrict__ gate) {
+  if (gate != nullptr && __ldcg(gate) == 0) return;
   const int64_t total = rows * cols;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
