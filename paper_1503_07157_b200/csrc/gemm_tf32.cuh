@@ -25,10 +25,11 @@
 //               (warp w reads TMEM lanes 32 (w % 4) .. + 31 = tile rows) while the MMAs of the
 //               next unit run in the other TMEM buffer
 //   warp 10     TF_SUB_COL only: TMA-loads the C tile, 128 x 32 at a time, into a ring that
-//               the epilogue updates in place and TMA-stores back
+//               the epilogue updates in place, and TMA-stores each sub-tile back once the
+//               epilogue warps are done with it
 // Barriers per stage: full (TMA bytes landed), conv (128 splitters done), empty (MMAs done,
 // tcgen05.commit); per TMEM buffer: acc_full (chunk's MMAs done), acc_empty (drained); per C
-// slot: cfull (loaded), cempty (stored).
+// slot: cfull (loaded), cdone (updated by the 4 epilogue warps).
 //
 // Operand layouts in shared memory (UMMA canonical 128B-swizzle layouts):
 //   K-major (TN): box {32 k, rows}: row r at r*128 B, 8-row groups at 1024 B (SBO), the k-th
@@ -47,7 +48,7 @@ constexpr int TF_PROMO = 4;       // k-tiles (128 k) per TMEM accumulation chunk
 constexpr int TF_THREADS = 352;   // 11 warps, see the header comment
 constexpr int TF_CSUB = 32;       // TF_SUB_COL: C streams through shared memory 128 x 32 at a time
 #ifndef QB_TF_CSLOTS
-#define QB_TF_CSLOTS 2
+#define QB_TF_CSLOTS 4
 #endif
 constexpr int TF_CSLOTS = QB_TF_CSLOTS;  // ring of C sub-tiles
 
@@ -246,8 +247,8 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint64_t* cfull = acc_empty + 2;      // [TF_CSLOTS]
-  uint64_t* cempty = cfull + TF_CSLOTS; // [TF_CSLOTS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + TF_CSLOTS);
+  uint64_t* cdone = cfull + TF_CSLOTS;  // [TF_CSLOTS] the promoters are done with the slot's sub-tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cdone + TF_CSLOTS);
   double* red = reinterpret_cast<double*>(tmem_slot + 2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
     }
     for (int s = 0; s < TF_CSLOTS; ++s) {
       mbar_init(&cfull[s], 1);
-      mbar_init(&cempty[s], 1);
+      mbar_init(&cdone[s], 4);  // one arrive per promoter warp
     }
     fence_barrier_init();
   }
@@ -516,31 +517,27 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           const int slot = cs % TF_CSLOTS;
           mbar_wait(&cfull[slot], (cs / TF_CSLOTS) & 1);
           float* cb = sC + slot * (TF_BM * TF_CSUB);
-          double s4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent FP64 chains (latency)
+          // squares summed in FP32 over 8 entries (four chains), then in FP64: relative error
+          // <= 8 * 2^-24 (positive terms), far below the FP32 residual's own rounding; FP64
+          // conversions per entry cost 18 % of this kernel (R18)
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int i = 0; i < TF_CSUB; ++i) {
             const float r = cb[i * TF_BM + row] - acc[sub * TF_CSUB + i];
             cb[i * TF_BM + row] = r;
-            const double rd = sub * TF_CSUB + i < ncols ? static_cast<double>(r) : 0.0;
-            s4[i & 3] = fma(rd, rd, s4[i & 3]);
+            const float rv = sub * TF_CSUB + i < ncols ? r : 0.f;
+            s4[i & 3] = fmaf(rv, rv, s4[i & 3]);
           }
-          sq += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          sq += (static_cast<double>(s4[0]) + static_cast<double>(s4[1])) +
+                (static_cast<double>(s4[2]) + static_cast<double>(s4[3]));
+          // generic-proxy writes -> visible to the TMA store the C warp issues after cdone
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("bar.sync 2, 128;" ::: "memory");
-          if (warp == 6 && lane == 0) {
-            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                             reinterpret_cast<uint64_t>(&tC)),
-                         "r"(smem_u32(cb)), "r"(w.m0), "r"(w.n0 + sub * TF_CSUB)
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            mbar_arrive(&cempty[slot]);
-          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&cdone[slot]);
         }
       }
     }
     if (SUB) {
-      if (warp == 6 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       if (p.norm_partials != nullptr) {
         sq = warp_sum(sq);
         if (lane == 0) red[warp - 6] = sq;
@@ -549,19 +546,39 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
       }
     }
   } else if (SUB) {
-    // ---------------------------------------------------------------- C producer (warp 10)
+    // ---------------------------------------------------------------- C warp (warp 10)
+    // Loads sub-tile cs into slot cs % TF_CSLOTS once the store of sub-tile cs - TF_CSLOTS (same
+    // slot) has read it out; that store is issued here as soon as the promoters are done with
+    // it (cdone), so the promoters never wait for a store.
     if (lane == 0) {
       tma_prefetch_desc(&tC);
+      int cm[TF_CSLOTS] = {}, cn[TF_CSLOTS] = {};  // origin of the sub-tile held by each slot
       int cs = 0;
+      auto store = [&](int t) {
+        const int slot = t % TF_CSLOTS;
+        mbar_wait(&cdone[slot], (t / TF_CSLOTS) & 1);
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tC)),
+                     "r"(smem_u32(sC + slot * (TF_BM * TF_CSUB))), "r"(cm[slot]), "r"(cn[slot])
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      };
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const TfUnit w = tf_unit(p, u, BN);
         for (int sub = 0; sub < BN / TF_CSUB; ++sub, ++cs) {
           const int slot = cs % TF_CSLOTS;
-          if (cs >= TF_CSLOTS) mbar_wait(&cempty[slot], ((cs / TF_CSLOTS) - 1) & 1);
+          if (cs >= TF_CSLOTS) {
+            store(cs - TF_CSLOTS);
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          cm[slot] = w.m0;
+          cn[slot] = w.n0 + sub * TF_CSUB;
           mbar_arrive_expect_tx(&cfull[slot], Cfg::CSUB_BYTES);
-          tma_load_2d(sC + slot * (TF_BM * TF_CSUB), &tC, &cfull[slot], w.m0, w.n0 + sub * TF_CSUB);
+          tma_load_2d(sC + slot * (TF_BM * TF_CSUB), &tC, &cfull[slot], cm[slot], cn[slot]);
         }
       }
+      for (int t = cs - TF_CSLOTS < 0 ? 0 : cs - TF_CSLOTS; t < cs; ++t) store(t);
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   }
 
