@@ -200,10 +200,12 @@ __device__ __forceinline__ void pin8(float (&t)[8]) {
   asm volatile("" : "+f"(t[0]), "+f"(t[1]), "+f"(t[2]), "+f"(t[3]), "+f"(t[4]), "+f"(t[5]), "+f"(t[6]), "+f"(t[7]));
 }
 
+// RN_tf32 with ties away from zero (= cvt.rna.tf32.f32 on finite x): add half an ulp of the
+// 10-bit mantissa to the magnitude bits and truncate; two integer ops instead of cvt's four
+// (cvt also keeps Inf/NaN; here Inf stays Inf and a NaN may become Inf, but lo = x - hi is NaN
+// for both, so the products come out NaN either way)
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 template <int LAYOUT, int BN>
@@ -334,8 +336,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
               const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
               const uint32_t tah = ta + 8 * kk, tal = ta + 32 + 8 * kk;
               umma_tf32_ts(tacc, tah, dBh + adv, idesc_ts, (!first || kk > 0) ? 1u : 0u);
+#ifndef QB_TF_EXP_1MMA
               umma_tf32_ts(tacc, tah, dBl + adv, idesc_ts, 1u);
               umma_tf32_ts(tacc, tal, dBh + adv, idesc_ts, 1u);
+#endif
             }
           } else {
             const uint32_t a_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES);
@@ -374,6 +378,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           // raw stage, split, store hi / lo to the stage's TMEM columns
           const int quad = warp & 3, r = quad * 32 + lane;
           uint32_t hi[32], lo[32];
+#ifndef QB_TF_EXP_NOATMEM
 #pragma unroll
           for (int k = 0; k < TF_BK; ++k) {
             const uint32_t off = LAYOUT == 0
@@ -388,9 +393,12 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
                               static_cast<uint32_t>(Cfg::A_TMEM_COL + 64 * slot);
           tmem_st32(ta, hi);
           tmem_st32(ta + 32, lo);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#endif
           // B: hi in place, lo after it
           uint8_t* sb = st + Cfg::A_BYTES;
+#ifdef QB_TF_EXP_NOBSPLIT
+          if (false)
+#endif
 #pragma unroll 4
           for (int i = t; i < Cfg::B_BYTES / 16; i += 128) {
             float4* hp = reinterpret_cast<float4*>(sb + i * 16);
@@ -407,6 +415,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
             *hp = h;
             *reinterpret_cast<float4*>(sb + Cfg::B_BYTES + i * 16) = l;
           }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // A's TMEM stores (overlapped with B)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         } else {

@@ -16,7 +16,8 @@ def classify(name, grid):
         lay, bn, epi = (int(m.group(1)), int(m.group(2)), int(m.group(3))) if m else (-1, -1, -1)
         return f"gemm_f64<{'NN' if lay == 0 else 'TN'},{bn},{['STORE_COL', 'STORE_ROW', 'SUB_COL'][epi]}>"
     if "gemm_tf32_kernel" in name:
-        m = re.search(r"gemm_tf32_kernel<(?:\(int\))?(\d), (?:\(int\))?(\d+), (?:\(int\))?(\d)>", name)
+        m = re.search(r"gemm_tf32_kernel<(?:\(int\))?(\d), (?:\(int\))?(\d+), (?:\(int\))?(\d)(?:, (?:\(bool\))?\w+)?>",
+                      name)
         lay, bn, epi = (int(m.group(1)), int(m.group(2)), int(m.group(3))) if m else (-1, -1, -1)
         return f"gemm_tf32<{'NN' if lay == 0 else 'TN'},{bn},{['STORE_COL', 'STORE_ROW', 'SUB_COL'][epi]}>"
     m = re.search(r"qbk::(\w+)", name)
