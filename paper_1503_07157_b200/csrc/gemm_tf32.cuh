@@ -67,6 +67,7 @@ struct TfParams {
   double* norm_partials;  // SUB_COL: per-CTA sum of squares of the new C (FP64), one per CTA
   int a3d, b3d;       // NN: one 3D TMA per operand per stage ({32, K, rows/32} view)
   const int* gate;    // optional: the kernel does nothing unless *gate != 0
+  int bsplit;         // TS: B arrives pre-split (tB = hi, tB2 = lo, tf32_split_kernel); no B split here
 };
 
 // TS = true: the A operand goes to TMEM (hi and lo, 64 columns per stage, written by the
@@ -209,17 +210,8 @@ __device__ __forceinline__ float tf32_rna(float x) {
 }
 
 template <int LAYOUT, int BN>
-__device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, uint8_t* sA, uint8_t* sB,
-                                               uint64_t* bar, int m0, int n0, int k0, int a3d, int b3d) {
-  using Cfg = TfCfg<BN>;  // raw operand bytes do not depend on the epilogue or on TS
-  mbar_arrive_expect_tx(bar, Cfg::HI_BYTES);
-  if (LAYOUT == 0) {  // NN: MN-major chunks of 32 rows x 32 k
-    if (a3d) {
-      tma_load_3d(sA, tA, bar, 0, k0, m0 / 32);
-    } else {
-#pragma unroll
-      for (int c = 0; c < TF_BM / 32; ++c) tma_load_2d(sA + c * 4096, tA, bar, m0 + 32 * c, k0);
-    }
+__device__ __forceinline__ void tf_load_b(const CUtensorMap* tB, uint8_t* sB, uint64_t* bar, int n0, int k0, int b3d) {
+  if (LAYOUT == 0) {  // NN: MN-major chunks of 32 columns x 32 k
     if (b3d) {
       tma_load_3d(sB, tB, bar, 0, k0, n0 / 32);
     } else {
@@ -227,15 +219,52 @@ __device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUte
       for (int c = 0; c < BN / 32; ++c) tma_load_2d(sB + c * 4096, tB, bar, n0 + 32 * c, k0);
     }
   } else {  // TN: K-major rows
-    tma_load_2d(sA, tA, bar, k0, m0);
     tma_load_2d(sB, tB, bar, k0, n0);
+  }
+}
+
+// One stage's raw A and B tiles; with bsplit, B's hi and lo tiles (tB, tB2) into sB and sB2.
+template <int LAYOUT, int BN>
+__device__ __forceinline__ void tf_issue_stage(const CUtensorMap* tA, const CUtensorMap* tB, const CUtensorMap* tB2,
+                                               uint8_t* sA, uint8_t* sB, uint8_t* sB2, uint64_t* bar, int m0, int n0,
+                                               int k0, int a3d, int b3d, int bsplit) {
+  using Cfg = TfCfg<BN>;  // raw operand bytes do not depend on the epilogue or on TS
+  mbar_arrive_expect_tx(bar, Cfg::HI_BYTES + (bsplit ? Cfg::B_BYTES : 0));
+  if (LAYOUT == 0) {  // NN: MN-major chunks of 32 rows x 32 k
+    if (a3d) {
+      tma_load_3d(sA, tA, bar, 0, k0, m0 / 32);
+    } else {
+#pragma unroll
+      for (int c = 0; c < TF_BM / 32; ++c) tma_load_2d(sA + c * 4096, tA, bar, m0 + 32 * c, k0);
+    }
+  } else {  // TN: K-major rows
+    tma_load_2d(sA, tA, bar, k0, m0);
+  }
+  tf_load_b<LAYOUT, BN>(tB, sB, bar, n0, k0, b3d);
+  if (bsplit) tf_load_b<LAYOUT, BN>(tB2, sB2, bar, n0, k0, b3d);
+}
+
+// hi = RN_tf32(x), lo = x - hi for a small operand that many tiles re-read (outer x inner,
+// inner contiguous, leading dimension ld for all three arrays), split once instead of per tile.
+__global__ void __launch_bounds__(256) tf32_split_kernel(const float* __restrict__ x, int64_t ld, int64_t outer,
+                                                         int64_t inner, float* __restrict__ hi,
+                                                         float* __restrict__ lo) {
+  const int64_t total = outer * inner;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t o = idx / inner, i = idx - o * inner;
+    const float v = x[o * ld + i];
+    const float h = tf32_rna(v);
+    hi[o * ld + i] = h;
+    lo[o * ld + i] = v - h;
   }
 }
 
 template <int LAYOUT, int BN, int EPI, bool TS>
 __global__ void __launch_bounds__(TF_THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
-                     const __grid_constant__ CUtensorMap tC, const TfParams p) {
+                     const __grid_constant__ CUtensorMap tB2, const __grid_constant__ CUtensorMap tC,
+                     const TfParams p) {
   if (p.gate != nullptr && __ldcg(p.gate) == 0) return;
   constexpr bool SUB = EPI == TF_SUB_COL;
   using Cfg = TfCfg<BN, SUB, TS>;
@@ -259,6 +288,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   if (tid == 0) {
     tma_prefetch_desc(&tA);
     tma_prefetch_desc(&tB);
+    if (p.bsplit) tma_prefetch_desc(&tB2);
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -295,8 +325,8 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           const int slot = j % STAGES;
           if (j >= STAGES) mbar_wait(&empty[slot], ((j / STAGES) - 1) & 1);
           uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
-          tf_issue_stage<LAYOUT, BN>(&tA, &tB, st, st + Cfg::A_BYTES, &full[slot], w.m0, w.n0, (w.kt0 + kt) * TF_BK,
-                                     p.a3d, p.b3d);
+          tf_issue_stage<LAYOUT, BN>(&tA, &tB, &tB2, st, st + Cfg::A_BYTES, st + Cfg::A_BYTES + Cfg::B_BYTES,
+                                     &full[slot], w.m0, w.n0, (w.kt0 + kt) * TF_BK, p.a3d, p.b3d, TS ? p.bsplit : 0);
         }
       }
     }
@@ -336,10 +366,8 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
               const uint64_t adv = static_cast<uint64_t>(kk) * KSTEP;
               const uint32_t tah = ta + 8 * kk, tal = ta + 32 + 8 * kk;
               umma_tf32_ts(tacc, tah, dBh + adv, idesc_ts, (!first || kk > 0) ? 1u : 0u);
-#ifndef QB_TF_EXP_1MMA
               umma_tf32_ts(tacc, tah, dBl + adv, idesc_ts, 1u);
               umma_tf32_ts(tacc, tal, dBh + adv, idesc_ts, 1u);
-#endif
             }
           } else {
             const uint32_t a_hi = smem_u32(smem + slot * Cfg::STAGE_BYTES);
@@ -378,7 +406,6 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           // raw stage, split, store hi / lo to the stage's TMEM columns
           const int quad = warp & 3, r = quad * 32 + lane;
           uint32_t hi[32], lo[32];
-#ifndef QB_TF_EXP_NOATMEM
 #pragma unroll
           for (int k = 0; k < TF_BK; ++k) {
             const uint32_t off = LAYOUT == 0
@@ -393,27 +420,25 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
                               static_cast<uint32_t>(Cfg::A_TMEM_COL + 64 * slot);
           tmem_st32(ta, hi);
           tmem_st32(ta + 32, lo);
-#endif
           // B: hi in place, lo after it
           uint8_t* sb = st + Cfg::A_BYTES;
-#ifdef QB_TF_EXP_NOBSPLIT
-          if (false)
-#endif
+          if (!p.bsplit) {
 #pragma unroll 4
-          for (int i = t; i < Cfg::B_BYTES / 16; i += 128) {
-            float4* hp = reinterpret_cast<float4*>(sb + i * 16);
-            const float4 v = *hp;
-            float4 h, l;
-            h.x = tf32_rna(v.x);
-            h.y = tf32_rna(v.y);
-            h.z = tf32_rna(v.z);
-            h.w = tf32_rna(v.w);
-            l.x = v.x - h.x;
-            l.y = v.y - h.y;
-            l.z = v.z - h.z;
-            l.w = v.w - h.w;
-            *hp = h;
-            *reinterpret_cast<float4*>(sb + Cfg::B_BYTES + i * 16) = l;
+            for (int i = t; i < Cfg::B_BYTES / 16; i += 128) {
+              float4* hp = reinterpret_cast<float4*>(sb + i * 16);
+              const float4 v = *hp;
+              float4 h, l;
+              h.x = tf32_rna(v.x);
+              h.y = tf32_rna(v.y);
+              h.z = tf32_rna(v.z);
+              h.w = tf32_rna(v.w);
+              l.x = v.x - h.x;
+              l.y = v.y - h.y;
+              l.z = v.z - h.z;
+              l.w = v.w - h.w;
+              *hp = h;
+              *reinterpret_cast<float4*>(sb + Cfg::B_BYTES + i * 16) = l;
+            }
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // A's TMEM stores (overlapped with B)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -175,6 +175,7 @@ struct qb_ctx_s {
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
   DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw;  // qb_pivoted_qr
   DevBuf X32, T32;  // FP32 contexts: FP32 copies of a CholeskyQR pass's X and T
+  DevBuf Bsp;       // FP32 GEMM: a small B operand split into hi / lo
   cusolverDnHandle_t solver = nullptr;
   int block_fallbacks = 0;
   const double* outQ = nullptr;
@@ -479,8 +480,8 @@ qb_status make_map3d_f32(qb_ctx ctx, CUtensorMap* map, const float* ptr, uint64_
 }
 
 template <int LAYOUT, int BN, int EPI, bool TS>
-qb_status launch_tf_ts(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                       const TfParams& p, int splits) {
+qb_status launch_tf_ts(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
+                       const CUtensorMap& tc, const TfParams& p, int splits) {
   using Cfg = TfCfg<BN, EPI == TF_SUB_COL, TS>;
   auto kern = gemm_tf32_kernel<LAYOUT, BN, EPI, TS>;
   static bool attr_done = false;
@@ -489,30 +490,34 @@ qb_status launch_tf_ts(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb,
     attr_done = true;
   }
   const int units = p.tiles_m * p.tiles_n * splits;
-  kern<<<std::min(units, ctx->num_sms), Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tc, p);
+  kern<<<std::min(units, ctx->num_sms), Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tb2, tc, p);
   return check_launch(ctx, "gemm_tf32");
 }
 
 // A operand in TMEM (TS, more pipeline stages) unless QB_TF_SS=1 (both operands in shared memory)
-template <int LAYOUT, int BN, int EPI>
-qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                      const TfParams& p, int splits) {
+int tf_ss_mode() {
   static const int ss = debug_env("QB_TF_SS");
-  if (ss) return launch_tf_ts<LAYOUT, BN, EPI, false>(ctx, ta, tb, tc, p, splits);
-  return launch_tf_ts<LAYOUT, BN, EPI, true>(ctx, ta, tb, tc, p, splits);
+  return ss;
+}
+
+template <int LAYOUT, int BN, int EPI>
+qb_status launch_tf_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2,
+                      const CUtensorMap& tc, const TfParams& p, int splits) {
+  if (tf_ss_mode()) return launch_tf_ts<LAYOUT, BN, EPI, false>(ctx, ta, tb, tb2, tc, p, splits);
+  return launch_tf_ts<LAYOUT, BN, EPI, true>(ctx, ta, tb, tb2, tc, p, splits);
 }
 
 template <int BN>
 qb_status dispatch_tf(qb_ctx ctx, int layout, int epi, const CUtensorMap& ta, const CUtensorMap& tb,
-                      const CUtensorMap& tc, const TfParams& p, int splits) {
+                      const CUtensorMap& tb2, const CUtensorMap& tc, const TfParams& p, int splits) {
   if (layout == GEMM_NN) {
-    if (epi == TF_STORE_COL) return launch_tf_t<GEMM_NN, BN, TF_STORE_COL>(ctx, ta, tb, tc, p, splits);
-    if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_NN, BN, TF_STORE_ROW>(ctx, ta, tb, tc, p, splits);
-    return launch_tf_t<GEMM_NN, BN, TF_SUB_COL>(ctx, ta, tb, tc, p, splits);
+    if (epi == TF_STORE_COL) return launch_tf_t<GEMM_NN, BN, TF_STORE_COL>(ctx, ta, tb, tb2, tc, p, splits);
+    if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_NN, BN, TF_STORE_ROW>(ctx, ta, tb, tb2, tc, p, splits);
+    return launch_tf_t<GEMM_NN, BN, TF_SUB_COL>(ctx, ta, tb, tb2, tc, p, splits);
   }
-  if (epi == TF_STORE_COL) return launch_tf_t<GEMM_TN, BN, TF_STORE_COL>(ctx, ta, tb, tc, p, splits);
-  if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_TN, BN, TF_STORE_ROW>(ctx, ta, tb, tc, p, splits);
-  return launch_tf_t<GEMM_TN, BN, TF_SUB_COL>(ctx, ta, tb, tc, p, splits);
+  if (epi == TF_STORE_COL) return launch_tf_t<GEMM_TN, BN, TF_STORE_COL>(ctx, ta, tb, tb2, tc, p, splits);
+  if (epi == TF_STORE_ROW) return launch_tf_t<GEMM_TN, BN, TF_STORE_ROW>(ctx, ta, tb, tb2, tc, p, splits);
+  return launch_tf_t<GEMM_TN, BN, TF_SUB_COL>(ctx, ta, tb, tb2, tc, p, splits);
 }
 
 // FP32 operands, 3xTF32 products with FP32 accumulation.  epi TF_STORE_COL / TF_STORE_ROW
@@ -541,24 +546,45 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   splits = std::max(1, (p.nkt + p.kt_per_split - 1) / p.kt_per_split);
   p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
 
-  CUtensorMap ta, tb;
+  // A small B operand that many row tiles re-read (Ω, B_i, W, T) is split into hi / lo once
+  // (tf32_split_kernel) instead of in every tile's stages
+  static const int no_bsplit = debug_env("QB_TF_NO_BSPLIT");
+  p.bsplit = !no_bsplit && !tf_ss_mode() && p.tiles_m >= 4 && static_cast<int64_t>(K) * N <= (int64_t{4} << 20);
+  const float* Bhi = B;
+  float* Blo = nullptr;
+  if (p.bsplit) {
+    const int64_t outer = layout == GEMM_NN ? K : N, inner = layout == GEMM_NN ? N : K;
+    QB_TRY(ensure(ctx, ctx->Bsp, sizeof(float) * (size_t)(2 * outer * ldb)));
+    float* hi = static_cast<float*>(ctx->Bsp.p);
+    Blo = hi + outer * ldb;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((outer * inner + 255) / 256, 4 * ctx->num_sms));
+    tf32_split_kernel<<<grid, 256, 0, ctx->stream>>>(B, ldb, outer, inner, hi, Blo);
+    QB_TRY(check_launch(ctx, "tf32_split"));
+    Bhi = hi;
+  }
+  CUtensorMap ta, tb, tb2;
+  auto map_b = [&](CUtensorMap* map, const float* ptr) -> qb_status {
+    if (layout == GEMM_TN) return make_map_f32(ctx, map, ptr, K, N, ldb, TF_BK, bn, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (p.b3d) return make_map3d_f32(ctx, map, ptr, N, K, ldb, bn / 32);
+    return make_map_f32(ctx, map, ptr, N, K, ldb, 32, TF_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  };
   if (layout == GEMM_NN) {
     p.a3d = M % 32 == 0;
     p.b3d = N % 32 == 0 && N >= bn;
     if (p.a3d) QB_TRY(make_map3d_f32(ctx, &ta, A, M, K, lda, TF_BM / 32));
     else QB_TRY(make_map_f32(ctx, &ta, A, M, K, lda, 32, TF_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
-    if (p.b3d) QB_TRY(make_map3d_f32(ctx, &tb, B, N, K, ldb, bn / 32));
-    else QB_TRY(make_map_f32(ctx, &tb, B, N, K, ldb, 32, TF_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   } else {
     QB_TRY(make_map_f32(ctx, &ta, A, K, M, lda, TF_BK, TF_BM, CU_TENSOR_MAP_SWIZZLE_128B));
-    QB_TRY(make_map_f32(ctx, &tb, B, K, N, ldb, TF_BK, bn, CU_TENSOR_MAP_SWIZZLE_128B));
   }
+  QB_TRY(map_b(&tb, Bhi));
+  if (p.bsplit) QB_TRY(map_b(&tb2, Blo));
+  else tb2 = tb;
   CUtensorMap tc = ta;
   if (epi == TF_SUB_COL)
     QB_TRY(make_map_f32(ctx, &tc, static_cast<const float*>(C), M, N, ldc, TF_BM, TF_CSUB, CU_TENSOR_MAP_SWIZZLE_NONE));
   auto run = [&](int e, int s) -> qb_status {
-    if (bn == 64) return dispatch_tf<64>(ctx, layout, e, ta, tb, tc, p, s);
-    if (bn == 128) return dispatch_tf<128>(ctx, layout, e, ta, tb, tc, p, s);
+    if (bn == 64) return dispatch_tf<64>(ctx, layout, e, ta, tb, tb2, tc, p, s);
+    if (bn == 128) return dispatch_tf<128>(ctx, layout, e, ta, tb, tb2, tc, p, s);
     return fail(ctx, QB_ERR_INVALID_ARG, "QB_TF_BN must be 64 or 128");
   };
 
@@ -949,7 +975,8 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->QB,    &ctx->R,    &ctx->Usv,    &ctx->Vsv,  &ctx->Ssv, &ctx->Wsv,    &ctx->Ut,
                     &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
-                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32};
+                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32,
+                    &ctx->Bsp};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
