@@ -624,4 +624,293 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Subtract-update C -= A B for a short K (<= 128, the block size b: the downdate A^(i) -= Q_i B_i
+// and the re-projection Q_i -= Q̄ W) with the A row block RESIDENT in TMEM.  Each persistent CTA
+// takes a contiguous run of tiles in n-fast order, so consecutive tiles share their 128 rows of
+// A: those are loaded, split (hi, lo) and stored to TMEM once per row block instead of once
+// per tile, and the only per-tile operand traffic is the pre-split B tile (hi, lo; L2-resident)
+// besides C itself.  Warp roles as in gemm_tf32_kernel; the splitters only handle A.
+template <int BN>
+struct TfAresCfg {
+  static constexpr int A_BYTES = TF_BM * TF_BK * 4;          // one 32-k slab of A (raw)
+  static constexpr int B_BYTES = BN * TF_BK * 4;             // one 32-k slab of B (hi or lo)
+  static constexpr int BSTAGE_BYTES = 2 * B_BYTES;
+  static constexpr int CSUB_BYTES = TF_BM * TF_CSUB * 4;
+  static constexpr int C_BYTES = TF_CSLOTS * CSUB_BYTES;
+  static constexpr int ASTAGES = 2;
+  static constexpr int BSTAGES = (224 * 1024 - C_BYTES - ASTAGES * A_BYTES) / BSTAGE_BYTES;
+  static constexpr int A_TMEM_COL = 2 * BN;                  // slab s: hi at +64 s, lo at +64 s + 32
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int NBAR = 2 * BSTAGES + 2 * ASTAGES + 2 + 4 + 2 * TF_CSLOTS;
+  static constexpr int SMEM_BYTES = 1024 + BSTAGES * BSTAGE_BYTES + ASTAGES * A_BYTES + C_BYTES + NBAR * 8 + 64;
+  static_assert(BSTAGES >= 2, "B double buffering");
+  static_assert(A_TMEM_COL + 64 * 4 <= TMEM_COLS, "A (K <= 128) and two accumulators fit TMEM");
+};
+
+__device__ __forceinline__ void tf_ares_range(const TfParams& p, int& u0, int& u1) {
+  const int64_t units = static_cast<int64_t>(p.tiles_m) * p.tiles_n;
+  u0 = static_cast<int>(units * blockIdx.x / gridDim.x);
+  u1 = static_cast<int>(units * (blockIdx.x + 1) / gridDim.x);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(TF_THREADS, 1)
+    gemm_tf32_sub_ares_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBh,
+                              const __grid_constant__ CUtensorMap tBl, const __grid_constant__ CUtensorMap tC,
+                              const TfParams p) {
+  if (p.gate != nullptr && __ldcg(p.gate) == 0) return;
+  using Cfg = TfAresCfg<BN>;
+  constexpr int BS = Cfg::BSTAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sBst = smem;                                           // [BS][B hi | B lo]
+  uint8_t* sAst = sBst + BS * Cfg::BSTAGE_BYTES;                  // [2][A slab]
+  float* sC = reinterpret_cast<float*>(sAst + Cfg::ASTAGES * Cfg::A_BYTES);  // [TF_CSLOTS][32][128]
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sC) + Cfg::C_BYTES);
+  uint64_t* bempty = bfull + BS;
+  uint64_t* afull = bempty + BS;       // [2] A slab landed
+  uint64_t* aempty = afull + 2;        // [2] A slab read by the 128 splitters
+  uint64_t* a_ready = aempty + 2;      // A row block in TMEM (128 splitters)
+  uint64_t* a_free = a_ready + 1;      // MMAs done with the row block (tcgen05.commit)
+  uint64_t* acc_full = a_free + 1;     // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint64_t* cfull = acc_empty + 2;     // [TF_CSLOTS]
+  uint64_t* cdone = cfull + TF_CSLOTS; // [TF_CSLOTS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cdone + TF_CSLOTS);
+  double* red = reinterpret_cast<double*>(tmem_slot + 2);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int u0, u1;
+  tf_ares_range(p, u0, u1);
+  const int nkt = p.nkt;  // <= 4
+  auto tile_m0 = [&](int u) { return (u / p.tiles_n) * TF_BM; };
+  auto tile_n0 = [&](int u) { return (u % p.tiles_n) * BN; };
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tA);
+    tma_prefetch_desc(&tBh);
+    tma_prefetch_desc(&tBl);
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 128);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
+    }
+    mbar_init(a_ready, 128);
+    mbar_init(a_free, 1);
+    for (int s = 0; s < TF_CSLOTS; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cdone[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer: A slabs per row block, B per tile
+    if (lane == 0) {
+      int jb = 0, ja = 0, prev_m = -1;
+      for (int u = u0; u < u1; ++u) {
+        const int m0 = tile_m0(u), n0 = tile_n0(u);
+        if (m0 != prev_m) {
+          for (int s = 0; s < nkt; ++s, ++ja) {
+            const int slot = ja & 1;
+            if (ja >= 2) mbar_wait(&aempty[slot], ((ja >> 1) - 1) & 1);
+            uint8_t* sa = sAst + slot * Cfg::A_BYTES;
+            mbar_arrive_expect_tx(&afull[slot], Cfg::A_BYTES);
+            if (p.a3d) {
+              tma_load_3d(sa, &tA, &afull[slot], 0, s * TF_BK, m0 / 32);
+            } else {
+#pragma unroll
+              for (int c = 0; c < TF_BM / 32; ++c) tma_load_2d(sa + c * 4096, &tA, &afull[slot], m0 + 32 * c, s * TF_BK);
+            }
+          }
+          prev_m = m0;
+        }
+        for (int kt = 0; kt < nkt; ++kt, ++jb) {
+          const int slot = jb % BS;
+          if (jb >= BS) mbar_wait(&bempty[slot], ((jb / BS) - 1) & 1);
+          uint8_t* sb = sBst + slot * Cfg::BSTAGE_BYTES;
+          mbar_arrive_expect_tx(&bfull[slot], 2 * Cfg::B_BYTES);
+          tf_load_b<0, BN>(&tBh, sb, &bfull[slot], n0, kt * TF_BK, p.b3d);
+          tf_load_b<0, BN>(&tBl, sb + Cfg::B_BYTES, &bfull[slot], n0, kt * TF_BK, p.b3d);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_ts = tf32_idesc<BN>(0, 1);  // A K-major in TMEM, B MN-major
+      int jb = 0, c = 0, r = 0, prev_m = -1;
+      for (int u = u0; u < u1; ++u) {
+        const int m0 = tile_m0(u);
+        if (m0 != prev_m) {
+          mbar_wait(a_ready, r & 1);
+          ++r;
+          prev_m = m0;
+        }
+        const int b = c & 1;
+        if (c >= 2) mbar_wait(&acc_empty[b], ((c >> 1) - 1) & 1);
+        const uint32_t tacc = tmem_base + static_cast<uint32_t>(b * BN);
+        for (int kt = 0; kt < nkt; ++kt, ++jb) {
+          const int slot = jb % BS;
+          mbar_wait(&bfull[slot], (jb / BS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t b_hi = smem_u32(sBst + slot * Cfg::BSTAGE_BYTES);
+          const uint64_t dBh = umma_desc(b_hi, 4096u, 512u, 1u), dBl = umma_desc(b_hi + Cfg::B_BYTES, 4096u, 512u, 1u);
+          const uint32_t ta = tmem_base + static_cast<uint32_t>(Cfg::A_TMEM_COL + 64 * kt);
+#pragma unroll
+          for (int kk = 0; kk < TF_BK / 8; ++kk) {
+            const uint64_t adv = static_cast<uint64_t>(kk) * 64u;
+            const uint32_t tah = ta + 8 * kk, tal = ta + 32 + 8 * kk;
+            umma_tf32_ts(tacc, tah, dBh + adv, idesc_ts, (kt > 0 || kk > 0) ? 1u : 0u);
+            umma_tf32_ts(tacc, tah, dBl + adv, idesc_ts, 1u);
+            umma_tf32_ts(tacc, tal, dBh + adv, idesc_ts, 1u);
+          }
+          umma_commit(&bempty[slot]);
+        }
+        umma_commit(&acc_full[b]);
+        ++c;
+        if (u + 1 == u1 || tile_m0(u + 1) != m0) umma_commit(a_free);
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ splitters: A row block -> TMEM
+    const int quad = warp & 3, rr = quad * 32 + lane;
+    int ja = 0, r = 0, prev_m = -1;
+    for (int u = u0; u < u1; ++u) {
+      const int m0 = tile_m0(u);
+      if (m0 == prev_m) continue;
+      prev_m = m0;
+      if (r > 0) {
+        mbar_wait(a_free, (r - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      for (int s = 0; s < nkt; ++s, ++ja) {
+        const int slot = ja & 1;
+        mbar_wait(&afull[slot], (ja >> 1) & 1);
+        const uint8_t* sa = sAst + slot * Cfg::A_BYTES;
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < TF_BK; ++k) {
+          const uint32_t off = (rr >> 5) * 4096 + k * 128 + ((((rr & 31) >> 3) ^ (k & 3)) << 5) + ((rr & 7) << 2);
+          const float x = *reinterpret_cast<const float*>(sa + off);
+          const float h = tf32_rna(x);
+          hi[k] = __float_as_uint(h);
+          lo[k] = __float_as_uint(x - h);
+        }
+        mbar_arrive(&aempty[slot]);
+        const uint32_t ta = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                            static_cast<uint32_t>(Cfg::A_TMEM_COL + 64 * s);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(a_ready);
+      ++r;
+    }
+  } else if (warp < 10) {
+    // ------------------------------------------------------------ epilogue: C -= acc, sum of squares
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t trow = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    double sq = 0.0;
+    int c = 0, cs = 0;
+    for (int u = u0; u < u1; ++u, ++c) {
+      const int m0 = tile_m0(u), n0 = tile_n0(u);
+      const int b = c & 1;
+      mbar_wait(&acc_full[b], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float acc[BN];
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(trow + static_cast<uint32_t>(b * BN + c0), v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[c0 + i] = __uint_as_float(v[i]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acc_empty[b]);
+      const int ncols = m0 + row < p.M ? min(BN, p.N - n0) : 0;
+#pragma unroll
+      for (int sub = 0; sub < BN / TF_CSUB; ++sub, ++cs) {
+        const int slot = cs % TF_CSLOTS;
+        mbar_wait(&cfull[slot], (cs / TF_CSLOTS) & 1);
+        float* cb = sC + slot * (TF_BM * TF_CSUB);
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};  // FP32 over 8 entries, then FP64 (R18)
+#pragma unroll
+        for (int i = 0; i < TF_CSUB; ++i) {
+          const float x = cb[i * TF_BM + row] - acc[sub * TF_CSUB + i];
+          cb[i * TF_BM + row] = x;
+          const float xv = sub * TF_CSUB + i < ncols ? x : 0.f;
+          s4[i & 3] = fmaf(xv, xv, s4[i & 3]);
+        }
+        sq += (static_cast<double>(s4[0]) + static_cast<double>(s4[1])) +
+              (static_cast<double>(s4[2]) + static_cast<double>(s4[3]));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cdone[slot]);
+      }
+    }
+    if (p.norm_partials != nullptr) {
+      sq = warp_sum(sq);
+      if (lane == 0) red[warp - 6] = sq;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 6 && lane == 0) p.norm_partials[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+    }
+  } else {
+    // ------------------------------------------------------------ C warp: load / store the C ring
+    if (lane == 0) {
+      tma_prefetch_desc(&tC);
+      int cm[TF_CSLOTS] = {}, cn[TF_CSLOTS] = {};
+      int cs = 0;
+      auto store = [&](int t) {
+        const int slot = t % TF_CSLOTS;
+        mbar_wait(&cdone[slot], (t / TF_CSLOTS) & 1);
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tC)),
+                     "r"(smem_u32(sC + slot * (TF_BM * TF_CSUB))), "r"(cm[slot]), "r"(cn[slot])
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      };
+      for (int u = u0; u < u1; ++u) {
+        for (int sub = 0; sub < BN / TF_CSUB; ++sub, ++cs) {
+          const int slot = cs % TF_CSLOTS;
+          if (cs >= TF_CSLOTS) {
+            store(cs - TF_CSLOTS);
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          cm[slot] = tile_m0(u);
+          cn[slot] = tile_n0(u) + sub * TF_CSUB;
+          mbar_arrive_expect_tx(&cfull[slot], Cfg::CSUB_BYTES);
+          tma_load_2d(sC + slot * (TF_BM * TF_CSUB), &tC, &cfull[slot], cm[slot], cn[slot]);
+        }
+      }
+      for (int t = cs - TF_CSLOTS < 0 ? 0 : cs - TF_CSLOTS; t < cs; ++t) store(t);
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+  }
+}
+
 }  // namespace qbk

@@ -495,6 +495,21 @@ qb_status launch_tf_ts(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb,
 }
 
 // A operand in TMEM (TS, more pipeline stages) unless QB_TF_SS=1 (both operands in shared memory)
+template <int BN>
+qb_status launch_tf_ares(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
+                         const CUtensorMap& tc, const TfParams& p) {
+  using Cfg = TfAresCfg<BN>;
+  auto kern = gemm_tf32_sub_ares_kernel<BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_done = true;
+  }
+  const int units = p.tiles_m * p.tiles_n;
+  kern<<<std::min(units, ctx->num_sms), TF_THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tbh, tbl, tc, p);
+  return check_launch(ctx, "gemm_tf32_sub_ares");
+}
+
 int tf_ss_mode() {
   static const int ss = debug_env("QB_TF_SS");
   return ss;
@@ -597,6 +612,12 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
       QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
       p.norm_partials = ctx->parts.d();
       if (nparts) *nparts = grid;
+    }
+    // short K (the block size): A's row block stays in TMEM across the CTA's run of tiles
+    static const int no_ares = debug_env("QB_TF_NO_ARES");
+    if (!no_ares && layout == GEMM_NN && p.bsplit && K <= 4 * TF_BK) {
+      if (bn == 64) return launch_tf_ares<64>(ctx, ta, tb, tb2, tc, p);
+      if (bn == 128) return launch_tf_ares<128>(ctx, ta, tb, tb2, tc, p);
     }
     return run(TF_SUB_COL, 1);
   }

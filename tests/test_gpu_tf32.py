@@ -62,7 +62,10 @@ def run(qbp, c, layout, epi, M, N, K, A, lda, B, ldb, C0, split):
 
 
 SHAPES = [(1, 1, 1), (7, 5, 3), (128, 64, 32), (129, 65, 33), (300, 200, 1000), (1000, 256, 5000),
-          (256, 1250, 333), (4000, 130, 64), (200, 2100, 40), (385, 2000, 256), (2000, 128, 20000)]
+          (256, 1250, 333), (4000, 130, 64), (200, 2100, 40), (385, 2000, 256), (2000, 128, 20000),
+          # short K with >= 4 row tiles: the subtract-update keeps A's row block in TMEM
+          # (several tiles per CTA share a row block in the last two)
+          (1000, 300, 128), (777, 129, 100), (2000, 2000, 33), (513, 64, 1), (40000, 256, 128), (20000, 700, 96)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
