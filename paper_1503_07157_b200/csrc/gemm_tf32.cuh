@@ -68,6 +68,8 @@ struct TfParams {
   int a3d, b3d;       // NN: one 3D TMA per operand per stage ({32, K, rows/32} view)
   const int* gate;    // optional: the kernel does nothing unless *gate != 0
   int bsplit;         // TS: B arrives pre-split (tB = hi, tB2 = lo, tf32_split_kernel); no B split here
+  float* C32;         // STORE_COL without split-K: optional FP32 copy of C (ld ldc32)
+  int64_t ldc32;
 };
 
 // TS = true: the A operand goes to TMEM (hi and lo, 64 columns per stage, written by the
@@ -507,6 +509,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           if (EPI == TF_STORE_COL) {
             double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(w.split) * p.split_stride + m +
                           static_cast<int64_t>(w.n0) * p.ldc;
+            float* dst32 = p.C32 != nullptr ? p.C32 + m + static_cast<int64_t>(w.n0) * p.ldc32 : nullptr;
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 8) {
               float t[8];
@@ -515,7 +518,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
               pin8(t);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                if (c0 + i < ncols) *dst = static_cast<double>(t[i]);
+                if (c0 + i < ncols) {
+                  *dst = static_cast<double>(t[i]);
+                  if (dst32 != nullptr) dst32[static_cast<int64_t>(c0 + i) * p.ldc32] = t[i];
+                }
                 dst += p.ldc;
               }
             }

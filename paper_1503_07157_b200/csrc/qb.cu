@@ -175,6 +175,7 @@ struct qb_ctx_s {
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
   DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw;  // qb_pivoted_qr
   DevBuf X32, T32;  // FP32 contexts: FP32 copies of a CholeskyQR pass's X and T
+  DevBuf X32b;      // FP32 contexts: RN_32 of CholeskyQR2's scratch (when the caller takes an FP32 copy)
   DevBuf Bsp;       // FP32 GEMM: a small B operand split into hi / lo
   cusolverDnHandle_t solver = nullptr;
   int block_fallbacks = 0;
@@ -539,9 +540,10 @@ qb_status dispatch_tf(qb_ctx ctx, int layout, int epi, const CUtensorMap& ta, co
 // write a DOUBLE C (column- / row-major); TF_SUB_COL updates a FLOAT column-major C -= result
 // with the per-CTA FP64 sum of squares of the new C in ctx->parts (want_norm).  Split-K
 // partials (STORE only) are FP64 and reduced in a fixed order as in gemm().
+// TF_STORE_COL may also write an FP32 copy C32 (ld ldc32) of the result (= RN_32 of C).
 qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const float* A, int64_t lda, const float* B,
                   int64_t ldb, void* C, int64_t ldc, bool want_norm, int64_t* nparts, bool allow_split = true,
-                  const int* gate = nullptr) {
+                  const int* gate = nullptr, float* C32 = nullptr, int64_t ldc32 = 0) {
   if (nparts) *nparts = 0;
   if (M <= 0 || N <= 0) return QB_OK;
   TfParams p{};
@@ -623,9 +625,12 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   }
   p.splits = splits;
   const int64_t rows = epi == TF_STORE_ROW ? M : N, cols = epi == TF_STORE_ROW ? N : M;
+  if (epi != TF_STORE_COL) C32 = nullptr;
   if (splits == 1) {
     p.C = C;
     p.ldc = ldc;
+    p.C32 = C32;
+    p.ldc32 = ldc32;
     QB_TRY(run(epi, 1));
     if (want_norm) {
       const int grid = (int)std::min<int64_t>(rows, 4 * ctx->num_sms);
@@ -652,7 +657,8 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
     if (nparts) *nparts = grid;
   }
   splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp,
-                                                               static_cast<double*>(C), ldc, sq, gate, 0);
+                                                               static_cast<double*>(C), ldc, sq, gate, 0, C32,
+                                                               ldc32);
   return check_launch(ctx, "splitk_reduce");
 }
 
@@ -682,8 +688,11 @@ qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) 
 }
 
 // One CholeskyQR pass: dst = src T, with T from chol_inv (all on the device; gated).
+// FP32 contexts: src32 (optional) is RN_32(src) already in memory (ld lds32), else src is
+// converted into ctx->X32; dst32 (optional) receives RN_32(dst) (ld ldd32); src32 != dst32.
 qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
-                      const int* gate, bool row_distributed) {
+                      const int* gate, bool row_distributed, const float* src32 = nullptr, int64_t lds32 = 0,
+                      float* dst32 = nullptr, int64_t ldd32 = 0) {
   const int64_t ldgb = round_up(kMaxB, 16);
   QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr, true,
               gate));
@@ -694,16 +703,24 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
     // FP32 contexts (reading R18c): X T on the 3xTF32 tensor cores from FP32 copies of X and T;
     // the Gram stays FP64
     const int64_t ldx = round_up(m, 16);
-    QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(ldx * w)));
     QB_TRY(ensure(ctx, ctx->T32, sizeof(float) * (size_t)(ldgb * ldgb)));
-    float* X32 = static_cast<float*>(ctx->X32.p);
+    const float* X32 = src32;
+    int64_t ld_x = lds32;
+    if (X32 == nullptr) {
+      QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(ldx * w)));
+      QB_TRY(launch_convert(ctx, src, lds, m, w, static_cast<float*>(ctx->X32.p), ldx, gate));
+      X32 = static_cast<const float*>(ctx->X32.p);
+      ld_x = ldx;
+    }
     float* T32 = static_cast<float*>(ctx->T32.p);
-    QB_TRY(launch_convert(ctx, src, lds, m, w, X32, ldx, gate));
     QB_TRY(launch_convert(ctx, static_cast<const double*>(ctx->Rinv.d()), ldgb, w, w, T32, ldgb, gate));
-    return gemm_tf(ctx, GEMM_NN, TF_STORE_COL, (int)m, w, w, X32, ldx, T32, ldgb, dst, ldd, false, nullptr, true, gate);
+    return gemm_tf(ctx, GEMM_NN, TF_STORE_COL, (int)m, w, w, X32, ld_x, T32, ldgb, dst, ldd, false, nullptr, true, gate,
+                   dst32, ldd32);
   }
-  return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr, true,
-              gate);
+  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, w, w, src, lds, ctx->Rinv.d(), ldgb, dst, ldd, false, nullptr, true,
+              gate));
+  if (dst32 != nullptr) QB_TRY(launch_convert(ctx, static_cast<const double*>(dst), ldd, m, w, dst32, ldd32, gate));
+  return QB_OK;
 }
 
 // orth(src) -> dst: CholeskyQR2, where a pass whose Gram is already within 1e-8 of I takes
@@ -716,22 +733,40 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
 // replicated T applied to the local rows.
 // single = true (cholqr1 below): the second pass runs only after a SHIFTED first factorization
 // (then the whole shifted CholeskyQR3 runs); otherwise a factorized first pass is final.
+// FP32 contexts: src32 / dst32 (optional) as in cholqr_pass; the FP32 copy of the scratch
+// lives in ctx->X32b, so that no pass reads and writes the same FP32 buffer.
 qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
-                  bool row_distributed = false, bool single = false) {
+                  bool row_distributed = false, bool single = false, const float* src32 = nullptr,
+                  int64_t lds32 = 0, float* dst32 = nullptr, int64_t ldd32 = 0) {
   const int64_t ldt = round_up(m, 16);
   double* T = ctx->T1.d();
+  float* T32 = nullptr;  // RN_32(T) when the caller wants dst32
+  if (dst32 != nullptr) {
+    QB_TRY(ensure(ctx, ctx->X32b, sizeof(float) * (size_t)(ldt * w)));
+    T32 = static_cast<float*>(ctx->X32b.p);
+  }
   QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, 2 * sizeof(int), ctx->stream));
-  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr, row_distributed));
+  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr, row_distributed, src32, lds32, T32, ldt));
   // second pass only after a factorization (status[2]); a Newton-Schulz first pass is final
   const int* gate2 = status_dev(ctx) + (single ? 1 : 2);
-  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, gate2, row_distributed));
+  if (T32 != nullptr) {
+    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, gate2, row_distributed, T32, ldt, dst32, ldd32));
+  } else {
+    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, gate2, row_distributed));
+  }
   {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
-    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, gate2);
+    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, gate2, T32, ldt, dst32, ldd32);
     QB_TRY(check_launch(ctx, "gated_copy"));
   }
-  QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed));
-  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed));
+  if (T32 != nullptr) {
+    // src32 of the shifted passes: dst32 -> T32 -> dst32 (never read and written in one pass)
+    QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed, dst32, ldd32, T32, ldt));
+    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed, T32, ldt, dst32, ldd32));
+  } else {
+    QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed));
+    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed));
+  }
   return QB_OK;
 }
 
@@ -739,8 +774,9 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
 // and its CholeskyQR2 follow in the same block; the orth after the projection restores full
 // orthogonality.  A first pass that needed the shift still runs the whole shifted CholeskyQR3.
 qb_status cholqr1(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
-                  bool row_distributed = false) {
-  return cholqr2(ctx, src, lds, dst, ldd, m, w, row_distributed, true);
+                  bool row_distributed = false, const float* src32 = nullptr, int64_t lds32 = 0,
+                  float* dst32 = nullptr, int64_t ldd32 = 0) {
+  return cholqr2(ctx, src, lds, dst, ldd, m, w, row_distributed, true, src32, lds32, dst32, ldd32);
 }
 
 // Orthonormalise the m x l column-major panel X (ld ldx) in place for any l: 256 columns at a
@@ -997,7 +1033,7 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
                     &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32,
-                    &ctx->Bsp};
+                    &ctx->Bsp,   &ctx->X32b};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -1642,10 +1678,22 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     double* Bi = ctx->Bbar.d() + ell * ctx->ldb;
 
     // Y = A X for a row-major n x w operand X (ld bp): Ω_i or Z^T
+    // FP32 contexts: Q̄32_i = RN_32(Q_i) is written by the orth passes themselves, and the sketch
+    // leaves Y32 = RN_32(Y) in ctx->X32 for the first CholeskyQR pass (not on column shards, where
+    // Y is the all-reduced sum of the local products)
+    float* Qbar32 = static_cast<float*>(ctx->Qbar32.p);
+    float* Qi32 = is_f32 ? Qbar32 + ell * ctx->ldq : nullptr;
+    float* Y32 = nullptr;
+    if (is_f32 && !colsh) {
+      // sized for every CholeskyQR pass of the block (Y's and the power steps' Z), so that no
+      // later ensure() moves the buffer under Y32
+      QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(std::max(ldm, ldn) * w)));
+      Y32 = static_cast<float*>(ctx->X32.p);
+    }
     auto sketch = [&](const void* X) -> qb_status {
       if (is_f32)
         return gemm_tf(ctx, GEMM_NN, TF_STORE_COL, (int)m, (int)w, (int)n, A32, ldA, static_cast<const float*>(X), bp,
-                       ctx->Y.d(), ldm, false, nullptr);
+                       ctx->Y.d(), ldm, false, nullptr, true, nullptr, Y32, ldm);
       return gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)w, (int)n, A, ldA, static_cast<const double*>(X), bp,
                   ctx->Y.d(), ldm, false, nullptr);
     };
@@ -1680,13 +1728,14 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     // orth of line (3); a single CholeskyQR pass when the re-projection's orth follows (R11b)
     static const int full_first_orth = debug_env("QB_FULL_FIRST_ORTH");  // experiment: 1 = CholeskyQR2 always
     const bool reproj_follows = ell > 0 && !(flags & QB_NO_REPROJ) && !full_first_orth;
-    auto orth_y = [&]() -> qb_status {
-      return reproj_follows ? cholqr1(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh)
-                            : cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh);
+    // orth of a freshly sketched Y into Q_i (and Q̄32_i on FP32 contexts)
+    auto orth_y_into = [&](bool single) -> qb_status {
+      return cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh, single, Y32, ldm, Qi32, ctx->ldq);
     };
+    auto orth_y = [&]() -> qb_status { return orth_y_into(reproj_follows); };
     if (!(skip_orth_flag(flags) && q > 0)) {
       if (q == 0) QB_TRY(orth_y());
-      else QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
+      else QB_TRY(orth_y_into(false));
     }
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     const bool skip_orth = (flags & QB_SKIP_POWER_ORTH) != 0;
@@ -1706,16 +1755,13 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       QB_TRY(sketch(ctx->Zt.p));
       if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
       if (j == q - 1) QB_TRY(orth_y());  // the last orth of the power scheme, line (6)
-      else QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh));
+      else QB_TRY(orth_y_into(false));
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
-    float* Qbar32 = static_cast<float*>(ctx->Qbar32.p);
-    float* Qi32 = is_f32 ? Qbar32 + ell * ctx->ldq : nullptr;
     if (ell > 0 && !(flags & QB_NO_REPROJ)) {
       QB_TRY(ensure(ctx, ctx->W, sizeof(double) * (size_t)(ell * bp)));
       if (is_f32) {  // on the FP32 copies: W = Q̄^T Q_i, Q_i -= Q̄ W (3xTF32), then orth in FP64
         QB_TRY(ensure(ctx, ctx->W32, sizeof(float) * (size_t)(ell * bp)));
-        QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Qi32, ctx->ldq));
         QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)ell, (int)w, (int)m, Qbar32, ctx->ldq, Qi32, ctx->ldq,
                        ctx->W.d(), bp, false, nullptr));
         if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->W.d(), (size_t)(ell * bp)));  // W = sum_p Q̄_p^T Q_p
@@ -1723,17 +1769,17 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
         QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)w, (int)ell, Qbar32, ctx->ldq,
                        static_cast<const float*>(ctx->W32.p), bp, Qi32, ctx->ldq, false, nullptr));
         QB_TRY(launch_convert(ctx, static_cast<const float*>(Qi32), ctx->ldq, m, w, Qi, ctx->ldq));
+        // Q̄32_i = RN_32(Q_i) holds: it is both the pass's FP32 source and its FP32 destination
+        QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, rowsh, false, Qi32, ctx->ldq, Qi32, ctx->ldq));
       } else {
         QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)ell, (int)w, (int)m, Qbar, ctx->ldq, Qi, ctx->ldq, ctx->W.d(),
                     bp, false, nullptr));
         if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->W.d(), (size_t)(ell * bp)));  // W = sum_p Q̄_p^T Q_p
         QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)ell, Qbar, ctx->ldq, ctx->W.d(), bp, Qi,
                     ctx->ldq, false, nullptr));
+        QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, rowsh));
       }
-      QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, rowsh));
     }
-    // FP32 contexts: Q̄32_i = RN_32(Q_i), the factor the caller receives and the residual's GEMMs use
-    if (is_f32) QB_TRY(launch_convert(ctx, static_cast<const double*>(Qi), ctx->ldq, m, w, Qi32, ctx->ldq));
     // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
     int64_t nb_parts = 0;
     QB_CUDA(cudaEventRecord(ctx->evp[2], ctx->stream));

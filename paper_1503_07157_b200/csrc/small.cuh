@@ -61,7 +61,9 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
                                                                     int64_t rows, int64_t cols, int64_t ldp,
                                                                     double* __restrict__ out, int64_t ldo,
                                                                     double* __restrict__ sq_partials,
-                                                                    const int* __restrict__ gate, int subtract) {
+                                                                    const int* __restrict__ gate, int subtract,
+                                                                    float* __restrict__ out32 = nullptr,
+                                                                    int64_t ld32 = 0) {
   if (gate != nullptr && __ldcg(gate) == 0) return;
   __shared__ double red[RED_THREADS / 32];
   double sq = 0.0;
@@ -74,6 +76,7 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
     for (int s = 0; s < S; ++s) v += src[s * stride];
     if (subtract) v = out[r * ldo + c] - v;  // C -= sum of the split products
     out[r * ldo + c] = v;
+    if (out32 != nullptr) out32[r * ld32 + c] = static_cast<float>(v);  // FP32 contexts: RN_32 copy
     sq = fma(v, v, sq);
   }
   if (sq_partials != nullptr) {
@@ -124,13 +127,17 @@ __global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in
 // Newton-Schulz step is final; its result moves from the scratch to the destination).
 __global__ void __launch_bounds__(256) gated_copy_kernel(const double* __restrict__ src, int64_t lds,
                                                          double* __restrict__ dst, int64_t ldd, int64_t rows,
-                                                         int64_t cols, const int* __restrict__ gate) {
+                                                         int64_t cols, const int* __restrict__ gate,
+                                                         const float* __restrict__ src32 = nullptr,
+                                                         int64_t lds32 = 0, float* __restrict__ dst32 = nullptr,
+                                                         int64_t ldd32 = 0) {
   if (__ldcg(gate) != 0) return;
   const int64_t total = rows * cols;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t c = idx / rows, r = idx - c * rows;
     dst[r + c * ldd] = src[r + c * lds];
+    if (dst32 != nullptr) dst32[r + c * ldd32] = src32[r + c * lds32];  // and its FP32 copy
   }
 }
 
