@@ -735,6 +735,10 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
 // (then the whole shifted CholeskyQR3 runs); otherwise a factorized first pass is final.
 // FP32 contexts: src32 / dst32 (optional) as in cholqr_pass; the FP32 copy of the scratch
 // lives in ctx->X32b, so that no pass reads and writes the same FP32 buffer.
+// When src and dst are different buffers, the first pass writes dst directly and a second
+// pass goes through the scratch and back (gated copy), so the common single-pass case (a
+// Newton-Schulz first pass, or cholqr1 without the shift) moves no data; in place, the first
+// pass goes to the scratch.
 qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
                   bool row_distributed = false, bool single = false, const float* src32 = nullptr,
                   int64_t lds32 = 0, float* dst32 = nullptr, int64_t ldd32 = 0) {
@@ -745,28 +749,24 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
     QB_TRY(ensure(ctx, ctx->X32b, sizeof(float) * (size_t)(ldt * w)));
     T32 = static_cast<float*>(ctx->X32b.p);
   }
+  const bool inplace = src == dst || (src32 != nullptr && src32 == dst32);
   QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, 2 * sizeof(int), ctx->stream));
-  QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr, row_distributed, src32, lds32, T32, ldt));
   // second pass only after a factorization (status[2]); a Newton-Schulz first pass is final
   const int* gate2 = status_dev(ctx) + (single ? 1 : 2);
-  if (T32 != nullptr) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
+  if (inplace) {
+    QB_TRY(cholqr_pass(ctx, src, lds, T, ldt, m, w, nullptr, row_distributed, src32, lds32, T32, ldt));
     QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, gate2, row_distributed, T32, ldt, dst32, ldd32));
+    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, gate2, T32, ldt, dst32, ldd32, 0);
   } else {
-    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, gate2, row_distributed));
+    QB_TRY(cholqr_pass(ctx, src, lds, dst, ldd, m, w, nullptr, row_distributed, src32, lds32, dst32, ldd32));
+    QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, gate2, row_distributed, dst32, ldd32, T32, ldt));
+    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, gate2, T32, ldt, dst32, ldd32, 1);
   }
-  {
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
-    gated_copy_kernel<<<grid, 256, 0, ctx->stream>>>(T, ldt, dst, ldd, m, w, gate2, T32, ldt, dst32, ldd32);
-    QB_TRY(check_launch(ctx, "gated_copy"));
-  }
-  if (T32 != nullptr) {
-    // src32 of the shifted passes: dst32 -> T32 -> dst32 (never read and written in one pass)
-    QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed, dst32, ldd32, T32, ldt));
-    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed, T32, ldt, dst32, ldd32));
-  } else {
-    QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed));
-    QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed));
-  }
+  QB_TRY(check_launch(ctx, "gated_copy"));
+  // shifted first factorization (status[1]): two more passes, dst -> T -> dst
+  QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed, dst32, ldd32, T32, ldt));
+  QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed, T32, ldt, dst32, ldd32));
   return QB_OK;
 }
 
@@ -1768,9 +1768,16 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
         QB_TRY(launch_convert(ctx, ctx->W.d(), bp, w, ell, static_cast<float*>(ctx->W32.p), bp));
         QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)w, (int)ell, Qbar32, ctx->ldq,
                        static_cast<const float*>(ctx->W32.p), bp, Qi32, ctx->ldq, false, nullptr));
-        QB_TRY(launch_convert(ctx, static_cast<const float*>(Qi32), ctx->ldq, m, w, Qi, ctx->ldq));
-        // Q̄32_i = RN_32(Q_i) holds: it is both the pass's FP32 source and its FP32 destination
-        QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, rowsh, false, Qi32, ctx->ldq, Qi32, ctx->ldq));
+        // the projected panel to Y (FP64, for the Gram) and X32 (its FP32 source), so that the
+        // CholeskyQR2 into Q_i / Q̄32_i is not in place and its usual single pass moves no data
+        QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(std::max(ldm, ldn) * w)));
+        float* X32 = static_cast<float*>(ctx->X32.p);
+        {
+          const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
+          convert_dual_kernel<<<grid, 256, 0, ctx->stream>>>(Qi32, ctx->ldq, m, w, ctx->Y.d(), ldm, X32, ldm);
+          QB_TRY(check_launch(ctx, "convert_dual"));
+        }
+        QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh, false, X32, ldm, Qi32, ctx->ldq));
       } else {
         QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)ell, (int)w, (int)m, Qbar, ctx->ldq, Qi, ctx->ldq, ctx->W.d(),
                     bp, false, nullptr));

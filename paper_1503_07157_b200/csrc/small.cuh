@@ -123,15 +123,30 @@ __global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in
   }
 }
 
-// dst = src (column-major rows x cols) unless *gate != 0 (CholeskyQR: a first pass that took the
-// Newton-Schulz step is final; its result moves from the scratch to the destination).
+// out = (double) in and out2 = in, column-major rows x cols (FP32 contexts: an FP32 panel and its
+// FP64 copy for the Gram, R18c).
+__global__ void __launch_bounds__(256) convert_dual_kernel(const float* __restrict__ in, int64_t ldi, int64_t rows,
+                                                           int64_t cols, double* __restrict__ out, int64_t ldo,
+                                                           float* __restrict__ out2, int64_t ldo2) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = idx / rows, r = idx - c * rows;
+    const float v = in[r + c * ldi];
+    out[r + c * ldo] = static_cast<double>(v);
+    out2[r + c * ldo2] = v;
+  }
+}
+
+// dst = src (column-major rows x cols) if *gate == 0, or if *gate != 0 with when_set (CholeskyQR2:
+// moves the final pass's result from the scratch to the destination; see cholqr2).
 __global__ void __launch_bounds__(256) gated_copy_kernel(const double* __restrict__ src, int64_t lds,
                                                          double* __restrict__ dst, int64_t ldd, int64_t rows,
                                                          int64_t cols, const int* __restrict__ gate,
                                                          const float* __restrict__ src32 = nullptr,
                                                          int64_t lds32 = 0, float* __restrict__ dst32 = nullptr,
-                                                         int64_t ldd32 = 0) {
-  if (__ldcg(gate) != 0) return;
+                                                         int64_t ldd32 = 0, int when_set = 0) {
+  if ((__ldcg(gate) != 0) != (when_set != 0)) return;
   const int64_t total = rows * cols;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
