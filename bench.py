@@ -290,9 +290,17 @@ def run_ours(args, cfg):
     else:  # FP32: the 3xTF32 subtract-update streams A in and out of HBM (K = b is short)
         hbm, hbm_src = hbm_peak()
         achieved = 2.0 * m * n_local * 4 / t_down * 1e-9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_summary_r01h_tf32.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("downdate_dram_bytes_per_launch")
+            except Exception:
+                traffic = None
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": None,
-                    "kernel": "gemm_tf32_kernel<NN,128,SUB_COL> (A -= Q_i B_i, 3xTF32, fused ||A||_F^2)",
+                    "traffic": traffic,
+                    "kernel": "gemm_tf32_sub_ares_kernel<128> (A -= Q_i B_i, 3xTF32, A rows resident in TMEM, "
+                              "fused ||A||_F^2)",
                     "peak_source": hbm_src,
                     "algorithmic_per_launch": f"2*m*n_local*4 = {2.0 * m * n_local * 4:.4g} bytes (A read + write)",
                     "share_of_step": sum(s["ms_down"] for s in stats) / ms}
