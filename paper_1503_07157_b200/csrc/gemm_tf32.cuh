@@ -262,6 +262,32 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float* __restrict
   }
 }
 
+// STORE_COL epilogue of one row (m) of a unit: FP64 C (or split partial) and the optional FP32
+// copy; groups of 8 columns, pinned in order so that the compiler does not widen all BN
+// accumulators to FP64 at once (register pressure)
+template <int BN>
+__device__ __forceinline__ void tf_store_col(const TfParams& p, const TfUnit& w, const float (&acc)[BN], int m,
+                                             int ncols) {
+  double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(w.split) * p.split_stride + m +
+                static_cast<int64_t>(w.n0) * p.ldc;
+  float* dst32 = p.C32 != nullptr ? p.C32 + m + static_cast<int64_t>(w.n0) * p.ldc32 : nullptr;
+#pragma unroll
+  for (int c0 = 0; c0 < BN; c0 += 8) {
+    float t[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
+    pin8(t);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (c0 + i < ncols) {
+        *dst = static_cast<double>(t[i]);
+        if (dst32 != nullptr) dst32[static_cast<int64_t>(c0 + i) * p.ldc32] = t[i];
+      }
+      dst += p.ldc;
+    }
+  }
+}
+
 template <int LAYOUT, int BN, int EPI, bool TS>
 __global__ void __launch_bounds__(TF_THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
@@ -327,8 +353,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           const int slot = j % STAGES;
           if (j >= STAGES) mbar_wait(&empty[slot], ((j / STAGES) - 1) & 1);
           uint8_t* st = smem + slot * Cfg::STAGE_BYTES;
-          tf_issue_stage<LAYOUT, BN>(&tA, &tB, &tB2, st, st + Cfg::A_BYTES, st + Cfg::A_BYTES + Cfg::B_BYTES,
-                                     &full[slot], w.m0, w.n0, (w.kt0 + kt) * TF_BK, p.a3d, p.b3d, TS ? p.bsplit : 0);
+          // B lo: after B hi (TS: [A raw][B hi][B lo]) or in the lo half (SS: [A hi][B hi][A lo][B lo])
+          uint8_t* sblo = TS ? st + Cfg::A_BYTES + Cfg::B_BYTES : st + Cfg::HI_BYTES + Cfg::A_BYTES;
+          tf_issue_stage<LAYOUT, BN>(&tA, &tB, &tB2, st, st + Cfg::A_BYTES, sblo, &full[slot], w.m0, w.n0,
+                                     (w.kt0 + kt) * TF_BK, p.a3d, p.b3d, p.bsplit);
         }
       }
     }
@@ -446,8 +474,10 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         } else {
+          // [A hi][B hi] split in place, lo halves after them; a pre-split B only needs A
+          const int nsplit = p.bsplit ? Cfg::A_BYTES / 16 : Cfg::HI_BYTES / 16;
 #pragma unroll 4
-          for (int i = t; i < Cfg::HI_BYTES / 16; i += 128) {
+          for (int i = t; i < nsplit; i += 128) {
             float4* hp = reinterpret_cast<float4*>(st + i * 16);
             const float4 v = *hp;
             float4 h, l;
@@ -507,24 +537,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
           // groups of 8 columns, pinned in order so that the compiler does not widen all BN
           // accumulators to FP64 at once (register pressure)
           if (EPI == TF_STORE_COL) {
-            double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(w.split) * p.split_stride + m +
-                          static_cast<int64_t>(w.n0) * p.ldc;
-            float* dst32 = p.C32 != nullptr ? p.C32 + m + static_cast<int64_t>(w.n0) * p.ldc32 : nullptr;
-#pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 8) {
-              float t[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) t[i] = acc[c0 + i];
-              pin8(t);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (c0 + i < ncols) {
-                  *dst = static_cast<double>(t[i]);
-                  if (dst32 != nullptr) dst32[static_cast<int64_t>(c0 + i) * p.ldc32] = t[i];
-                }
-                dst += p.ldc;
-              }
-            }
+            tf_store_col<BN>(p, w, acc, m, ncols);
           } else {
             double* dst = static_cast<double*>(p.C) + static_cast<int64_t>(w.split) * p.split_stride +
                           static_cast<int64_t>(m) * p.ldc + w.n0;

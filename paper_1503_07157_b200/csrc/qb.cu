@@ -566,7 +566,7 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   // A small B operand that many row tiles re-read (Ω, B_i, W, T) is split into hi / lo once
   // (tf32_split_kernel) instead of in every tile's stages
   static const int no_bsplit = debug_env("QB_TF_NO_BSPLIT");
-  p.bsplit = !no_bsplit && !tf_ss_mode() && p.tiles_m >= 4 && static_cast<int64_t>(K) * N <= (int64_t{4} << 20);
+  p.bsplit = !no_bsplit && p.tiles_m >= 4 && static_cast<int64_t>(K) * N <= (int64_t{4} << 20);
   const float* Bhi = B;
   float* Blo = nullptr;
   if (p.bsplit) {
