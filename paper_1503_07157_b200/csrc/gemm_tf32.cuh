@@ -1,8 +1,9 @@
 // FP32 GEMM for sm_100a on the 5th-generation tensor cores (tcgen05.mma kind::tf32, TMEM
 // accumulators), split "3xTF32" so that the products keep FP32 accuracy.  This is the FP32
 // context's path for the contractions with the residual A (K2f/K5f/K6f):
-// Y = A Ω, B = Q^* A (:710), A -= Q B (:712), and the power steps A^* Q, A Z
-// (:868-870).  The small m x b panel work (CholeskyQR, re-projection) stays in FP64.
+// Y = A Ω, B = Q^* A (:710), A -= Q B (:712), the power steps A^* Q, A Z
+// (:868-870), and on FP32 copies the re-projection Q_i -= Q̄ (Q̄^* Q_i) (:708) and CholeskyQR's
+// X T (reading R18c).  The Grams and the Cholesky factorizations stay in FP64.
 //
 // Splitting (reading R18b): every operand x is written x = hi + lo with hi = RN_tf32(x) (10
 // explicit mantissa bits, exactly representable in TF32) and lo = x - hi (exact in FP32,
@@ -18,9 +19,10 @@
 //
 // Persistent CTAs (one per SM) walk the work units (tile x K-split) statically; CTA tile
 // 128 x BN, k-tile 32 floats (one 128-byte swizzle row); 11 warps:
-//   warp 0      TMA producer (one thread): raw FP32 tiles -> the stage's "hi" buffers
+//   warp 0      TMA producer (one thread): raw FP32 tiles (and a pre-split B's hi / lo)
 //   warp 1      TMEM allocator + MMA issuer (one thread): 4 k-steps x 3 tcgen05.mma per stage
-//   warps 2..5  split the stage in place (hi = RN_tf32(x), lo = x - hi)
+//   warps 2..5  split the stage: A's row hi / lo into the stage's TMEM columns (TS, default) or
+//               in place in shared memory (SS); B in place unless it arrives pre-split
 //   warps 6..9  drain TMEM chunks into register accumulators, then the epilogue of the unit
 //               (warp w reads TMEM lanes 32 (w % 4) .. + 31 = tile rows) while the MMAs of the
 //               next unit run in the other TMEM buffer
@@ -30,6 +32,9 @@
 // Barriers per stage: full (TMA bytes landed), conv (128 splitters done), empty (MMAs done,
 // tcgen05.commit); per TMEM buffer: acc_full (chunk's MMAs done), acc_empty (drained); per C
 // slot: cfull (loaded), cdone (updated by the 4 epilogue warps).
+//
+// gemm_tf32_sub_ares_kernel (end of file) is the short-K subtract-update variant whose A row
+// block stays resident in TMEM across a CTA's run of tiles.
 //
 // Operand layouts in shared memory (UMMA canonical 128B-swizzle layouts):
 //   K-major (TN): box {32 k, rows}: row r at r*128 B, 8-row groups at 1024 B (SBO), the k-th
