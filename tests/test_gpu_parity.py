@@ -284,19 +284,25 @@ def test_fresh_context_reproducible_across_growth(qbmod):
 
 
 @pytest.mark.parametrize("q", [0, 1])
-def test_distributed_context_single_rank_bitwise(qbmod, q):
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_distributed_context_single_rank_bitwise(qbmod, q, dt):
     """A column-sharded context (NCCL communicator of one rank) runs the allreduce code path
-    and must reproduce the plain context bit for bit."""
+    and must reproduce the plain context bit for bit.  FP32: the plain context takes Y's FP32
+    copy from the sketch's epilogue, the sharded one converts the all-reduced Y; same values."""
     try:
         uid = qbmod.qb_nccl_unique_id()
     except qbmod.QBError:
         pytest.skip("NCCL not loadable")
     A, _ = make(600, 500, "exp10_25", 9)
-    plain = qbmod.QB(0)
-    g0 = plain.factor(to_dev(A), 1e-8, 32, q, seed=4)
+    f32 = dt == "f32"
+    dtype = qbmod.QB_F32 if f32 else qbmod.QB_F64
+    Ad = torch.from_numpy(np.asfortranarray(A.astype(np.float32))).cuda() if f32 else to_dev(A)
+    eps = 1e-4 if f32 else 1e-8
+    plain = qbmod.QB(0, dtype=dtype)
+    g0 = plain.factor(Ad.clone(), eps, 32, q, seed=4)
     plain.close()
-    d = qbmod.QB(0, dist=dict(rank=0, nranks=1, unique_id=uid, col_offset=0, n_global=500))
-    g1 = d.factor(to_dev(A), 1e-8, 32, q, seed=4)
+    d = qbmod.QB(0, dtype=dtype, dist=dict(rank=0, nranks=1, unique_id=uid, col_offset=0, n_global=500))
+    g1 = d.factor(Ad.clone(), eps, 32, q, seed=4)
     d.close()
     assert g0["k"] == g1["k"]
     assert torch.equal(g0["Q"], g1["Q"]) and torch.equal(g0["B"], g1["B"])
