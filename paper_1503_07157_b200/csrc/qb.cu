@@ -731,7 +731,8 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
 // row_distributed: src holds this rank's rows of a matrix whose rows are spread over the
 // ranks (the power step's Z = A^T Q on column shards); the Gram is summed with NCCL and the
 // replicated T applied to the local rows.
-// single = true (cholqr1 below): the second pass runs only after a SHIFTED first factorization
+// single = true ("cholqr1", reading R11b: the orth of line (3)/(6) when the re-projection and its
+// CholeskyQR2 follow in the same block): the second pass runs only after a SHIFTED first factorization
 // (then the whole shifted CholeskyQR3 runs); otherwise a factorized first pass is final.
 // FP32 contexts: src32 / dst32 (optional) as in cholqr_pass; the FP32 copy of the scratch
 // lives in ctx->X32b, so that no pass reads and writes the same FP32 buffer.
@@ -768,15 +769,6 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
   QB_TRY(cholqr_pass(ctx, dst, ldd, T, ldt, m, w, status_dev(ctx) + 1, row_distributed, dst32, ldd32, T32, ldt));
   QB_TRY(cholqr_pass(ctx, T, ldt, dst, ldd, m, w, status_dev(ctx) + 1, row_distributed, T32, ldt, dst32, ldd32));
   return QB_OK;
-}
-
-// One CholeskyQR pass (reading R11b): used for the orth of line (3)/(6) when the re-projection
-// and its CholeskyQR2 follow in the same block; the orth after the projection restores full
-// orthogonality.  A first pass that needed the shift still runs the whole shifted CholeskyQR3.
-qb_status cholqr1(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
-                  bool row_distributed = false, const float* src32 = nullptr, int64_t lds32 = 0,
-                  float* dst32 = nullptr, int64_t ldd32 = 0) {
-  return cholqr2(ctx, src, lds, dst, ldd, m, w, row_distributed, true, src32, lds32, dst32, ldd32);
 }
 
 // Orthonormalise the m x l column-major panel X (ld ldx) in place for any l: 256 columns at a
