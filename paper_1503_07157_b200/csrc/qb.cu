@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -751,7 +752,8 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
     T32 = static_cast<float*>(ctx->X32b.p);
   }
   const bool inplace = src == dst || (src32 != nullptr && src32 == dst32);
-  QB_CUDA(cudaMemsetAsync(status_dev(ctx) + 1, 0, 2 * sizeof(int), ctx->stream));
+  zero_ints_kernel<<<1, 32, 0, ctx->stream>>>(status_dev(ctx) + 1, 2);
+  QB_TRY(check_launch(ctx, "zero_flags"));
   // second pass only after a factorization (status[2]); a Newton-Schulz first pass is final
   const int* gate2 = status_dev(ctx) + (single ? 1 : 2);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
@@ -794,8 +796,8 @@ qb_status orth_blocked(qb_ctx ctx, double* X, int64_t ldx, int64_t m, int64_t l)
 bool skip_orth_flag(unsigned flags) { return (flags & QB_SKIP_POWER_ORTH) != 0; }
 
 qb_status reset_flags(qb_ctx ctx) {
-  QB_CUDA(cudaMemsetAsync(status_dev(ctx), 0, 8 * sizeof(int), ctx->stream));
-  return QB_OK;
+  zero_ints_kernel<<<1, 32, 0, ctx->stream>>>(status_dev(ctx), 8);
+  return check_launch(ctx, "zero_flags");
 }
 
 // kind 0: FP64 Ω; 1: FP32 Ω (qb_omega on an FP32 context); 2: FP64 buffer holding RN_32(Ω).
@@ -843,6 +845,7 @@ qb_status grow_factors(qb_ctx ctx, int64_t m, int64_t n, int64_t need, int64_t k
                             ctx->stream));
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  if (ctx->copy_stream) QB_CUDA(cudaStreamSynchronize(ctx->copy_stream));  // block copies read the old factors
   if (ctx->dtype == QB_F32) {  // FP32 copy of Q̄ (the published Q and the residual GEMMs' operand)
     DevBuf nq32;
     QB_CUDA(cudaMalloc(&nq32.p, sizeof(float) * (size_t)(ldq * cap)));
@@ -855,7 +858,6 @@ qb_status grow_factors(qb_ctx ctx, int64_t m, int64_t n, int64_t need, int64_t k
     if (ctx->Qbar32.p) QB_CUDA(cudaFree(ctx->Qbar32.p));
     ctx->Qbar32 = nq32;
   }
-  if (ctx->copy_stream) QB_CUDA(cudaStreamSynchronize(ctx->copy_stream));  // block copies read the old factors
   if (ctx->Qbar.p) QB_CUDA(cudaFree(ctx->Qbar.p));
   if (ctx->Bbar.p) QB_CUDA(cudaFree(ctx->Bbar.p));
   ctx->Qbar = nq;
@@ -1624,6 +1626,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   }
   float* Q32 = static_cast<float*>(ctx->Q32.p);
   float* B32 = static_cast<float*>(ctx->B32.p);
+  bool b32_copy_pending = false;  // qb_factor_host: B32 of the last block on its way to the host
 
   // per-CTA partials of the largest reduction (the downdate GEMM grid), sized once up front
   QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)std::max<int64_t>(
@@ -1660,7 +1663,36 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   }
 
   int64_t ell = 0;
+  // qb_factor_host: block [c0, c0 + wc) of Q̄ / B̄ still to be copied to the host
+  struct {
+    int64_t c0 = -1, wc = 0;
+  } pending_copy;
+  auto host_copy = [&]() -> qb_status {
+    if (pending_copy.c0 < 0) return QB_OK;
+    const int64_t c0 = pending_copy.c0, wc = pending_copy.wc;
+    pending_copy.c0 = -1;
+    const size_t es = is_f32 ? 4 : 8;
+    const void* qsrc = is_f32 ? static_cast<const void*>(static_cast<const float*>(ctx->Qbar32.p) + c0 * ctx->ldq)
+                              : static_cast<const void*>(ctx->Qbar.d() + c0 * ctx->ldq);
+    const void* bsrc = is_f32 ? ctx->B32.p : static_cast<const void*>(ctx->Bbar.d() + c0 * ctx->ldb);
+    QB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->hout.Q) + c0 * ctx->hout.ldq * es, ctx->hout.ldq * es, qsrc,
+                              ctx->ldq * es, m * es, wc, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    QB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->hout.B) + c0 * ctx->hout.ldb * es, ctx->hout.ldb * es, bsrc,
+                              ctx->ldb * es, n * es, wc, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    // FP32: B32 is rewritten by the next block's downdate, which waits for this copy first
+    // (by then long done); everything else the copies read is final
+    if (is_f32) {
+      QB_CUDA(cudaEventRecord(ctx->ev_copy, ctx->copy_stream));
+      b32_copy_pending = true;
+    }
+    return QB_OK;
+  };
+  static const int host_timing = debug_env("QB_HOST_TIMING");  // diagnostics: host time per block phase
+  auto now_ms = [] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
   while (ell < kmax_eff) {
+    const double th0 = host_timing ? now_ms() : 0.0;
     const int64_t w = std::min<int64_t>(b, kmax_eff - ell);
     QB_TRY(grow_factors(ctx, m, n, ell + w, kmax_eff));
     QB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -1715,6 +1747,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp, is_f32 ? 1 : 0));
     // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
     QB_TRY(sketch(ctx->Om.p));
+    QB_TRY(host_copy());  // the previous block's Q_i / B_i (qb_factor_host)
     if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));  // Y = sum_p A_p Omega_p (column shards)
     QB_CUDA(cudaEventRecord(ctx->evp[1], ctx->stream));
     // orth of line (3); a single CholeskyQR pass when the re-projection's orth follows (R11b)
@@ -1802,6 +1835,10 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     int64_t na_parts = 0;
     QB_CUDA(cudaEventRecord(ctx->evp[4], ctx->stream));
     if (is_f32) {  // A -= RN32(Q_i) RN32(B_i): the residual of the factors the caller receives
+      if (b32_copy_pending) {  // the previous block's B32 is still being copied to the host
+        QB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
+        b32_copy_pending = false;
+      }
       QB_TRY(launch_convert(ctx, static_cast<const double*>(Bi), ctx->ldb, n, w, B32, ctx->ldb));
       QB_TRY(gemm_tf(ctx, GEMM_NN, TF_SUB_COL, (int)m, (int)n, (int)w, Qi32, ctx->ldq, B32, ctx->ldb, A32, ldA, true,
                      &na_parts));
@@ -1816,7 +1853,17 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    const double th1 = host_timing ? now_ms() : 0.0;
+    double th_ev0 = 0.0;
+    if (host_timing) {  // when did the block's first event complete on the device (host clock)?
+      while (cudaEventQuery(ctx->ev0) == cudaErrorNotReady) {
+      }
+      th_ev0 = now_ms();
+    }
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (host_timing)
+      fprintf(stderr, "[qb host] block at %lld: enqueue %.3f ms, block start +%.3f ms, wait %.3f ms\n", (long long)ell,
+              th1 - th0, th_ev0 - th0, now_ms() - th1);
     if (ctx->h_status[4])
       return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift in the block ending at %lld",
                   (long long)(ell + w));
@@ -1842,23 +1889,16 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     ctx->stats.push_back(st);
     if (ctx->hout.Q && ell - w < ctx->hout.kcap) {
       // the block is final (host-synchronised above): its Q_i columns and B_i rows go to the
-      // host on the copy stream while the next block computes
-      const int64_t c0 = ell - w, wc = std::min(w, ctx->hout.kcap - c0);
-      const size_t es = is_f32 ? 4 : 8;
-      const void* qsrc = is_f32 ? static_cast<const void*>(static_cast<const float*>(ctx->Qbar32.p) + c0 * ctx->ldq)
-                                : static_cast<const void*>(ctx->Qbar.d() + c0 * ctx->ldq);
-      const void* bsrc = is_f32 ? ctx->B32.p : static_cast<const void*>(ctx->Bbar.d() + c0 * ctx->ldb);
-      QB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->hout.Q) + c0 * ctx->hout.ldq * es, ctx->hout.ldq * es, qsrc,
-                                ctx->ldq * es, m * es, wc, cudaMemcpyDeviceToHost, ctx->copy_stream));
-      QB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(ctx->hout.B) + c0 * ctx->hout.ldb * es, ctx->hout.ldb * es, bsrc,
-                                ctx->ldb * es, n * es, wc, cudaMemcpyDeviceToHost, ctx->copy_stream));
-      // FP32: B32 is rewritten by the next block; the main stream waits for this copy first
-      QB_CUDA(cudaEventRecord(ctx->ev_copy, ctx->copy_stream));
-      QB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
+      // host on the copy stream while the next block computes; enqueued once the next block's
+      // sketch is (host_copy below) — enqueued here, ahead of the next block, they held that
+      // block's first operations back for the length of the copy (measured: +1.45 ms per block)
+      pending_copy = {ell - w, std::min(w, ctx->hout.kcap - (ell - w))};
     }
+    if (r2 <= eps2 || !std::isfinite(r2)) QB_TRY(host_copy());
     if (!std::isfinite(r2)) return fail(ctx, QB_ERR_CUDA, "non-finite residual after block ending at %lld", (long long)ell);
     if (r2 <= eps2) break;  // line (11): stop test (R1, R4)
   }
+  QB_TRY(host_copy());  // kmax reached without the stop test firing
   *k_out = ell;
   ctx->last_m = m;
   ctx->last_n = n;

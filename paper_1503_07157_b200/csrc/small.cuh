@@ -123,6 +123,12 @@ __global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in
   }
 }
 
+// p[0..n) = 0 (device flag words).  A kernel rather than cudaMemsetAsync: a memset may queue on
+// a copy engine behind qb_factor_host's block copies to the host and stall the next block.
+__global__ void zero_ints_kernel(int* __restrict__ p, int n) {
+  if (static_cast<int>(threadIdx.x) < n) p[threadIdx.x] = 0;
+}
+
 // out = (double) in and out2 = in, column-major rows x cols (FP32 contexts: an FP32 panel and its
 // FP64 copy for the Gram, R18c).
 __global__ void __launch_bounds__(256) convert_dual_kernel(const float* __restrict__ in, int64_t ldi, int64_t rows,
