@@ -161,6 +161,7 @@ struct qb_ctx_s {
   double* h_scal = nullptr;  // pinned: [0] r2, [1] sum B^2, [2..3] spare
   int* h_status = nullptr;   // pinned
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_gap = nullptr;  // QB_HOST_TIMING: end of the previous block (device gap between blocks)
   cudaEvent_t evp[6] = {};  // phase events: sketch, B, downdate (begin/end)
   std::vector<qb_block_stats> stats;
   int64_t last_m = 0, last_n = 0, last_k = -1;  // the last qb_factor (for rqb_svd); -1: none
@@ -1034,6 +1035,7 @@ void qb_destroy(qb_ctx ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->ev_gap) cudaEventDestroy(ctx->ev_gap);
   for (auto& e : ctx->evp)
     if (e) cudaEventDestroy(e);
   if (ctx->comm) nccl().commDestroy(ctx->comm);
@@ -1696,6 +1698,16 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     const int64_t w = std::min<int64_t>(b, kmax_eff - ell);
     QB_TRY(grow_factors(ctx, m, n, ell + w, kmax_eff));
     QB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    double gap_ms = -1.0;  // QB_HOST_TIMING: device idle between the previous block's end and this start
+    if (host_timing) {
+      if (!ctx->ev_gap) {
+        QB_CUDA(cudaEventCreate(&ctx->ev_gap));
+      } else if (ell > 0) {
+        QB_CUDA(cudaEventSynchronize(ctx->ev0));
+        float g = 0.f;
+        if (cudaEventElapsedTime(&g, ctx->ev_gap, ctx->ev0) == cudaSuccess) gap_ms = g;
+      }
+    }
     QB_TRY(reset_flags(ctx));
     double* Qbar = ctx->Qbar.d();
     double* Qi = Qbar + ell * ctx->ldq;
@@ -1860,10 +1872,11 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       }
       th_ev0 = now_ms();
     }
+    if (host_timing) QB_CUDA(cudaEventRecord(ctx->ev_gap, ctx->stream));  // this block's end on the device
     QB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (host_timing)
-      fprintf(stderr, "[qb host] block at %lld: enqueue %.3f ms, block start +%.3f ms, wait %.3f ms\n", (long long)ell,
-              th1 - th0, th_ev0 - th0, now_ms() - th1);
+      fprintf(stderr, "[qb host] block at %lld: enqueue %.3f ms, block start +%.3f ms, wait %.3f ms, device gap %.3f ms\n",
+              (long long)ell, th1 - th0, th_ev0 - th0, now_ms() - th1, gap_ms);
     if (ctx->h_status[4])
       return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift in the block ending at %lld",
                   (long long)(ell + w));
