@@ -403,6 +403,24 @@ def test_factor_host_entry_point(qbmod, dt):
     c.close()
 
 
+def test_factor_host_kmax_reached(qbmod):
+    """qb_factor_host when kmax ends the loop before the stop test fires (QB_NOT_CONVERGED): the last
+    block's host copy is still issued, and the host factors equal the device entry point's."""
+    A, _ = make(900, 700, "exp10_25", 23)
+    Ah = np.asfortranarray(A)
+    c = qbmod.QB(0)
+    g = c.factor(torch.from_numpy(Ah).cuda(), 1e-12, 32, 0, seed=3, kmax=96)
+    assert g["status"] == qbmod.QB_NOT_CONVERGED and g["k"] == 96
+    Qh = np.full((96, 900), np.nan)
+    Bh = np.full((96, 700), np.nan)
+    r = qbmod.qb_factor_host(c.ctx, Ah.ctypes.data, 900, 700, 900, 1e-12, 32, 0, 3, 96, Qh.ctypes.data, 900,
+                             Bh.ctypes.data, 700, 96)
+    assert r["status"] == qbmod.QB_NOT_CONVERGED and r["k"] == 96
+    assert np.array_equal(Qh.T, g["Q"].cpu().numpy())
+    assert np.array_equal(Bh, g["B"].cpu().numpy())
+    c.close()
+
+
 def test_orth_fp32_context(qbmod):
     """qb_orth on an FP32 context: FP64 CholeskyQR2 of the widened panel, rounded to FP32."""
     X = np.random.default_rng(4).standard_normal((3000, 100)).astype(np.float32)
