@@ -1604,8 +1604,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   if (!inplace_ok) {
     ldA = round_up(m, 16);
     QB_TRY(ensure(ctx, ctx->Awork, es * (size_t)(ldA * n)));
-    QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * es, Ain, lda * es, m * es, n, cudaMemcpyDeviceToDevice, ctx->stream));
-    Av = ctx->Awork.p;
+    Av = ctx->Awork.p;  // filled by a0's pass below
   }
   double* A = static_cast<double*>(Av);  // FP64 contexts
   float* A32 = static_cast<float*>(Av);  // FP32 contexts
@@ -1634,14 +1633,23 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)std::max<int64_t>(
                                      ((m + GEMM_BM - 1) / GEMM_BM) * ((n + kBN - 1) / kBN), 16 * ctx->num_sms)));
 
-  // ---- a0: r0^2 = ||A||_F^2; trivial exit (Algorithm 1 line (2), reading R3)
+  // ---- a0: r0^2 = ||A||_F^2; trivial exit (Algorithm 1 line (2), reading R3); fused with the
+  // working copy when A is not factored in place (one pass over A instead of two)
   {
     const int grid = (int)std::min<int64_t>(n, 8 * ctx->num_sms);
     QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
-    if (is_f32)
+    if (!inplace_ok) {
+      if (is_f32)
+        copy_sumsq_kernel<float><<<grid, RED_THREADS, 0, ctx->stream>>>(static_cast<const float*>(Ain), lda, m, n, A32,
+                                                                         ldA, ctx->parts.d());
+      else
+        copy_sumsq_kernel<double><<<grid, RED_THREADS, 0, ctx->stream>>>(static_cast<const double*>(Ain), lda, m, n, A,
+                                                                          ldA, ctx->parts.d());
+    } else if (is_f32) {
       sumsq_kernel<float><<<grid, RED_THREADS, 0, ctx->stream>>>(A32, m, n, ldA, ctx->parts.d());
-    else
+    } else {
       sumsq_kernel<double><<<grid, RED_THREADS, 0, ctx->stream>>>(A, m, n, ldA, ctx->parts.d());
+    }
     QB_TRY(check_launch(ctx, "sumsq"));
     QB_TRY(reduce_to_scal(ctx, grid, 0));
     QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 1));  // ||A||_F^2 over the column shards

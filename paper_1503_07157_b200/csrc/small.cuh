@@ -1,5 +1,6 @@
 // Small and bandwidth-bound kernels of the QB path:
 //   sumsq_kernel       a0: partial sums of squares of A (||A||_F^2)
+//   copy_sumsq_kernel  the same fused with the working copy of A
 //   reduce_kernel      K8: fixed-order sum of per-CTA partials -> one FP64 scalar
 //   splitk_reduce      fixed-order sum of split-K partials (+ sum of squares, the EI term)
 //   transpose_kernel   column-major <-> row-major copy of a tall-skinny panel
@@ -88,6 +89,34 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
       for (int w = 0; w < RED_THREADS / 32; ++w) t += red[w];
       sq_partials[blockIdx.x] = t;
     }
+  }
+}
+
+// a0 fused with the working copy (qb_factor without QB_OVERWRITE_A): dst = src column by column
+// and the same per-block sums of squares as sumsq_kernel, in the same order (bitwise equal r0^2).
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS) copy_sumsq_kernel(const T* __restrict__ src, int64_t lds, int64_t m,
+                                                                 int64_t n, T* __restrict__ dst, int64_t ldd,
+                                                                 double* __restrict__ partials) {
+  __shared__ double red[RED_THREADS / 32];
+  double s = 0.0;
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const T* col = src + j * lds;
+    T* out = dst + j * ldd;
+    for (int64_t i = threadIdx.x; i < m; i += RED_THREADS) {
+      const T x = col[i];
+      out[i] = x;
+      const double v = static_cast<double>(x);
+      s = fma(v, v, s);
+    }
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < RED_THREADS / 32; ++w) t += red[w];
+    partials[blockIdx.x] = t;
   }
 }
 
