@@ -1459,7 +1459,17 @@ qb_status qb_fixed_rank(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda
   if (!aligned || (resid_out && !(flags & QB_OVERWRITE_A))) {
     ldA = round_up(m, 16);
     QB_TRY(ensure(ctx, ctx->Awork, es * (size_t)(ldA * n)));
-    QB_CUDA(cudaMemcpy2DAsync(ctx->Awork.p, ldA * es, Ain, lda * es, m * es, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    // an SM copy (the copy engine's device-to-device copy is slower); its sums of squares are unused
+    const int grid = (int)std::min<int64_t>(n, 8 * ctx->num_sms);
+    QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
+    if (is_f32)
+      copy_sumsq_kernel<float><<<grid, RED_THREADS, 0, ctx->stream>>>(static_cast<const float*>(Ain), lda, m, n,
+                                                                       static_cast<float*>(ctx->Awork.p), ldA,
+                                                                       ctx->parts.d());
+    else
+      copy_sumsq_kernel<double><<<grid, RED_THREADS, 0, ctx->stream>>>(static_cast<const double*>(Ain), lda, m, n,
+                                                                        ctx->Awork.d(), ldA, ctx->parts.d());
+    QB_TRY(check_launch(ctx, "copy"));
     Av = ctx->Awork.p;
   }
   double* A = static_cast<double*>(Av);
