@@ -1371,15 +1371,20 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
       QB_TRY(check_launch(ctx, "qrcp_renorm"));
     }
   } else {  // one-step lookahead: the trailing block is read and written once per step
-    QB_TRY(ensure(ctx, ctx->qw, sizeof(double) * (size_t)(n + 2 * l + 64)));
+    const int64_t nblk = (n + QRCP_THREADS - 1) / QRCP_THREADS + 8;
+    QB_TRY(ensure(ctx, ctx->qw, sizeof(double) * (size_t)(n + 2 * l + 64 + 2 * nblk)));
     double* wprev = ctx->qw.d();
     double* vbs[2] = {vb, wprev + n};  // v_i alternates between two buffers (v_{i-1} still needed)
+    // per-block (max partial norm, first index) of step i's updated norms: step i+1's pivot search
+    double* pmax = wprev + n + 2 * l + 64;
+    int* pidx = reinterpret_cast<int*>(pmax + nblk);
     QB_CUDA(cudaMemsetAsync(wprev, 0, sizeof(double) * (size_t)n, ctx->stream));
     for (int i = 0; i < (int)l; ++i) {
       double* vcur = vbs[i & 1];
       const double* vprev = vbs[(i + 1) & 1];
+      const int npart = i > 0 && n - i > 0 ? (int)((n - i + QRCP_THREADS - 1) / QRCP_THREADS) : 0;
       qrcp_la_pivot_kernel<<<1, 1024, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2, perm, tau, vprev, wprev,
-                                                         vcur);
+                                                         vcur, pmax, pidx, npart);
       QB_TRY(check_launch(ctx, "qrcp_la_pivot"));
       if (i + 1 >= n) continue;
       const int ncol = (int)(n - i - 1);
@@ -1389,7 +1394,7 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
                                                                 parts, ldp);
       QB_TRY(check_launch(ctx, "qrcp_la_fw"));
       qrcp_la_row_kernel<<<grid.x, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, tau, vcur, parts, ldp,
-                                                                   rch, wprev, vn1, vn2, tol3z);
+                                                                   rch, wprev, vn1, vn2, tol3z, pmax, pidx);
       QB_TRY(check_launch(ctx, "qrcp_la_row"));
     }
     // the last deferred update reaches rows below l only: nothing left to apply

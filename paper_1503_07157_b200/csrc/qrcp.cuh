@@ -297,7 +297,9 @@ __global__ void __launch_bounds__(1024) qrcp_la_pivot_kernel(double* __restrict_
                                                              double* __restrict__ vn1, double* __restrict__ vn2,
                                                              int* __restrict__ perm, double* __restrict__ tau,
                                                              const double* __restrict__ vprev, double* __restrict__ wprev,
-                                                             double* __restrict__ vbuf) {
+                                                             double* __restrict__ vbuf,
+                                                             const double* __restrict__ pmax,
+                                                             const int* __restrict__ pidx, int npart) {
   __shared__ double s_val[32];
   __shared__ int s_idx[32];
   __shared__ int s_p;
@@ -306,11 +308,22 @@ __global__ void __launch_bounds__(1024) qrcp_la_pivot_kernel(double* __restrict_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double best = -1.0;
   int bi = n;
-  for (int j = i + tid; j < n; j += blockDim.x) {
-    const double v = vn1[j];
-    if (v > best) {
-      best = v;
-      bi = j;
+  if (npart > 0) {
+    // the previous step's qrcp_la_row left one (max, first index) per block of columns > i - 1
+    for (int c = tid; c < npart; c += blockDim.x) {
+      const double v = pmax[c];
+      if (v > best || (v == best && pidx[c] < bi)) {
+        best = v;
+        bi = pidx[c];
+      }
+    }
+  } else {
+    for (int j = i + tid; j < n; j += blockDim.x) {
+      const double v = vn1[j];
+      if (v > best) {
+        best = v;
+        bi = j;
+      }
     }
   }
 #pragma unroll
@@ -463,32 +476,67 @@ __global__ void __launch_bounds__(QRCP_THREADS) qrcp_la_row_kernel(double* __res
                                                                  const double* __restrict__ partials, int64_t ldp,
                                                                  int nchunks, double* __restrict__ wprev,
                                                                  double* __restrict__ vn1, double* __restrict__ vn2,
-                                                                 double tol3z) {
+                                                                 double tol3z, double* __restrict__ pmax,
+                                                                 int* __restrict__ pidx) {
+  __shared__ double s_val[QRCP_THREADS / 32];
+  __shared__ int s_idx[QRCP_THREADS / 32];
   const int j = i + 1 + blockIdx.x * QRCP_THREADS + threadIdx.x;
-  if (j >= n) return;
-  double w = 0.0;
-  for (int c = 0; c < nchunks; ++c) w += partials[c * ldp + j];
-  wprev[j] = w;
-  const double tw = tau[i] * w;
-  double* bij = B + static_cast<int64_t>(i) * ldb + j;
-  const double rij = *bij - tw;
-  *bij = rij;
-  const double n1 = vn1[j];
-  if (n1 != 0.0) {
-    double temp = fabs(rij) / n1;
-    temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
-    const double ratio = n1 / vn2[j];
-    if (temp * ratio * ratio <= tol3z) {
-      double s = 0.0;
-      for (int r = i + 1; r < l; ++r) {
-        const double a = fma(-vcur[r - i], tw, B[static_cast<int64_t>(r) * ldb + j]);
-        s = fma(a, a, s);
+  double best = -1.0;  // this column's new partial norm, for the next step's pivot search
+  int bi = n;
+  if (j < n) {
+    double w = 0.0;
+    for (int c = 0; c < nchunks; ++c) w += partials[c * ldp + j];
+    wprev[j] = w;
+    const double tw = tau[i] * w;
+    double* bij = B + static_cast<int64_t>(i) * ldb + j;
+    const double rij = *bij - tw;
+    *bij = rij;
+    double n1 = vn1[j];
+    if (n1 != 0.0) {
+      double temp = fabs(rij) / n1;
+      temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+      const double ratio = n1 / vn2[j];
+      if (temp * ratio * ratio <= tol3z) {
+        double s = 0.0;
+        for (int r = i + 1; r < l; ++r) {
+          const double a = fma(-vcur[r - i], tw, B[static_cast<int64_t>(r) * ldb + j]);
+          s = fma(a, a, s);
+        }
+        n1 = sqrt(s);
+        vn2[j] = n1;
+      } else {
+        n1 = n1 * sqrt(temp);
       }
-      vn1[j] = sqrt(s);
-      vn2[j] = vn1[j];
-    } else {
-      vn1[j] = n1 * sqrt(temp);
+      vn1[j] = n1;
     }
+    best = n1;
+    bi = j;
+  }
+  if (pmax == nullptr) return;
+  // (max, first index) over this block's columns
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_val[warp] = best;
+    s_idx[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < QRCP_THREADS / 32; ++w2)
+      if (s_val[w2] > best || (s_val[w2] == best && s_idx[w2] < bi)) {
+        best = s_val[w2];
+        bi = s_idx[w2];
+      }
+    pmax[blockIdx.x] = best;
+    pidx[blockIdx.x] = bi;
   }
 }
 
