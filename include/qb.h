@@ -124,6 +124,8 @@ qb_status qb_nccl_unique_id(void* out128);
  *          every rank).  *B: device, ROW-major k x n (row i = B(i, :)), leading dimension
  *          *ldb (context-owned; the local column shard on a distributed context).  Both stay
  *          valid until the next qb_factor or qb_destroy.
+ * Empty A (m = 0 or n = 0, single-rank context; A may be NULL, lda >= max(m, 1)): ||A||_F = 0
+ * <= eps, so QB_OK with k = 0, *resid = 0 and NULL Q / B (reading R3).
  * Returns QB_OK, QB_NOT_CONVERGED (outputs valid), or an error.                           */
 qb_status qb_factor(qb_ctx ctx, void* A, int64_t m, int64_t n, int64_t lda, double eps,
                     int64_t b, int q, uint64_t seed, int64_t kmax, unsigned flags,

@@ -312,9 +312,9 @@ class QB:
 
     def factor(self, A, eps, b, q=0, seed=1, kmax=0, overwrite=False, copy_out=True, flags=0):
         import torch
-        assert A.is_cuda and A.dtype in (torch.float64, torch.float32) and A.dim() == 2 and A.stride(0) == 1
+        assert A.is_cuda and A.dtype in (torch.float64, torch.float32) and A.dim() == 2 and (A.stride(0) == 1 or A.numel() == 0)
         m, n = A.shape
-        r = qb_factor(self.ctx, A.data_ptr(), m, n, A.stride(1) if n > 1 else m, eps, b, q, seed, kmax,
+        r = qb_factor(self.ctx, A.data_ptr(), m, n, max(A.stride(1) if n > 1 else m, 1), eps, b, q, seed, kmax,
                       (QB_OVERWRITE_A if overwrite else 0) | flags)
         k = r["k"]
         ts = "<f8" if A.dtype == torch.float64 else "<f4"

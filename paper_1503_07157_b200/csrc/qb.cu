@@ -1592,6 +1592,24 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   if (!k_out) return fail(ctx, QB_ERR_INVALID_ARG, "k must not be NULL");
   *k_out = 0;
   const bool is_f32 = ctx->dtype == QB_F32;
+  // empty A (m = 0 or n = 0, single-rank contexts): ||A||_F = 0 <= eps, so k = 0 (reading R3,
+  // Algorithm 1 line (2)); A may be NULL.  Arguments b, q, eps are still validated.
+  if (m >= 0 && n >= 0 && (m == 0 || n == 0) && ctx->nranks <= 1 && lda >= std::max<int64_t>(m, 1)) {
+    if (b < 1 || b > kMaxB) return fail(ctx, QB_ERR_INVALID_ARG, "block size b=%lld outside [1, %lld]", (long long)b, (long long)kMaxB);
+    if (q < 0) return fail(ctx, QB_ERR_INVALID_ARG, "q=%d < 0", q);
+    if (!(eps >= 0.0)) return fail(ctx, QB_ERR_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
+    ctx->outQ = nullptr;
+    ctx->outB = nullptr;
+    ctx->last_m = m;
+    ctx->last_n = n;
+    ctx->last_k = 0;
+    if (resid_out) *resid_out = 0.0;
+    if (Q_out) *Q_out = nullptr;
+    if (ldq_out) *ldq_out = round_up(std::max<int64_t>(m, 1), 16);
+    if (B_out) *B_out = nullptr;
+    if (ldb_out) *ldb_out = round_up(std::max<int64_t>(n, 1), 16);
+    return QB_OK;
+  }
   if (!Ain || m < 1 || n < 1 || lda < m || m > INT32_MAX || n > INT32_MAX)
     return fail(ctx, QB_ERR_INVALID_ARG, "bad matrix arguments (m=%lld n=%lld lda=%lld)", (long long)m, (long long)n,
                 (long long)lda);

@@ -163,6 +163,26 @@ def test_degenerate_inputs(qbmod, ctx):
     assert g["k"] == 40 and g["resid"] < 1e-9
 
 
+def test_empty_inputs(qbmod, ctx):
+    """m = 0 or n = 0: k = 0 like the oracle (reading R3); b, q, eps are still validated, and
+    rqb_svd / qb_pivoted_qr of the empty factorization return empty factors."""
+    for shape in ((0, 7), (7, 0), (0, 0)):
+        A = torch.zeros(shape, dtype=torch.float64, device="cuda")
+        o = oqb.randqb_pb(np.zeros(shape), 0.0, 4)
+        g = ctx.factor(A, 0.0, 4)
+        assert (g["status"], g["k"]) == (o.status, o.k) == (0, 0)
+        assert tuple(g["Q"].shape) == (shape[0], 0) and tuple(g["B"].shape) == (0, shape[1])
+        assert g["resid"] == 0.0
+        sv = ctx.svd()
+        assert tuple(sv["U"].shape) == (shape[0], 0) and tuple(sv["V"].shape) == (shape[1], 0)
+        pq = ctx.pivoted_qr()
+        assert list(pq["perm"]) == list(range(shape[1])) and tuple(pq["R"].shape) == (0, shape[1])
+        with pytest.raises(qbmod.QBError):
+            ctx.factor(A, 1e-3, 0)
+        with pytest.raises(qbmod.QBError):
+            ctx.factor(A, -1.0, 4)
+
+
 def test_rank_exhaustion_inside_block(qbmod, ctx):
     rng = np.random.default_rng(2)
     A = rng.standard_normal((120, 25)) @ rng.standard_normal((25, 90))

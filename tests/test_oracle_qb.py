@@ -213,6 +213,14 @@ def test_degenerate_inputs():
     assert r.k == 10 and r.resid < 1e-10
 
 
+def test_empty_inputs():
+    """m = 0 or n = 0: ||A||_F = 0 <= eps for every eps >= 0, so k = 0 (reading R3)."""
+    for shape in ((0, 7), (7, 0), (0, 0)):
+        r = qb.randqb_pb(np.zeros(shape), 0.0, 4)
+        assert (r.status, r.k) == (qb.QB_OK, 0)
+        assert r.Q.shape == (shape[0], 0) and r.B.shape == (0, shape[1])
+
+
 def test_rank_exhaustion_inside_a_block():
     """Exact rank 25 with b = 10: the third block's sketch has rank 5; orth (Householder)
     still returns an orthonormal block and the residual reaches round-off (reading R8)."""
