@@ -11,12 +11,17 @@ point with the H2D copy of A and the D2H copy of Q, B inside the timed region (`
 The metric is BASELINE.json's: FP64 GFLOP/s of the algorithmic work F_alg (DESIGN.md §8,
 PAPER.md:902 cost model with C_mm = 2) and seconds-to-eps, as a fraction of the FP64 peak.
 
-Multi-GPU (torchrun, N > 1): the column-sharded path — every rank owns a
-column block of A, Y_i and the norm scalars are summed with NCCL, orth is replicated, B_i and
-the downdate stay local.  Default "weak" scaling: every rank holds a 20000 x 20000 block of
-the 20000 x 20000N matrix with the T spectrum (synth.make_shard_torch), so per-GPU work is
-fixed; ``--strong`` shards the one 20000 x 20000 T matrix instead.  The time is the max over
-ranks; ``value`` is the algorithmic work of the whole (global) factorization per second.
+Multi-GPU (N > 1): one process per GPU over NCCL.  Under torchrun the ranks
+come from the environment; ``--gpus N`` without torchrun relaunches itself under
+torch.distributed.run, and fails loudly when fewer than N GPUs are visible.  Default is
+STRONG scaling: one matrix is sharded (columns for square A, rows for tall-skinny A, NEXT-2),
+so the N = 1 point is the single-GPU measurement; ``--weak`` gives every rank its own
+20000 x 20000 block of a 20000 x 20000N matrix instead.  The time is the max over ranks;
+``value`` is the algorithmic work of the whole factorization per second.
+
+Beside the main workload the line carries ``configs``: one record per other BASELINE config
+(C1, C2, C3, C4 FP32, C5 and T1 = T with q = 1 at N = 1; the sharded C3, C4, C5, T1 at N > 1),
+each timed the same way (device-resident A, CUDA events, W warm-up steps, max over ranks).
 """
 import argparse
 import json
@@ -179,91 +184,207 @@ def run_reference(args, cfg):
     return 0
 
 
-def run_ours(args, cfg):
-    import numpy as np
+def tf32x3_peak():
+    """3xTF32 tensor ceiling for the FP32 path: the measured dense BF16 rate x the nominal
+    TF32/BF16 ratio (1/2), / 3 MMAs per FP32-equivalent product."""
+    try:
+        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        return bf16 / 2 / 3, "MEASURED_PEAKS.json bf16 x 1/2 (TF32) / 3 (3xTF32)"
+    except Exception:
+        return 2250.0 / 2 / 3, "nominal 2.25 PF bf16 x 1/2 / 3"
+
+
+def bytes_alg(m, n, k, b, q, s, es):
+    """Algorithmic HBM bytes: (3+2q) passes over A per block + the re-projection's
+    reads of Q̄ (sum_i 2 m ell_{i-1} es)."""
+    ells = [min(i * b, k) for i in range(s)]
+    return s * (3 + 2 * q) * m * n * es + sum(2 * m * l * es for l in ells)
+
+
+def shard_inputs(cfg, ws, rank, local, weak, shard):
+    """This rank's block of the workload's A (device-resident, column-major) and its descriptor.
+    rows: tall-skinny A sharded by rows (NEXT-2), else columns.  Strong scaling (default) slices
+    one matrix; weak scaling builds an m x n block of an (m x nP) or (mP x n) matrix with the
+    same spectrum (synth.make_shard_torch / make_row_shard_torch)."""
+    import torch
+    import synth
+    sig = synth.config_sigma(cfg)
+    tdt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    dev = torch.device(f"cuda:{local}")
+    rows = (shard == "rows") or (shard == "auto" and cfg.m >= 8 * cfg.n)
+    out = dict(rows=rows, dspec=None, m_global=cfg.m, n_global=cfg.n, m_local=cfg.m, n_local=cfg.n)
+    if ws == 1:
+        out["A0"] = make_A(cfg, dev)
+        return out
+    from paper_1503_07157_b200.dist import dist_spec, dist_spec_rows
+    if rows:
+        out["m_global"] = cfg.m * ws if weak else cfg.m
+        d = dist_spec_rows(out["m_global"])
+        if weak:
+            d["row_offset"], d["m_local"] = rank * cfg.m, cfg.m
+            out["A0"] = synth.make_row_shard_torch(cfg.m, cfg.n, sig, cfg.seed_matrix, rank, ws, device=dev, dtype=tdt)
+        else:
+            Af = make_A(cfg, dev)
+            off, ml = d["row_offset"], d["m_local"]
+            out["A0"] = Af[off:off + ml].t().contiguous().t()
+            del Af
+        out["m_local"] = d["m_local"]
+    else:
+        out["n_global"] = cfg.n * ws if weak else cfg.n
+        d = dist_spec(out["n_global"])
+        if weak:
+            d["col_offset"], d["n_local"] = rank * cfg.n, cfg.n
+            out["A0"] = synth.make_shard_torch(cfg.m, cfg.n, sig, cfg.seed_matrix, rank, ws, device=dev, dtype=tdt)
+        else:
+            Af = make_A(cfg, dev)
+            off, nl = d["col_offset"], d["n_local"]
+            out["A0"] = Af.t()[off:off + nl].contiguous().t()
+            del Af
+        out["n_local"] = d["n_local"]
+    out["dspec"] = d
+    torch.cuda.synchronize()
+    return out
+
+
+def timed_steps(step, steps, warmup, stream, ws, dev, flush=None):
+    """W untimed warm-up steps, then K steps timed with CUDA events on the library's stream,
+    bracketed by a barrier + synchronize; max over ranks.  flush: an L2 flush run between
+    timed steps outside the events (inputs smaller than L2)."""
     import torch
     import torch.distributed as dist
-    import paper_1503_07157_b200 as qbp
-    import synth
-
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dspec = None
-    sig = synth.config_sigma(cfg)
-    f32 = cfg.dtype == "f32"
-    tdt = torch.float32 if f32 else torch.float64
-    es = 4 if f32 else 8
-    # tall-skinny workloads shard rows (NEXT-2), square ones columns; --shard overrides
-    rows = (args.shard == "rows") or (args.shard == "auto" and cfg.m >= 8 * cfg.n)
-    m_global, m_local = cfg.m, cfg.m
-    if ws > 1:
-        from paper_1503_07157_b200.dist import dist_spec, dist_spec_rows
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        if rows:
-            m_global = cfg.m if args.strong else cfg.m * ws
-            dspec = dist_spec_rows(m_global)
-        else:
-            n_global = cfg.n if args.strong else cfg.n * ws
-            dspec = dist_spec(n_global)
-    dev = torch.device(f"cuda:{local}")
-    stream = torch.cuda.current_stream(dev)
-    if dspec is None:
-        A0 = make_A(cfg, dev)
-        n_global, n_local = cfg.n, cfg.n
-    elif rows:
-        n_global, n_local = cfg.n, cfg.n
-        if args.strong:
-            Af = make_A(cfg, dev)
-            off, m_local = dspec["row_offset"], dspec["m_local"]
-            A0 = Af[off:off + m_local].t().contiguous().t()
-            del Af
-        else:
-            m_local = cfg.m
-            dspec["row_offset"], dspec["m_local"] = rank * m_local, m_local
-            A0 = synth.make_row_shard_torch(m_local, cfg.n, sig, cfg.seed_matrix, rank, ws, device=dev, dtype=tdt)
-    elif args.strong:
-        Af = make_A(cfg, dev)
-        off, n_local = dspec["col_offset"], dspec["n_local"]
-        A0 = Af.t()[off:off + n_local].contiguous().t()
-        del Af
-        n_global = cfg.n
-    else:
-        n_local = cfg.n
-        n_global = cfg.n * ws
-        dspec["col_offset"], dspec["n_local"] = rank * n_local, n_local
-        A0 = synth.make_shard_torch(cfg.m, n_local, sig, cfg.seed_matrix, rank, ws, device=dev, dtype=tdt)
-    torch.cuda.synchronize()
-    ctx = qbp.QB(local, dtype=qbp.QB_F32 if f32 else qbp.QB_F64, stream=ctypes_stream(stream), dist=dspec)
-    m, b, q = m_local, cfg.b, cfg.q
-
-    def step():
-        return ctx.factor(A0, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=False)
-
     g = None
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         g = step()
     torch.cuda.synchronize()
-    clocks = Clocks(local)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
-    l0 = ctx.launches()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        g = step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    launches = ctx.launches() - l0
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
+    total = 0.0
+    if flush is None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            g = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total = e0.elapsed_time(e1)
+    else:
+        for _ in range(steps):
+            flush()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            total += e0.elapsed_time(e1)
+    ms = total / steps
     if ws > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
+    return ms, g
+
+
+RECORD_STEPS = {"C1": 20, "C2": 20, "C3": 5, "C4": 5, "C5": 2, "T1": 3, "T": 5}
+
+
+def run_record(name, args, ws, rank, local):
+    """One BASELINE config timed like the main workload (device-resident A, CUDA events,
+    >= 3 warm-up steps, max over ranks), strong-sharded over the N ranks."""
+    import torch
+    import paper_1503_07157_b200 as qbp
+    import synth
+    cfg = synth.CONFIGS[name]
+    f32 = cfg.dtype == "f32"
+    es = 4 if f32 else 8
+    inp = shard_inputs(cfg, ws, rank, local, False, args.shard)
+    dev = torch.device(f"cuda:{local}")
+    stream = torch.cuda.current_stream(dev)
+    ctx = qbp.QB(local, dtype=qbp.QB_F32 if f32 else qbp.QB_F64, stream=ctypes_stream(stream), dist=inp["dspec"])
+    A0 = inp["A0"]
+    flush = None
+    l2_note = f"inputs larger than L2 (A is {A0.numel() * es / 1e9:.2f} GB per GPU)"
+    if A0.numel() * es < 512e6:   # A not far above the 126 MB L2: flush it between timed steps
+        junk = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)
+        flush = lambda: junk.fill_(1.0)  # noqa: E731
+        l2_note = "L2 flushed between timed steps (256 MB write)"
+    steps = RECORD_STEPS.get(name, 3)
+    ms, g = timed_steps(lambda: ctx.factor(A0, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=False),
+                        steps, max(3, args.warmup if name in ("C1", "C2") else 3), stream, ws, dev, flush)
+    k, st = g["k"], g["stats"]
+    F = falg(inp["m_global"], inp["n_global"], k, cfg.b, cfg.q, len(st))
+    rec = {"ms_per_step": ms, "value": F / (ms * 1e-3) * 1e-9, "unit": "GFLOP/s", "seconds_to_eps": ms * 1e-3,
+           "k": k, "blocks": len(st), "status": g["status"], "m": inp["m_global"], "n": inp["n_global"],
+           "b": cfg.b, "q": cfg.q, "eps": cfg.eps, "dtype": cfg.dtype, "steps": steps, "warmup": 3, "n_gpus": ws,
+           "sharding": "single" if ws == 1 else ("rows" if inp["rows"] else "cols"), "l2": l2_note}
+    if f32:
+        tf, tf_src = tf32x3_peak()
+        hbm, _ = hbm_peak()
+        t_flop = F / (tf * 1e12)
+        t_hbm = bytes_alg(inp["m_global"], inp["n_global"], k, cfg.b, cfg.q, len(st), es) / (hbm * 1e9)
+        rec["roofline"] = {"bound": "tensor" if t_flop >= t_hbm else "hbm", "t_roof_ms": max(t_flop, t_hbm) * 1e3 / ws,
+                           "t_flop_ms": t_flop * 1e3 / ws, "t_hbm_ms": t_hbm * 1e3 / ws,
+                           "frac": max(t_flop, t_hbm) * 1e3 / ws / ms, "peak_3xtf32_tflops": tf, "peak_source": tf_src}
+    else:
+        peak, _, _ = fp64_peak()
+        rec["frac_fp64_peak"] = rec["value"] / ws / (peak * 1e3)
+    ctx.close()
+    del A0, inp
+    torch.cuda.empty_cache()
+    return rec
+
+
+def latest_profile(pattern_key, names):
+    """The newest committed ncu summary among `names` (profiles/) carrying `pattern_key`."""
+    for nm in names:
+        pth = os.path.join(ROOT, "profiles", nm)
+        if os.path.exists(pth):
+            try:
+                d = json.load(open(pth))
+                if d.get(pattern_key) is not None:
+                    return d[pattern_key], nm
+            except Exception:
+                pass
+    return None, None
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1503_07157_b200 as qbp
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    f32 = cfg.dtype == "f32"
+    tdt = torch.float32 if f32 else torch.float64
+    es = 4 if f32 else 8
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    weak = ws > 1 and args.weak
+    inp = shard_inputs(cfg, ws, rank, local, weak, args.shard)
+    A0, dspec, rows = inp["A0"], inp["dspec"], inp["rows"]
+    m_global, n_global, m, n_local = inp["m_global"], inp["n_global"], inp["m_local"], inp["n_local"]
+    dev = torch.device(f"cuda:{local}")
+    stream = torch.cuda.current_stream(dev)
+    ctx = qbp.QB(local, dtype=qbp.QB_F32 if f32 else qbp.QB_F64, stream=ctypes_stream(stream), dist=dspec)
+    b, q = cfg.b, cfg.q
+
+    def step():
+        return ctx.factor(A0, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = ctx.launches()
+    ms, g = timed_steps(step, args.steps, 0, stream, ws, dev)
+    launches = ctx.launches() - l0
+    clk = clocks.stop()
     k, stats = g["k"], g["stats"]
     F = falg(m_global, n_global, k, b, q, len(stats))
     value = F / (ms * 1e-3) * 1e-9
@@ -274,31 +395,25 @@ def run_ours(args, cfg):
     t_down = statistics.mean(s["ms_down"] for s in full) * 1e-3
     if not f32:
         achieved = 2.0 * m * n_local * b / t_down * 1e-12
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_summary_r01d.json")
-        if os.path.exists(prof):
-            try:
-                traffic = json.load(open(prof)).get("downdate_dram_bytes_per_launch")
-            except Exception:
-                traffic = None
+        traffic, tsrc = latest_profile("downdate_dram_bytes_per_launch",
+                                       ["ncu_summary_r02_down64.json", "ncu_summary_r01k_down64.json"])
+        alg_bytes = 2.0 * m * n_local * 8
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic,
+                    "traffic_over_algorithmic_bytes": (traffic / alg_bytes) if traffic else None,
+                    "traffic_source": tsrc,
                     "kernel": "gemm_f64_kernel<NN,64,SUB_COL> (A -= Q_i B_i, fused ||A||_F^2)",
                     "peak_source": peak_src,
-                    "algorithmic_per_launch": f"2*m*n_local*b = {2.0 * m * n_local * b:.4g} flop",
+                    "algorithmic_per_launch": f"2*m*n_local*b = {2.0 * m * n_local * b:.4g} flop "
+                                              f"(A read + write = {alg_bytes:.4g} bytes)",
                     "share_of_step": sum(s["ms_down"] for s in stats) / ms}
     else:  # FP32: the 3xTF32 subtract-update streams A in and out of HBM (K = b is short)
         hbm, hbm_src = hbm_peak()
         achieved = 2.0 * m * n_local * 4 / t_down * 1e-9
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_summary_r01h_tf32.json")
-        if os.path.exists(prof):
-            try:
-                traffic = json.load(open(prof)).get("downdate_dram_bytes_per_launch")
-            except Exception:
-                traffic = None
+        traffic, tsrc = latest_profile("downdate_dram_bytes_per_launch", ["ncu_summary_r01h_tf32.json"])
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": traffic,
+                    "traffic": traffic, "traffic_source": tsrc,
+                    "traffic_over_algorithmic_bytes": (traffic / (2.0 * m * n_local * 4)) if traffic else None,
                     "kernel": "gemm_tf32_sub_ares_kernel<128> (A -= Q_i B_i, 3xTF32, A rows resident in TMEM, "
                               "fused ||A||_F^2)",
                     "peak_source": hbm_src,
@@ -313,25 +428,15 @@ def run_ours(args, cfg):
         kcap = k + b
         Q_h = torch.empty((kcap, m), dtype=tdt, pin_memory=True)
         B_h = torch.empty((kcap, n_local), dtype=tdt, pin_memory=True)
-        res = qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n_local, m, cfg.eps, b, q, cfg.seed_omega, 0,
-                                 Q_h.data_ptr(), m, B_h.data_ptr(), n_local, kcap)
-        torch.cuda.synchronize()
+
+        def estep():
+            return qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n_local, m, cfg.eps, b, q, cfg.seed_omega, 0,
+                                      Q_h.data_ptr(), m, B_h.data_ptr(), n_local, kcap)
         esteps = max(1, min(args.steps, 3))
-        if ws > 1:
-            dist.barrier()
         t0 = time.perf_counter()
-        e0.record(stream)
-        for _ in range(esteps):
-            res = qbp.qb_factor_host(ctx.ctx, A_h.data_ptr(), m, n_local, m, cfg.eps, b, q, cfg.seed_omega, 0,
-                                     Q_h.data_ptr(), m, B_h.data_ptr(), n_local, kcap)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        wall = (time.perf_counter() - t0) / esteps * 1e3
-        ems = max(e0.elapsed_time(e1) / esteps, wall)
-        if ws > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems, res = timed_steps(estep, esteps, 1, stream, ws, dev)
+        wall = (time.perf_counter() - t0) / (esteps + 1) * 1e3
+        ems = max(ems, wall if ws == 1 else 0.0)
         ke = res["k"]
         e2e = {"value": falg(m_global, n_global, ke, b, q, -(-ke // b)) / (ems * 1e-3) * 1e-9, "unit": "GFLOP/s",
                "ms_per_step": ems, "h2d_bytes_per_step": ws * m * n_local * es,
@@ -344,6 +449,7 @@ def run_ours(args, cfg):
     # fixed-rank randQB at l = k (one wide GEMM per product instead of s narrow ones)
     post = None
     if ws == 1 and not args.no_post:
+        step()  # the factorization the post-processing converts
         post = {}
         for name, fn in (("rqb_svd", lambda: ctx.svd(copy_out=False)),
                          ("pivoted_qr", lambda: ctx.pivoted_qr(copy_out=False)),
@@ -368,9 +474,23 @@ def run_ours(args, cfg):
                "sample": f"first {args.cpu_sample_blocks} block(s) of the workload (kmax = "
                          f"{args.cpu_sample_blocks * b}), {tc:.1f} s of CPU work", "seconds": tc}
         del A_np
+    ctx.close()
+    del A0, inp
+    torch.cuda.empty_cache()
+
+    # the other BASELINE configs, each its own record (strong-sharded over the N ranks)
+    names = args.records
+    if names == "auto":
+        names = "C1,C2,C3,C4,C5,T1" if ws == 1 else "C3,C4,C5,T1"
+    records = {}
+    for nm in [x for x in names.split(",") if x and x != "none" and x != cfg.name]:
+        try:
+            records[nm] = run_record(nm, args, ws, rank, local)
+        except Exception as e:  # noqa: BLE001 - a failing record is reported, not fatal
+            records[nm] = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
-        scaling = "strong" if (ws > 1 and args.strong) else "weak"
+        scaling = "weak" if weak else "strong"
         par = "single" if ws == 1 else (
             f"row-sharded x{ws} (NCCL allreduce of Grams, W, Z, B_i, norms)" if rows else
             f"column-sharded x{ws} (NCCL allreduce of Y_i, Gram, norms)")
@@ -378,7 +498,7 @@ def run_ours(args, cfg):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
                 "config": {"workload": workload_desc(cfg) + ("" if ws == 1 else
-                           f"; {'one matrix sharded' if args.strong else 'weak: %d x %d global' % (m_global, n_global)}"),
+                           ("; one matrix sharded" if not weak else f"; weak: {m_global} x {n_global} global")),
                            "m": m_global, "n": n_global, "m_per_gpu": m, "n_per_gpu": n_local, "b": b, "q": q,
                            "eps": cfg.eps, "k": k, "blocks": len(stats), "parallelism": par,
                            "l2": f"inputs larger than L2 (A is {m * n_local * es / 1e9:.1f} GB per GPU; every step "
@@ -387,12 +507,31 @@ def run_ours(args, cfg):
                 "frac_fp64_peak": None if f32 else value / ws / (peak * 1e3),
                 "frac_cublas_dgemm": (value / ws / (cublas * 1e3)) if (cublas and not f32) else None,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "post": post,
-                "clocks": clk}
+                "configs": records, "clocks": clk}
         print(json.dumps(line), flush=True)
-    ctx.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def relaunch_under_torchrun(n):
+    """--gpus N without torchrun: start N ranks with torch.distributed.run (127.0.0.1), or fail
+    loudly when fewer than N GPUs are visible (never a silent single-rank run)."""
+    import socket
+    try:
+        import torch
+        have = torch.cuda.device_count()
+    except Exception:  # pragma: no cover
+        have = 0
+    if have < n:
+        sys.stderr.write(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}\n")
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def ctypes_stream(stream):
@@ -411,13 +550,23 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-post", action="store_true", help="skip timing rqb_svd / pivoted QR / fixed-rank")
-    ap.add_argument("--strong", action="store_true", help="N > 1: shard one matrix (strong scaling)")
+    ap.add_argument("--strong", action="store_true", help="N > 1: shard one matrix (strong scaling; the default)")
+    ap.add_argument("--weak", action="store_true", help="N > 1: every rank its own 20000^2 block (weak scaling)")
+    ap.add_argument("--records", default="auto",
+                    help="comma-separated extra configs timed into the line's `configs` ('none' to skip); "
+                         "auto = C1,C2,C3,C4,C5,T1 at N = 1 and C3,C4,C5,T1 at N > 1")
     ap.add_argument("--shard", default="auto", choices=["auto", "cols", "rows"],
                     help="N > 1: shard columns (square A) or rows (tall-skinny A, NEXT-2); auto picks rows "
                          "when m >= 8 n")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:
+        return relaunch_under_torchrun(args.gpus)
+    if ws > 0 and ws != args.gpus and not (ws == 1 and args.gpus <= 1):
+        sys.stderr.write(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}\n")
+        return 2
     import synth
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":

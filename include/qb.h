@@ -87,7 +87,8 @@ typedef struct {
  * Errors: QB_ERR_INVALID_ARG (bad device / dtype), QB_ERR_CUDA.                           */
 qb_status qb_create(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream);
 
-/* Distributed context (column sharding): this process is rank `rank` of
+/* Distributed context (column sharding; = qb_create_sharded with QB_SHARD_COLS,
+ * QB_COMM_NCCL): this process is rank `rank` of
  * `nranks`, one GPU each; `nccl_unique_id` points to the 128-byte ncclUniqueId that rank 0
  * created (qb_nccl_unique_id) and the caller broadcast.  Each rank passes its column shard
  * A(:, col_offset : col_offset + n_local) to qb_factor with n = n_local and the global
@@ -98,7 +99,8 @@ qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_str
                          int rank, int nranks, const void* nccl_unique_id,
                          int64_t col_offset, int64_t n_global);
 
-/* Row-sharded distributed context (NEXT-2, tall-skinny A): this rank holds rows
+/* Row-sharded distributed context (NEXT-2, tall-skinny A; = qb_create_sharded with
+ * QB_SHARD_ROWS, QB_COMM_NCCL): this rank holds rows
  * row_offset .. row_offset + m_local - 1 of an m_global x n matrix and passes that block to
  * qb_factor with m = m_local.  Omega is replicated (all n rows), Y_i and Q_i stay local; the
  * CholeskyQR Grams, the re-projection coefficients W, the power step's Z and B_i are summed
@@ -107,6 +109,47 @@ qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_str
 qb_status qb_create_dist_rows(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream,
                               int rank, int nranks, const void* nccl_unique_id,
                               int64_t row_offset, int64_t m_global);
+
+/* ---- One descriptor for every sharded context (SURVEY.md §8(b) "qb_dist").
+ * The paper designs the method for "shared and distributed memory machines"; the
+ * sharded loop is the same Fig. 2 / Fig. 4 loop with one exchange per application of A.
+ *   shard   QB_SHARD_COLS: this rank holds columns offset .. offset + n_local - 1 of an
+ *           m x global matrix (square A; Y_i and the scalars are summed, Q replicated, B local).
+ *           QB_SHARD_ROWS: rows offset .. offset + m_local - 1 of a global x n matrix
+ *           (tall-skinny A; Grams, W, Z, B_i are summed, Q row-distributed, B replicated).
+ *   comm    QB_COMM_NCCL: one process (or thread) per GPU, an NCCL communicator built from the
+ *           128-byte `nccl_id` rank 0 created (qb_nccl_unique_id) and the caller broadcast.
+ *           QB_COMM_LOOPBACK: `nranks` contexts of ONE process on ONE device, each driven by its
+ *           own host thread, exchanging through `loopback` (qb_loopback_create): each collective
+ *           waits for every rank's stream on the host, sums all ranks' buffers in rank order
+ *           with one kernel, and copies the sum back.  No kernel waits on another rank, so the
+ *           sharded code path runs on one GPU for testing (it is not a performance path).
+ * The sums are identical on every rank, so the replicated orth is too.  Collective: all ranks
+ * call qb_create_sharded and then every qb_factor together.  Errors: QB_ERR_INVALID_ARG for an
+ * inconsistent descriptor (or loopback ranks on different devices), QB_ERR_NCCL when NCCL is
+ * unavailable or fails.  A failing rank aborts a loopback group, so its peers return
+ * QB_ERR_NCCL instead of waiting; NCCL waits poll ncclCommGetAsyncError and give up after
+ * QB_COMM_TIMEOUT_S seconds (default 600), aborting the communicator.                     */
+#define QB_LOOPBACK_MAX_RANKS 8
+typedef struct qb_loopback_s* qb_loopback;
+enum { QB_SHARD_COLS = 0, QB_SHARD_ROWS = 1 };
+enum { QB_COMM_NCCL = 0, QB_COMM_LOOPBACK = 1 };
+typedef struct {
+  int rank, nranks;        /* 0 <= rank < nranks                                             */
+  int shard;               /* QB_SHARD_COLS | QB_SHARD_ROWS                                  */
+  int comm;                /* QB_COMM_NCCL | QB_COMM_LOOPBACK                                */
+  const void* nccl_id;     /* QB_COMM_NCCL: 128-byte ncclUniqueId                            */
+  qb_loopback loopback;    /* QB_COMM_LOOPBACK: the group (outlives its contexts)            */
+  int64_t offset;          /* first global column (COLS) / row (ROWS) of this rank's shard   */
+  int64_t global;          /* n_global (COLS) / m_global (ROWS)                              */
+} qb_dist;
+
+qb_status qb_create_sharded(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, const qb_dist* dist);
+
+/* A loopback group of `nranks` (1 .. QB_LOOPBACK_MAX_RANKS) in-process ranks; destroy it after
+ * its contexts.  QB_ERR_INVALID_ARG for a bad count.                                        */
+qb_status qb_loopback_create(qb_loopback* out, int nranks);
+void qb_loopback_destroy(qb_loopback group);
 
 /* Write a fresh ncclUniqueId (128 bytes) to `out128`.  QB_ERR_NCCL if NCCL is absent.      */
 qb_status qb_nccl_unique_id(void* out128);

@@ -27,6 +27,12 @@ QB_ERR_UNSUPPORTED = 7
 QB_F64 = 0
 QB_F32 = 1
 
+QB_SHARD_COLS = 0
+QB_SHARD_ROWS = 1
+QB_COMM_NCCL = 0
+QB_COMM_LOOPBACK = 1
+QB_LOOPBACK_MAX_RANKS = 8
+
 QB_OVERWRITE_A = 1
 QB_NO_REPROJ = 2
 QB_SKIP_POWER_ORTH = 4
@@ -43,6 +49,13 @@ class BlockStats(ctypes.Structure):
                 ("ei", ctypes.c_double), ("ms", ctypes.c_double), ("ms_sketch", ctypes.c_double),
                 ("ms_bmat", ctypes.c_double), ("ms_down", ctypes.c_double), ("fallback", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
+
+
+class QBDist(ctypes.Structure):
+    """qb_dist (include/qb.h)."""
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("shard", ctypes.c_int), ("comm", ctypes.c_int),
+                ("nccl_id", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("offset", ctypes.c_int64),
+                ("global_", ctypes.c_int64)]
 
 
 _lib = None
@@ -65,6 +78,10 @@ def lib():
         L.qb_create_dist_rows.argtypes = [P(c_ctx), ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, vp,
                                           i64, i64]
         L.qb_nccl_unique_id.argtypes = [vp]
+        L.qb_create_sharded.argtypes = [P(c_ctx), ctypes.c_int, ctypes.c_int, vp, P(QBDist)]
+        L.qb_loopback_create.argtypes = [P(vp), ctypes.c_int]
+        L.qb_loopback_destroy.argtypes = [vp]
+        L.qb_loopback_destroy.restype = None
         L.qb_factor.argtypes = [c_ctx, vp, i64, i64, i64, dbl, i64, ctypes.c_int, u64, i64, ctypes.c_uint,
                                 P(i64), P(vp), P(i64), P(vp), P(i64), P(dbl)]
         L.qb_factor_host.argtypes = [c_ctx, vp, i64, i64, i64, dbl, i64, ctypes.c_int, u64, i64, P(i64), vp, i64,
@@ -87,7 +104,7 @@ def lib():
         L.qb_status_string.restype = ctypes.c_char_p
         L.qb_last_error.argtypes = [c_ctx]
         L.qb_last_error.restype = ctypes.c_char_p
-        for f in ("qb_create", "qb_create_dist", "qb_create_dist_rows", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_gemm", "qb_chol_rinv", "qb_stats", "qb_omega",
+        for f in ("qb_create", "qb_create_dist", "qb_create_dist_rows", "qb_create_sharded", "qb_loopback_create", "qb_nccl_unique_id", "qb_factor", "qb_factor_host", "qb_gemm", "qb_chol_rinv", "qb_stats", "qb_omega",
                   "qb_orth", "rqb_svd", "qb_fixed_rank", "qb_pivoted_qr"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -149,6 +166,45 @@ def qb_create_dist(device, rank, nranks, unique_id, col_offset, n_global, dtype=
             lib().qb_destroy(ctx)
         raise QBError(s, msg)
     return ctx
+
+
+def qb_create_sharded(device, rank, nranks, shard, offset, global_, dtype=QB_F64, stream=None, unique_id=None,
+                      loopback=None):
+    """Sharded context from a qb_dist descriptor: shard QB_SHARD_COLS / QB_SHARD_ROWS; NCCL
+    (unique_id, 128 bytes) or an in-process loopback group (loopback = qb_loopback_create())."""
+    d = QBDist()
+    d.rank, d.nranks, d.shard = int(rank), int(nranks), int(shard)
+    uid = None
+    if loopback is not None:
+        d.comm = QB_COMM_LOOPBACK
+        d.loopback = loopback.value if isinstance(loopback, ctypes.c_void_p) else loopback
+    else:
+        d.comm = QB_COMM_NCCL
+        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        d.nccl_id = ctypes.cast(uid, ctypes.c_void_p)
+    d.offset, d.global_ = int(offset), int(global_)
+    ctx = ctypes.c_void_p()
+    s = lib().qb_create_sharded(ctypes.byref(ctx), int(device), int(dtype), stream, ctypes.byref(d))
+    if s != QB_OK:
+        msg = qb_last_error(ctx) if ctx.value else ""
+        if ctx.value:
+            lib().qb_destroy(ctx)
+        raise QBError(s, msg)
+    return ctx
+
+
+def qb_loopback_create(nranks):
+    """An in-process loopback group of nranks ranks (one GPU, one host thread per rank)."""
+    g = ctypes.c_void_p()
+    s = lib().qb_loopback_create(ctypes.byref(g), int(nranks))
+    if s != QB_OK:
+        raise QBError(s, f"qb_loopback_create({nranks})")
+    return g
+
+
+def qb_loopback_destroy(group):
+    if group is not None and group.value:
+        lib().qb_loopback_destroy(group)
 
 
 def qb_destroy(ctx):
@@ -283,7 +339,8 @@ class QB:
     def __init__(self, device=0, dtype=QB_F64, stream=None, dist=None):
         """dist: None, dict(rank, nranks, unique_id, col_offset, n_global) for a column-sharded
         context, or dict(shard="rows", rank, nranks, unique_id, row_offset, m_global) for a
-        row-sharded one (see paper_1503_07157_b200.dist)."""
+        row-sharded one (see paper_1503_07157_b200.dist); with loopback=<qb_loopback_create()>
+        instead of unique_id the ranks are in-process contexts on one GPU (one host thread each)."""
         # Default to torch's current stream on `device` so that the library's kernels are
         # stream-ordered after the torch work that produced their inputs.
         if stream is None:
@@ -292,6 +349,13 @@ class QB:
             stream = ctypes.c_void_p(h if h else 1)   # 0 (torch's default) -> cudaStreamLegacy
         if dist is None:
             self.ctx = qb_create(device, dtype, stream)
+        elif dist.get("loopback") is not None:
+            rows = dist.get("shard", "cols") == "rows"
+            self.ctx = qb_create_sharded(device, dist["rank"], dist["nranks"],
+                                         QB_SHARD_ROWS if rows else QB_SHARD_COLS,
+                                         dist["row_offset"] if rows else dist["col_offset"],
+                                         dist["m_global"] if rows else dist["n_global"], dtype, stream,
+                                         loopback=dist["loopback"])
         else:
             if dist.get("shard", "cols") == "rows":
                 self.ctx = qb_create_dist(device, dist["rank"], dist["nranks"], dist["unique_id"], dist["row_offset"],

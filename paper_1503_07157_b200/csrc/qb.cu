@@ -9,9 +9,13 @@
 // words.  The post-processing entry points (rqb_svd, qb_pivoted_qr) and the fixed-rank schemes
 // (qb_fixed_rank) reuse the same kernels; the k x k SVD core of rqb_svd is cuSOLVER (dlopen).
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -23,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
 #include <nccl.h>  // types only: NCCL is loaded at run time (dlopen), never linked
 #include <cusolverDn.h>  // types only: cuSOLVER (the k x k SVD core of rqb_svd) is loaded at run time
 
@@ -59,6 +64,8 @@ struct NcclApi {
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclGetErrorString) errorString = nullptr;
+  decltype(&ncclCommGetAsyncError) getAsyncError = nullptr;
+  decltype(&ncclCommAbort) commAbort = nullptr;
 };
 
 NcclApi& nccl() {
@@ -76,7 +83,10 @@ NcclApi& nccl() {
   api.commDestroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(h, "ncclCommDestroy"));
   api.allReduce = reinterpret_cast<decltype(&ncclAllReduce)>(dlsym(h, "ncclAllReduce"));
   api.errorString = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
-  api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.errorString;
+  api.getAsyncError = reinterpret_cast<decltype(&ncclCommGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+  api.commAbort = reinterpret_cast<decltype(&ncclCommAbort)>(dlsym(h, "ncclCommAbort"));
+  api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.errorString &&
+           api.getAsyncError && api.commAbort;
   return api;
 }
 
@@ -153,7 +163,9 @@ struct qb_ctx_s {
   // row sharding (NEXT-2, tall-skinny A): this rank holds rows row_offset .. of an m_global-row A
   bool shard_rows = false;
   int64_t row_offset = 0, m_global = 0;
-  ncclComm_t comm = nullptr;  // set on distributed contexts (any nranks >= 1)
+  ncclComm_t comm = nullptr;  // set on NCCL-distributed contexts (any nranks >= 1)
+  qb_loopback loop = nullptr; // set on loopback-distributed contexts (in-process ranks, one GPU)
+  bool dist = false;          // a distributed context (NCCL or loopback), any nranks >= 1
 
   DevBuf Awork, Qbar, Bbar, Om, Y, T1, Z, Zt, G, L, Rinv, W, P, parts, scal, status, Qf, Bf, Astage, Q32, B32,
       Qbar32, W32;
@@ -185,6 +197,55 @@ struct qb_ctx_s {
   const double* outB = nullptr;
 };
 
+// In-process loopback group ("loopback"): nranks contexts of ONE process on ONE
+// GPU, each driven by its own host thread, exchange their sums through this object instead of
+// NCCL.  A collective is host-synchronised: every rank finishes its stream, meets the others at
+// a host barrier, rank 0 sums all ranks' buffers in rank order with ONE kernel over all ranks'
+// data, and after a second barrier every rank copies the sum back.  No kernel ever waits on
+// another rank's kernel (B200_PROFILING.md: such ranks on one GPU must not spin on each other).
+struct qb_loopback_s {
+  int nranks = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool aborted = false;
+  std::string why;
+  double* bufs[QB_LOOPBACK_MAX_RANKS] = {};
+  size_t counts[QB_LOOPBACK_MAX_RANKS] = {};
+  int device = -1;      // the one device of every member
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  double timeout_s = 600.0;
+
+  // false if the group was (or gets) aborted, or nobody else arrives within timeout_s
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return false;
+    const uint64_t g = gen;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    const bool done = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return gen != g || aborted; });
+    if (gen != g) return true;
+    if (!done && !aborted) {
+      aborted = true;
+      why = "loopback barrier timed out";
+      cv.notify_all();
+    }
+    return false;
+  }
+  void abort(const char* reason) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!aborted) why = reason;
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
 namespace {
 
 qb_status fail(qb_ctx c, qb_status s, const char* fmt, ...) {
@@ -210,6 +271,38 @@ qb_status fail(qb_ctx c, qb_status s, const char* fmt, ...) {
     qb_status s_ = (expr);           \
     if (s_ != QB_OK) return s_;      \
   } while (0)
+
+// The dynamic shared-memory limit of a >48 KB kernel is an attribute of the current device's
+// context: set it once per kernel and device (one bit per device; several host threads may
+// race to set it, which is harmless).  Callers have selected ctx->device.
+#define QB_SMEM_ATTR(kern, bytes)                                                                  \
+  do {                                                                                             \
+    static std::atomic<uint64_t> attr_mask_{0};                                                    \
+    const uint64_t bit_ = uint64_t{1} << (ctx->device & 63);                                       \
+    if (!(attr_mask_.load(std::memory_order_acquire) & bit_)) {                                    \
+      QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (bytes)));   \
+      attr_mask_.fetch_or(bit_, std::memory_order_acq_rel);                                        \
+    }                                                                                              \
+  } while (0)
+
+// NVTX range for the duration of a scope (the step names of SURVEY.md §5: K1 ... K8, C1 ...).
+struct NvtxPhase {  // consecutive phases of one scope: each call closes the previous range
+  bool on = false;
+  void operator()(const char* name) {
+    if (on) nvtxRangePop();
+    nvtxRangePushA(name);
+    on = true;
+  }
+  ~NvtxPhase() {
+    if (on) nvtxRangePop();
+  }
+};
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int debug_env(const char* name) {
   const char* v = getenv(name);
@@ -241,11 +334,95 @@ qb_status check_launch(qb_ctx ctx, const char* what) {
   return QB_OK;
 }
 
+double comm_timeout_s() {
+  static const double t = getenv("QB_COMM_TIMEOUT_S") ? atof(getenv("QB_COMM_TIMEOUT_S")) : 600.0;
+  return t > 0 ? t : 600.0;
+}
+
+// Host wait for the context stream.  On an NCCL context the wait polls the communicator's
+// asynchronous error state and gives up after QB_COMM_TIMEOUT_S seconds (default 600): a peer
+// that died or diverged would otherwise hang the collective forever.  The communicator is then
+// aborted (its pending collectives are cancelled) and the context is unusable.
+qb_status stream_wait(qb_ctx ctx) {
+  if (!ctx->comm) {
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return QB_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  int spins = 0;
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(ctx->stream);
+    if (e == cudaSuccess) return QB_OK;
+    if (e != cudaErrorNotReady)
+      return fail(ctx, QB_ERR_CUDA, "stream: %s", cudaGetErrorString(e));
+    ncclResult_t ae = ncclSuccess;
+    if (nccl().getAsyncError(ctx->comm, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+      nccl().commAbort(ctx->comm);
+      ctx->comm = nullptr;
+      return fail(ctx, QB_ERR_NCCL, "NCCL asynchronous error: %s", nccl().errorString(ae));
+    }
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > comm_timeout_s()) {
+      nccl().commAbort(ctx->comm);
+      ctx->comm = nullptr;
+      return fail(ctx, QB_ERR_NCCL, "collective timed out after %.0f s (QB_COMM_TIMEOUT_S)", comm_timeout_s());
+    }
+    if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// Loopback allreduce (see qb_loopback_s): in place, rank order, identical result on every rank.
+qb_status loopback_allreduce(qb_ctx ctx, double* buf, size_t count) {
+  qb_loopback G = ctx->loop;
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));  // this rank's buffer is final
+  {
+    std::lock_guard<std::mutex> lk(G->mu);
+    G->bufs[ctx->rank] = buf;
+    G->counts[ctx->rank] = count;
+  }
+  if (!G->barrier()) return fail(ctx, QB_ERR_NCCL, "loopback group aborted (%s)", G->why.c_str());
+  if (ctx->rank == 0) {
+    qb_status st = QB_OK;
+    for (int r = 1; r < G->nranks; ++r)
+      if (G->counts[r] != count) st = fail(ctx, QB_ERR_NCCL, "loopback allreduce: rank %d has %zu elements, rank 0 %zu", r, G->counts[r], count);
+    if (st == QB_OK && G->scratch_bytes < count * sizeof(double)) {
+      if (G->scratch) cudaFree(G->scratch);
+      G->scratch = nullptr;
+      G->scratch_bytes = 0;
+      if (cudaMalloc(&G->scratch, count * sizeof(double)) != cudaSuccess) {
+        G->scratch = nullptr;
+        st = fail(ctx, QB_ERR_OOM, "loopback allreduce: scratch of %zu doubles", count);
+      } else {
+        G->scratch_bytes = count * sizeof(double);
+      }
+    }
+    if (st == QB_OK) {
+      LoopPtrs in{};
+      for (int r = 0; r < G->nranks; ++r) in.p[r] = G->bufs[r];
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)count + 255) / 256, 8 * ctx->num_sms));
+      loopback_sum_kernel<<<grid, 256, 0, ctx->stream>>>(in, G->nranks, (int64_t)count, static_cast<double*>(G->scratch));
+      st = check_launch(ctx, "loopback_sum");
+      if (st == QB_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = fail(ctx, QB_ERR_CUDA, "loopback sum failed");
+    }
+    if (st != QB_OK) {
+      G->abort("rank 0 failed in a loopback allreduce");
+      return st;
+    }
+  }
+  if (!G->barrier()) return fail(ctx, QB_ERR_NCCL, "loopback group aborted (%s)", G->why.c_str());
+  QB_CUDA(cudaMemcpyAsync(buf, G->scratch, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  QB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QB_OK;
+}
+
 // Sum `count` doubles across the ranks of a distributed context, in place on the context
-// stream (no-op on a plain context).
+// stream (no-op on a plain context): NCCL, or the in-process loopback group.
 qb_status allreduce_sum(qb_ctx ctx, double* buf, size_t count) {
-  if (!ctx->comm || count == 0) return QB_OK;
+  if (count == 0) return QB_OK;
+  if (ctx->loop) return loopback_allreduce(ctx, buf, count);
+  if (!ctx->comm) return QB_OK;
+  nvtxRangePushA("C1 allreduce");
   ncclResult_t r = nccl().allReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream);
+  nvtxRangePop();
   if (r != ncclSuccess) return fail(ctx, QB_ERR_NCCL, "ncclAllReduce: %s", nccl().errorString(r));
   return QB_OK;
 }
@@ -289,11 +466,7 @@ qb_status launch_gemm_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb
                         const GemmParams& p, int splits) {
   using Cfg = GemmCfg<BN, EPI>;
   auto kern = gemm_f64_kernel<LAYOUT, BN, EPI>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_done = true;
-  }
+  QB_SMEM_ATTR(kern, Cfg::SMEM_BYTES);
   dim3 grid(p.tiles_m * p.tiles_n, splits);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tc, p);
   return check_launch(ctx, "gemm_f64");
@@ -487,11 +660,7 @@ qb_status launch_tf_ts(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb,
                        const CUtensorMap& tc, const TfParams& p, int splits) {
   using Cfg = TfCfg<BN, EPI == TF_SUB_COL, TS>;
   auto kern = gemm_tf32_kernel<LAYOUT, BN, EPI, TS>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_done = true;
-  }
+  QB_SMEM_ATTR(kern, Cfg::SMEM_BYTES);
   const int units = p.tiles_m * p.tiles_n * splits;
   kern<<<std::min(units, ctx->num_sms), Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tb, tb2, tc, p);
   return check_launch(ctx, "gemm_tf32");
@@ -503,11 +672,7 @@ qb_status launch_tf_ares(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& t
                          const CUtensorMap& tc, const TfParams& p) {
   using Cfg = TfAresCfg<BN>;
   auto kern = gemm_tf32_sub_ares_kernel<BN>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    QB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_done = true;
-  }
+  QB_SMEM_ATTR(kern, Cfg::SMEM_BYTES);
   const int units = p.tiles_m * p.tiles_n;
   kern<<<std::min(units, ctx->num_sms), TF_THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ta, tbh, tbl, tc, p);
   return check_launch(ctx, "gemm_tf32_sub_ares");
@@ -675,11 +840,7 @@ int* status_dev(qb_ctx ctx) { return static_cast<int*>(ctx->status.p); }
 // T for one CholeskyQR pass from the Gram matrix in ctx->G (no host synchronisation):
 // Newton-Schulz T = I - (G - I)/2 when ||G - I||_F <= 1e-8 (ns), else T = R^-1.
 qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    QB_CUDA(cudaFuncSetAttribute(chol_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CHOL_SMEM));
-    attr_done = true;
-  }
+  QB_SMEM_ATTR(chol_cluster_kernel, CHOL_SMEM);
   const int64_t ld = round_up(kMaxB, 16);
   // Newton-Schulz when ||G - I||_F <= 1e-8 (FP64: step error <= 1e-16), <= 1e-4 on FP32 contexts
   // (step error <= 7.5e-9, below FP32 rounding; reading R18c)
@@ -699,7 +860,10 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
   QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr, true,
               gate));
   if (row_distributed) QB_TRY(allreduce_sum(ctx, ctx->G.d(), (size_t)(ldgb * w)));  // G = sum_p src_p^T src_p
-  QB_TRY(chol_inv(ctx, w, m, true, gate));
+  // the shifted-CholeskyQR shift (reading R8) is sized for the GLOBAL row count of the panel:
+  // the power step's Z on column shards has n_global rows, a row shard's Y / Q_i m_global
+  const int64_t m_shift = !row_distributed ? m : (ctx->shard_rows ? ctx->m_global : ctx->n_global);
+  QB_TRY(chol_inv(ctx, w, m_shift, true, gate));
   static const int orth64 = debug_env("QB_ORTH64");
   if (ctx->dtype == QB_F32 && !orth64) {
     // FP32 contexts (reading R18c): X T on the 3xTF32 tensor cores from FP32 copies of X and T;
@@ -992,29 +1156,84 @@ qb_status qb_nccl_unique_id(void* out128) {
   return QB_OK;
 }
 
-qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, int rank, int nranks,
-                         const void* nccl_unique_id, int64_t col_offset, int64_t n_global) {
+qb_status qb_loopback_create(qb_loopback* out, int nranks) {
+  if (!out) return QB_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (nranks < 1 || nranks > QB_LOOPBACK_MAX_RANKS) return QB_ERR_INVALID_ARG;
+  qb_loopback g = new qb_loopback_s();
+  g->nranks = nranks;
+  g->timeout_s = comm_timeout_s();
+  *out = g;
+  return QB_OK;
+}
+
+void qb_loopback_destroy(qb_loopback g) {
+  if (!g) return;
+  if (g->scratch) {
+    cudaSetDevice(g->device);
+    cudaFree(g->scratch);
+  }
+  delete g;
+}
+
+qb_status qb_create_sharded(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, const qb_dist* d) {
+  if (!out) return QB_ERR_INVALID_ARG;
   qb_status s = qb_create(out, device, dtype, cuda_stream);
   if (s != QB_OK) return s;
   qb_ctx ctx = *out;
-  if (nranks < 1 || rank < 0 || rank >= nranks || col_offset < 0 || n_global < 1 || !nccl_unique_id)
+  if (!d || d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks || d->offset < 0 || d->global < 1 ||
+      (d->shard != QB_SHARD_COLS && d->shard != QB_SHARD_ROWS) ||
+      (d->comm != QB_COMM_NCCL && d->comm != QB_COMM_LOOPBACK) ||
+      (d->comm == QB_COMM_NCCL && !d->nccl_id) || (d->comm == QB_COMM_LOOPBACK && !d->loopback))
     return fail(ctx, QB_ERR_INVALID_ARG, "bad distributed arguments");
-  ctx->col_offset = col_offset;
-  ctx->n_global = n_global;
-  return init_comm(ctx, rank, nranks, nccl_unique_id);
+  ctx->dist = true;
+  if (d->shard == QB_SHARD_ROWS) {
+    ctx->shard_rows = true;
+    ctx->row_offset = d->offset;
+    ctx->m_global = d->global;
+  } else {
+    ctx->col_offset = d->offset;
+    ctx->n_global = d->global;
+  }
+  if (d->comm == QB_COMM_NCCL) return init_comm(ctx, d->rank, d->nranks, d->nccl_id);
+  qb_loopback g = d->loopback;
+  if (g->nranks != d->nranks) return fail(ctx, QB_ERR_INVALID_ARG, "loopback group has %d ranks, not %d", g->nranks, d->nranks);
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->device < 0) g->device = device;
+    if (g->device != device)
+      return fail(ctx, QB_ERR_INVALID_ARG, "loopback ranks must share one device (%d, not %d)", g->device, device);
+  }
+  ctx->rank = d->rank;
+  ctx->nranks = d->nranks;
+  ctx->loop = g;
+  return QB_OK;
+}
+
+qb_status qb_create_dist(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, int rank, int nranks,
+                         const void* nccl_unique_id, int64_t col_offset, int64_t n_global) {
+  qb_dist d{};
+  d.rank = rank;
+  d.nranks = nranks;
+  d.shard = QB_SHARD_COLS;
+  d.comm = QB_COMM_NCCL;
+  d.nccl_id = nccl_unique_id;
+  d.offset = col_offset;
+  d.global = n_global;
+  return qb_create_sharded(out, device, dtype, cuda_stream, &d);
 }
 
 qb_status qb_create_dist_rows(qb_ctx* out, int device, qb_dtype dtype, void* cuda_stream, int rank, int nranks,
                               const void* nccl_unique_id, int64_t row_offset, int64_t m_global) {
-  qb_status s = qb_create(out, device, dtype, cuda_stream);
-  if (s != QB_OK) return s;
-  qb_ctx ctx = *out;
-  if (nranks < 1 || rank < 0 || rank >= nranks || row_offset < 0 || m_global < 1 || !nccl_unique_id)
-    return fail(ctx, QB_ERR_INVALID_ARG, "bad distributed arguments");
-  ctx->shard_rows = true;
-  ctx->row_offset = row_offset;
-  ctx->m_global = m_global;
-  return init_comm(ctx, rank, nranks, nccl_unique_id);
+  qb_dist d{};
+  d.rank = rank;
+  d.nranks = nranks;
+  d.shard = QB_SHARD_ROWS;
+  d.comm = QB_COMM_NCCL;
+  d.nccl_id = nccl_unique_id;
+  d.offset = row_offset;
+  d.global = m_global;
+  return qb_create_sharded(out, device, dtype, cuda_stream, &d);
 }
 
 void qb_destroy(qb_ctx ctx) {
@@ -1584,9 +1803,9 @@ qb_status qb_fixed_rank(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda
   return publish_outputs(ctx, m, n, l, Q_out, ldq_out, B_out, ldb_out);
 }
 
-qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, double eps, int64_t b, int q,
-                    uint64_t seed, int64_t kmax, unsigned flags, int64_t* k_out, const void** Q_out,
-                    int64_t* ldq_out, const void** B_out, int64_t* ldb_out, double* resid_out) {
+static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, double eps, int64_t b, int q,
+                             uint64_t seed, int64_t kmax, unsigned flags, int64_t* k_out, const void** Q_out,
+                             int64_t* ldq_out, const void** B_out, int64_t* ldb_out, double* resid_out) {
   if (!ctx) return QB_ERR_INVALID_ARG;
   ctx->stats.clear();
   if (!k_out) return fail(ctx, QB_ERR_INVALID_ARG, "k must not be NULL");
@@ -1618,8 +1837,8 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   if (!(eps >= 0.0)) return fail(ctx, QB_ERR_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
   // sharding: column shards allreduce Y (and the row-distributed Z's Gram);
   // row shards (NEXT-2) allreduce Grams, W, Z and B_i instead, and keep Y, Q_i local
-  const bool rowsh = ctx->comm != nullptr && ctx->shard_rows;
-  const bool colsh = ctx->comm != nullptr && !ctx->shard_rows;
+  const bool rowsh = ctx->dist && ctx->shard_rows;
+  const bool colsh = ctx->dist && !ctx->shard_rows;
   const int64_t n_glob = (colsh && ctx->nranks > 1) ? ctx->n_global : n;
   const int64_t m_glob = (rowsh && ctx->nranks > 1) ? ctx->m_global : m;
   const int64_t kmax_eff = (kmax <= 0) ? std::min(m_glob, n_glob) : std::min(kmax, std::min(m_glob, n_glob));
@@ -1687,7 +1906,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(reduce_to_scal(ctx, grid, 0));
     QB_TRY(allreduce_sum(ctx, ctx->scal.d(), 1));  // ||A||_F^2 over the column shards
     QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    QB_TRY(stream_wait(ctx));
   }
   const double r2_0 = ctx->h_scal[0];
   if (!std::isfinite(r2_0)) return fail(ctx, QB_ERR_INVALID_ARG, "A contains NaN or Inf");
@@ -1796,6 +2015,8 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
 
     // line (2): Ω_i = randn(n, w), global columns ell .. ell+w-1, row-major (ld bp); FP32
     // contexts draw RN_32(Ω_i) (reading R18)
+    NvtxPhase phase;
+    phase("K1 omega + K2 sketch (+C1)");
     QB_CUDA(cudaEventRecord(ctx->evp[0], ctx->stream));
     QB_TRY(launch_omega(ctx, seed, ctx->col_offset, ctx->col_offset + n, ell, w, ctx->Om.p, bp, is_f32 ? 1 : 0));
     // line (3): Y_i = A^(i-1) Ω_i ; Q_i = orth(Y_i)
@@ -1811,6 +2032,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       return cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh, single, Y32, ldm, Qi32, ctx->ldq);
     };
     auto orth_y = [&]() -> qb_status { return orth_y_into(reproj_follows); };
+    phase("K4 orth + K3 power steps");
     if (!(skip_orth_flag(flags) && q > 0)) {
       if (q == 0) QB_TRY(orth_y());
       else QB_TRY(orth_y_into(false));
@@ -1837,6 +2059,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i))  (one projection + orth, reading R11)
     if (ell > 0 && !(flags & QB_NO_REPROJ)) {
+      phase("K5 re-projection + orth");
       QB_TRY(ensure(ctx, ctx->W, sizeof(double) * (size_t)(ell * bp)));
       if (is_f32) {  // on the FP32 copies: W = Q̄^T Q_i, Q_i -= Q̄ W (3xTF32), then orth in FP64
         QB_TRY(ensure(ctx, ctx->W32, sizeof(float) * (size_t)(ell * bp)));
@@ -1867,6 +2090,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     }
     // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
     int64_t nb_parts = 0;
+    phase("K6 B_i = Q_i^T A");
     QB_CUDA(cudaEventRecord(ctx->evp[2], ctx->stream));
     if (is_f32) {
       QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)w, (int)n, (int)m, Qi32, ctx->ldq, A32, ldA, Bi, ctx->ldb,
@@ -1886,6 +2110,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
     QB_TRY(reduce_to_scal(ctx, nb_parts, 1));
     // line (10): A^(i) = A^(i-1) - Q_i B_i, with sum A^(i)^2 in the epilogue (the stop test, R1)
     int64_t na_parts = 0;
+    phase("K7 downdate A -= Q_i B_i");
     QB_CUDA(cudaEventRecord(ctx->evp[4], ctx->stream));
     if (is_f32) {  // A -= RN32(Q_i) RN32(B_i): the residual of the factors the caller receives
       if (b32_copy_pending) {  // the previous block's B32 is still being copied to the host
@@ -1900,6 +2125,7 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
                   &na_parts));
     }
     QB_CUDA(cudaEventRecord(ctx->evp[5], ctx->stream));
+    phase("K8 stop test");
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
     // ||A^(i)||_F^2 (and, on column shards, ||B_i||_F^2) summed over the shards
     QB_TRY(allreduce_sum(ctx, ctx->scal.d(), rowsh ? 1 : 2));
@@ -1914,7 +2140,10 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
       th_ev0 = now_ms();
     }
     if (host_timing) QB_CUDA(cudaEventRecord(ctx->ev_gap, ctx->stream));  // this block's end on the device
-    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    {
+      NvtxRange nv("K8 stop test (host wait)");
+      QB_TRY(stream_wait(ctx));
+    }
     if (host_timing)
       fprintf(stderr, "[qb host] block at %lld: enqueue %.3f ms, block start +%.3f ms, wait %.3f ms, device gap %.3f ms\n",
               (long long)ell, th1 - th0, th_ev0 - th0, now_ms() - th1, gap_ms);
@@ -1960,6 +2189,17 @@ qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, do
   QB_TRY(publish_outputs(ctx, m, n, ell, Q_out, ldq_out, B_out, ldb_out));
   if (resid_out) *resid_out = std::sqrt(r2);
   return r2 <= eps2 ? QB_OK : QB_NOT_CONVERGED;
+}
+
+qb_status qb_factor(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda, double eps, int64_t b, int q,
+                    uint64_t seed, int64_t kmax, unsigned flags, int64_t* k_out, const void** Q_out,
+                    int64_t* ldq_out, const void** B_out, int64_t* ldb_out, double* resid_out) {
+  NvtxRange nv("qb_factor");
+  const qb_status s = factor_impl(ctx, Ain, m, n, lda, eps, b, q, seed, kmax, flags, k_out, Q_out, ldq_out, B_out,
+                                  ldb_out, resid_out);
+  // a failed rank of an in-process loopback group releases its peers from the next barrier
+  if (s != QB_OK && s != QB_NOT_CONVERGED && ctx && ctx->loop) ctx->loop->abort("a rank failed in qb_factor");
+  return s;
 }
 
 qb_status qb_factor_host(qb_ctx ctx, const void* A_host, int64_t m, int64_t n, int64_t lda_host, double eps,

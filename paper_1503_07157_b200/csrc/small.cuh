@@ -92,6 +92,21 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
   }
 }
 
+// Loopback collective: out = sum_r in[r] in rank order, one kernel over the data
+// of all in-process ranks (no rank's kernel waits on another's).
+constexpr int LOOP_MAX = 8;
+struct LoopPtrs {
+  const double* p[LOOP_MAX];
+};
+__global__ void __launch_bounds__(256) loopback_sum_kernel(LoopPtrs in, int nranks, int64_t count,
+                                                           double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < count; i += static_cast<int64_t>(gridDim.x) * 256) {
+    double s = in.p[0][i];
+    for (int r = 1; r < nranks; ++r) s += in.p[r][i];
+    out[i] = s;
+  }
+}
+
 // a0 fused with the working copy (qb_factor without QB_OVERWRITE_A): dst = src column by column
 // and the same per-block sums of squares as sumsq_kernel, in the same order (bitwise equal r0^2).
 template <typename T>
@@ -463,6 +478,10 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
       cluster.sync();
       if (p == 0) CHOL_TS(7);
       if (*cluster.map_shared_rank(&s_fail, p)) {
+        // every thread of every CTA has read CTA p's flag before any CTA passes this barrier, so
+        // CTA p cannot reset it (next attempt) or reload its panel while a peer still reads them;
+        // the flag is constant until then, so all threads take this branch together
+        cluster.sync();
         failed = true;
         break;
       }
