@@ -57,10 +57,10 @@ int main(void) {
          sqrt(err2), eps);
   if (!(sqrt(err2) <= eps * (1 + 1e-6)) || fabs(sqrt(err2) - resid) > 1e-10) return 2;
   const void *Ud = NULL, *Sd = NULL, *Vd = NULL;
-  int64_t ldu = 0, ldv = 0;
-  CHECK(rqb_svd(ctx, 5, &Ud, &ldu, &Sd, &Vd, &ldv));
-  printf("rqb_svd: leading singular values live on the device at %p (k' = 5); kernel launches so far: %lld\n", Sd,
-         (long long)qb_kernel_launches(ctx));
+  int64_t ldu = 0, ldv = 0, kk = 0;
+  CHECK(rqb_svd(ctx, 0.0, 5, &kk, &Ud, &ldu, &Sd, &Vd, &ldv));
+  printf("rqb_svd: leading singular values live on the device at %p (k' = %lld); kernel launches so far: %lld\n", Sd,
+         (long long)kk, (long long)qb_kernel_launches(ctx));
   qb_destroy(ctx);
   free(A); free(U); free(V); free(Q); free(B);
   return 0;

@@ -240,17 +240,28 @@ qb_status qb_gemm(qb_ctx ctx, int layout, int epi, int64_t M, int64_t N, int64_t
 qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_t m_rows,
                        void* Rinv, int64_t ldr, int* shifted);
 
-/* Partial SVD from the context's last qb_factor (NEXT-1): B = Uhat D V^*, U = Q Uhat,
- * so that A ~ U diag(S) V^* with U^*U = V^*V = I and S descending.  B^T = Q_B R by block
- * Gram-Schmidt + CholeskyQR2, R's k x k SVD by cuSOLVER dgesvd (loaded at run time), U = Q Vr,
- * V = Q_B Ur on the library's GEMMs; FP64 internally on every context.
- * kkeep > 0 keeps the leading kkeep triplets (the tail rule), else all k.
- * Outputs (context-owned, valid until the next call): U column-major m x kkeep (ld *ldu),
- * S kkeep values, V column-major n x kkeep (ld *ldv), in the context's dtype.  k = 0 gives
- * NULL pointers.  Errors: QB_ERR_INVALID_ARG without a prior factorization,
- * QB_ERR_UNSUPPORTED on distributed contexts or without libcusolver.  Blocking.            */
-qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U, int64_t* ldu, const void** S,
-                  const void** V, int64_t* ldv);
+/* Partial SVD from the context's last qb_factor / qb_fixed_rank (NEXT-1):
+ * B = Uhat D V^*, U = Q Uhat, so that A ~ U diag(S) V^* with U^*U = V^*V = I and S descending.
+ * B^T = Q_B R by block Gram-Schmidt + CholeskyQR2; the k x k SVD of R^T by this library's block
+ * one-sided Jacobi (relatively accurate, DESIGN.md §5 "rqb_svd"; no solver library); U = Q Uhat,
+ * V = Q_B J on the library's GEMMs; FP64 internally on every context.
+ * The rank kept, k' (*kk), is chosen from the decaying singular values ("choose a rank k ...
+ * based on the decaying singular values"; truncation undoes the over-sampling,
+ * P:405-406):
+ *   eps_or_0 > 0: the smallest k' with ||A - U_k' D_k' V_k'^*||_F^2 = r_k^2 + sum_{j > k'} D_j^2
+ *                 <= eps^2, where r_k = ||A - QB||_F of the factorization (0 for a qb_fixed_rank
+ *                 call without its residual) — the tail rule;
+ *   kkeep_or_0 > 0: at most kkeep triplets; with both, the smaller k'; with neither, k' = k.
+ * Outputs (context-owned, valid until the next call): U column-major m x k' (ld *ldu), S k'
+ * values, V column-major n x k' (ld *ldv), in the context's dtype.  k' = 0 gives NULL pointers.
+ * Errors: QB_ERR_INVALID_ARG without a prior factorization or with eps < 0 / NaN;
+ * QB_ERR_UNSUPPORTED on column-sharded contexts, or if the Jacobi sweeps do not converge
+ * (40 sweeps).  Blocking.                                                                   */
+qb_status rqb_svd(qb_ctx ctx, double eps_or_0, int64_t kkeep_or_0, int64_t* kk, const void** U, int64_t* ldu,
+                  const void** S, const void** V, int64_t* ldv);
+
+/* Number of Jacobi sweeps the last rqb_svd took (diagnostics).                              */
+int qb_svd_sweeps(qb_ctx ctx);
 
 /* Partial pivoted QR from the context's last factorization (NEXT-4):
  * B P = Q~ R by Householder QR with column pivoting of the k x n factor B (LAPACK dlaqp2

@@ -156,3 +156,33 @@ def qb_to_svd(Q, B):
     """QB -> partial SVD: B = Û D V^*, U = Q Û; A ≈ U D V^*."""
     Uh, D, Vt = np.linalg.svd(np.asarray(B, dtype=np.float64), full_matrices=False)
     return Q @ Uh, D, Vt.T
+
+
+def tail_rank(D, resid2, eps=0.0, kkeep=0):
+    """The rank kept when converting a QB factorization with residual ||A - QB||_F^2 = resid2 to a
+    partial SVD with singular values D (descending): "choose a rank k ... based on the decaying
+    singular values"; truncating the SVD of B to k' terms adds exactly the
+    dropped D_j^2 to the squared error, ||A - U_k' D_k' V_k'^*||_F^2 = resid2 + sum_{j >= k'} D_j^2
+    (the SVD tail identity), so k' = the smallest rank with that error <= eps^2 (eps > 0), capped
+    by kkeep (> 0).  The sum runs from the smallest D_j up, as written."""
+    D = np.asarray(D, dtype=np.float64)
+    k = len(D)
+    kk = k
+    if eps > 0:
+        tail = float(resid2)
+        for j in range(k - 1, -1, -1):
+            nt = tail + D[j] * D[j]
+            if nt > eps * eps:
+                break
+            tail = nt
+            kk = j
+    if kkeep > 0:
+        kk = min(kk, int(kkeep))
+    return kk
+
+
+def qb_to_svd_truncated(Q, B, resid2, eps=0.0, kkeep=0):
+    """QB -> partial SVD truncated to tail_rank(D, resid2, eps, kkeep) triplets."""
+    U, D, V = qb_to_svd(Q, B)
+    kk = tail_rank(D, resid2, eps, kkeep)
+    return U[:, :kk], D[:kk], V[:, :kk]

@@ -92,7 +92,9 @@ def lib():
         L.qb_stats.argtypes = [c_ctx, vp, i64, P(i64)]
         L.qb_omega.argtypes = [c_ctx, u64, i64, i64, i64, i64, vp, i64]
         L.qb_orth.argtypes = [c_ctx, vp, i64, i64, i64]
-        L.rqb_svd.argtypes = [c_ctx, i64, P(vp), P(i64), P(vp), P(vp), P(i64)]
+        L.rqb_svd.argtypes = [c_ctx, dbl, i64, P(i64), P(vp), P(i64), P(vp), P(vp), P(i64)]
+        L.qb_svd_sweeps.argtypes = [c_ctx]
+        L.qb_svd_sweeps.restype = ctypes.c_int
         L.qb_pivoted_qr.argtypes = [c_ctx, vp, P(vp), P(i64), P(vp), P(i64)]
         L.qb_fixed_rank.argtypes = [c_ctx, vp, i64, i64, i64, i64, ctypes.c_int, u64, ctypes.c_uint, P(vp), P(i64),
                                     P(vp), P(i64), P(dbl)]
@@ -263,14 +265,18 @@ def qb_stats(ctx):
                  ms_down=a.ms_down, fallback=a.fallback) for a in arr[:n.value]]
 
 
-def rqb_svd(ctx, kkeep=0):
+def rqb_svd(ctx, kkeep=0, eps=0.0):
     """QB -> partial SVD of the context's last factorization (see include/qb.h).
-    Returns dict(U, ldu, S, V, ldv) of device pointers (context-owned)."""
+    Returns dict(kk, U, ldu, S, V, ldv) of device pointers (context-owned); kk = the rank kept."""
     U, S, V = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
-    ldu, ldv = ctypes.c_int64(), ctypes.c_int64()
-    _check(ctx, lib().rqb_svd(ctx, kkeep, ctypes.byref(U), ctypes.byref(ldu), ctypes.byref(S), ctypes.byref(V),
-                              ctypes.byref(ldv)))
-    return dict(U=U.value or 0, ldu=ldu.value, S=S.value or 0, V=V.value or 0, ldv=ldv.value)
+    ldu, ldv, kk = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(ctx, lib().rqb_svd(ctx, float(eps), int(kkeep), ctypes.byref(kk), ctypes.byref(U), ctypes.byref(ldu),
+                              ctypes.byref(S), ctypes.byref(V), ctypes.byref(ldv)))
+    return dict(kk=kk.value, U=U.value or 0, ldu=ldu.value, S=S.value or 0, V=V.value or 0, ldv=ldv.value)
+
+
+def qb_svd_sweeps(ctx):
+    return int(lib().qb_svd_sweeps(ctx))
 
 
 def qb_pivoted_qr(ctx, n):
@@ -422,23 +428,23 @@ class QB:
             Qh, R = Qh.clone(), R.clone()
         return dict(perm=r["perm"], Qh=Qh, R=R)
 
-    def svd(self, kkeep=0, copy_out=True):
+    def svd(self, kkeep=0, eps=0.0, copy_out=True):
         """Partial SVD A ~ U diag(S) V^T from the last ``factor`` (rqb_svd):
-        U m x k', S k', V n x k' with k' = kkeep if 0 < kkeep < k else k."""
+        U m x k', S k', V n x k' with k' from kkeep and / or the tail rule with eps (include/qb.h)."""
         import torch
-        r = rqb_svd(self.ctx, kkeep)  # raises QBError without a prior factorization
+        r = rqb_svd(self.ctx, kkeep, eps)  # raises QBError without a prior factorization
         m, n, k, dt = self._last
-        kk = kkeep if 0 < kkeep < k else k
+        kk = r["kk"] if k > 0 else 0
         ts = "<f8" if dt == torch.float64 else "<f4"
         if kk == 0:
             z = lambda *s: torch.zeros(*s, dtype=dt, device="cuda")  # noqa: E731
-            return dict(U=z(m, 0), S=z(0), V=z(n, 0))
+            return dict(U=z(m, 0), S=z(0), V=z(n, 0), kk=0)
         U = view_colmajor(r["U"], m, kk, r["ldu"], ts)
         S = view_colmajor(r["S"], kk, 1, kk, ts)[:, 0]
         V = view_colmajor(r["V"], n, kk, r["ldv"], ts)
         if copy_out:
             U, S, V = U.clone(), S.clone(), V.clone()
-        return dict(U=U, S=S, V=V)
+        return dict(U=U, S=S, V=V, kk=kk)
 
     def launches(self):
         return qb_kernel_launches(self.ctx)

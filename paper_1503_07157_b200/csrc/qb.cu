@@ -7,7 +7,8 @@
 // small.cuh for CholeskyQR and reductions; qrcp.cuh for QB -> pivoted QR).  The host only
 // sequences launches and reads two scalars per block (the stop test) plus the CholeskyQR status
 // words.  The post-processing entry points (rqb_svd, qb_pivoted_qr) and the fixed-rank schemes
-// (qb_fixed_rank) reuse the same kernels; the k x k SVD core of rqb_svd is cuSOLVER (dlopen).
+// (qb_fixed_rank) reuse the same kernels; the k x k SVD core of rqb_svd is a block one-sided Jacobi
+// (svd.cuh).  No solver library is used.
 #include <algorithm>
 #include <atomic>
 #include <cstdarg>
@@ -29,7 +30,6 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
 #include <nccl.h>  // types only: NCCL is loaded at run time (dlopen), never linked
-#include <cusolverDn.h>  // types only: cuSOLVER (the k x k SVD core of rqb_svd) is loaded at run time
 
 #include "../../include/qb.h"
 #include "common.cuh"
@@ -38,6 +38,7 @@
 #include "omega.cuh"
 #include "qrcp.cuh"
 #include "small.cuh"
+#include "svd.cuh"
 
 namespace {
 
@@ -90,60 +91,6 @@ NcclApi& nccl() {
   return api;
 }
 
-// ---------------------------------------------------------------- cuSOLVER (dlopen)
-// rqb_svd (NEXT-1) needs one dense SVD of a k x k matrix (k = the QB rank); that small core is
-// the library's dgesvd, every O(mk^2) / O(nk^2) step around it runs in this library's kernels.
-struct SolverApi {
-  bool tried = false, ok = false;
-  decltype(&cusolverDnCreate) create = nullptr;
-  decltype(&cusolverDnDestroy) destroy = nullptr;
-  decltype(&cusolverDnSetStream) setStream = nullptr;
-  decltype(&cusolverDnDgesvd_bufferSize) gesvdBufferSize = nullptr;
-  decltype(&cusolverDnDgesvd) gesvd = nullptr;
-  decltype(&cusolverDnCreateParams) createParams = nullptr;
-  decltype(&cusolverDnDestroyParams) destroyParams = nullptr;
-  decltype(&cusolverDnDestroyGesvdjInfo) destroyGesvdjInfo = nullptr;
-  decltype(&cusolverDnXgesvdp_bufferSize) gesvdpBufferSize = nullptr;
-  decltype(&cusolverDnXgesvdp) gesvdp = nullptr;
-  decltype(&cusolverDnCreateGesvdjInfo) createGesvdjInfo = nullptr;
-  decltype(&cusolverDnXgesvdjSetTolerance) gesvdjSetTol = nullptr;
-  decltype(&cusolverDnXgesvdjSetMaxSweeps) gesvdjSetSweeps = nullptr;
-  decltype(&cusolverDnDgesvdj_bufferSize) gesvdjBufferSize = nullptr;
-  decltype(&cusolverDnDgesvdj) gesvdj = nullptr;
-};
-
-SolverApi& solver() {
-  static SolverApi api;
-  if (api.tried) return api;
-  api.tried = true;
-  void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) h = dlopen("libcusolver.so", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) return api;
-  api.create = reinterpret_cast<decltype(&cusolverDnCreate)>(dlsym(h, "cusolverDnCreate"));
-  api.destroy = reinterpret_cast<decltype(&cusolverDnDestroy)>(dlsym(h, "cusolverDnDestroy"));
-  api.setStream = reinterpret_cast<decltype(&cusolverDnSetStream)>(dlsym(h, "cusolverDnSetStream"));
-  api.gesvdBufferSize =
-      reinterpret_cast<decltype(&cusolverDnDgesvd_bufferSize)>(dlsym(h, "cusolverDnDgesvd_bufferSize"));
-  api.gesvd = reinterpret_cast<decltype(&cusolverDnDgesvd)>(dlsym(h, "cusolverDnDgesvd"));
-#define QB_SYM(field, name) api.field = reinterpret_cast<decltype(&name)>(dlsym(h, #name))
-  QB_SYM(createParams, cusolverDnCreateParams);
-  QB_SYM(destroyParams, cusolverDnDestroyParams);
-  QB_SYM(destroyGesvdjInfo, cusolverDnDestroyGesvdjInfo);
-  QB_SYM(gesvdpBufferSize, cusolverDnXgesvdp_bufferSize);
-  QB_SYM(gesvdp, cusolverDnXgesvdp);
-  QB_SYM(createGesvdjInfo, cusolverDnCreateGesvdjInfo);
-  QB_SYM(gesvdjSetTol, cusolverDnXgesvdjSetTolerance);
-  QB_SYM(gesvdjSetSweeps, cusolverDnXgesvdjSetMaxSweeps);
-  QB_SYM(gesvdjBufferSize, cusolverDnDgesvdj_bufferSize);
-  QB_SYM(gesvdj, cusolverDnDgesvdj);
-#undef QB_SYM
-  api.ok = api.create && api.destroy && api.setStream && api.gesvdBufferSize && api.gesvd && api.createParams &&
-           api.destroyParams && api.destroyGesvdjInfo &&
-           api.gesvdpBufferSize && api.gesvdp && api.createGesvdjInfo && api.gesvdjSetTol && api.gesvdjSetSweeps &&
-           api.gesvdjBufferSize && api.gesvdj;
-  return api;
-}
-
 }  // namespace
 
 struct qb_ctx_s {
@@ -185,13 +132,18 @@ struct qb_ctx_s {
     int64_t ldq = 0, ldb = 0, kcap = 0;
   } hout;
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t cap_stream = nullptr, cap_stream2 = nullptr;  // rqb_svd: CUDA-graph capture of a Jacobi sweep
+  cudaStream_t aux_stream = nullptr;  // rqb_svd: the J updates beside the next step (no-graph mode)
+  cudaEvent_t jev[5] = {};
   cudaEvent_t ev_copy = nullptr;
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
   DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw;  // qb_pivoted_qr
   DevBuf X32, T32;  // FP32 contexts: FP32 copies of a CholeskyQR pass's X and T
   DevBuf X32b;      // FP32 contexts: RN_32 of CholeskyQR2's scratch (when the caller takes an FP32 copy)
   DevBuf Bsp;       // FP32 GEMM: a small B operand split into hi / lo
-  cusolverDnHandle_t solver = nullptr;
+  DevBuf Jx, Jj, Jpart, Jw, Jint, Jsig, Jpairs;  // rqb_svd: block one-sided Jacobi (svd.cuh)
+  int jac_pairs_nblk = 0, jac_sweeps = 0;
+  double last_r2 = 0.0;  // ||A - QB||_F^2 of the last factorization (rqb_svd's tail rule)
   int block_fallbacks = 0;
   const double* outQ = nullptr;
   const double* outB = nullptr;
@@ -1247,7 +1199,8 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
                     &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32,
-                    &ctx->Bsp,   &ctx->X32b};
+                    &ctx->Bsp,   &ctx->X32b, &ctx->Jx,    &ctx->Jj,   &ctx->Jpart, &ctx->Jw,
+                    &ctx->Jint,  &ctx->Jsig, &ctx->Jpairs};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -1258,12 +1211,16 @@ void qb_destroy(qb_ctx ctx) {
   for (auto& e : ctx->evp)
     if (e) cudaEventDestroy(e);
   if (ctx->comm) nccl().commDestroy(ctx->comm);
-  if (ctx->solver) solver().destroy(ctx->solver);
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
   }
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->cap_stream2) cudaStreamDestroy(ctx->cap_stream2);
+  if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+  for (auto& e : ctx->jev)
+    if (e) cudaEventDestroy(e);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1369,19 +1326,39 @@ qb_status qb_chol_rinv(qb_ctx ctx, const void* G, int64_t ldg, int64_t w, int64_
   return QB_OK;
 }
 
-qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_out, const void** S_out,
-                  const void** V_out, int64_t* ldv_out) {
-  // QB -> partial SVD: B̄ = Û D V^*, U = Q̄ Û.  B̄^T (n x k) = Q_B R by block
-  // Gram-Schmidt (two projections) + CholeskyQR2 per 256 columns; R = Q_B^T B̄^T; dgesvd of the
-  // k x k R = Ũ D Ṽ^T; then B̄ = R^T Q_B^T = Ṽ D (Q_B Ũ)^T, so Û = Ṽ, V = Q_B Ũ, U = Q̄ Ṽ.
+// Round-robin tournament (circle method) over nblk (even) players: step s pairs (s, nblk-1) and
+// (s+i, s-i) mod (nblk-1); every pair of blocks meets once in nblk - 1 steps.
+static std::vector<int2> round_robin(int nblk) {
+  std::vector<int2> out;
+  const int mod = nblk - 1;
+  for (int st = 0; st < mod; ++st) {
+    for (int i = 0; i < nblk / 2; ++i) {
+      int a = i == 0 ? st : (st + i) % mod;
+      int b = i == 0 ? nblk - 1 : (st - i + mod) % mod;
+      out.push_back(make_int2(std::min(a, b), std::max(a, b)));
+    }
+  }
+  return out;
+}
+
+qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const void** U_out, int64_t* ldu_out,
+                  const void** S_out, const void** V_out, int64_t* ldv_out) {
+  // QB -> partial SVD: B̄ = Û D V^*, U = Q̄ Û.
+  //  1. B̄^T (n x k) = Q_B R: block Gram-Schmidt (two projections) + CholeskyQR2 per 256 columns;
+  //  2. R = Q_B^T B̄^T (k x k);
+  //  3. SVD of R^T by block one-sided Jacobi (svd.cuh): R^T J = Û D, J orthogonal, so
+  //     B̄ = R^T Q_B^T = Û D (Q_B J)^T, i.e. V = Q_B J;
+  //  4. U = Q̄ Û, V = Q_B J on the library GEMM, for the leading k' triplets: k' = kkeep, or the
+  //     smallest k' with ||A - U_k' D_k' V_k'^*||_F^2 = r_k^2 + sum_{j > k'} D_j^2 <= eps^2 (the tail
+  //     rule: "choose a rank ... based on the decaying singular values").
   if (!ctx) return QB_ERR_INVALID_ARG;
+  if (kk_out) *kk_out = 0;
   if (ctx->last_k < 0) return fail(ctx, QB_ERR_INVALID_ARG, "rqb_svd: no factorization to convert");
-  // row shards: B̄ is replicated and U = Q̄ Ṽ is this rank's rows of U; column shards hold B̄ split
+  if (!(eps >= 0.0)) return fail(ctx, QB_ERR_INVALID_ARG, "rqb_svd: eps must be >= 0");
+  // row shards: B̄ is replicated and U = Q̄ Û is this rank's rows of U; column shards hold B̄ split
   if (ctx->nranks > 1 && !ctx->shard_rows)
     return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: column-sharded B̄ (distributed) not supported");
-  if (!solver().ok) return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: libcusolver.so.11 not loadable");
   const int64_t m = ctx->last_m, n = ctx->last_n, k = ctx->last_k;
-  const int64_t kk = (kkeep > 0 && kkeep < k) ? kkeep : k;
   QB_CUDA(cudaSetDevice(ctx->device));
   if (k == 0) {
     if (U_out) *U_out = nullptr;
@@ -1392,20 +1369,28 @@ qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_ou
     return QB_OK;
   }
   if (k > INT32_MAX / 4) return fail(ctx, QB_ERR_INVALID_ARG, "rqb_svd: k too large");
+  NvtxRange nv("rqb_svd");
   const int64_t ldn = round_up(n, 16), ldm = round_up(m, 16), ldk = round_up(k, 16), bp = round_up(kMaxB, 16);
+  const int64_t kp = round_up(k, 2 * JNB);  // Jacobi columns, padded to whole block pairs
+  const int nblk = (int)(kp / JNB), npairs = nblk / 2, nsteps = nblk - 1;
+  const int nch = (int)((k + JRC - 1) / JRC);
   QB_TRY(ensure(ctx, ctx->QB, sizeof(double) * (size_t)(ldn * k)));
   QB_TRY(ensure(ctx, ctx->R, sizeof(double) * (size_t)(ldk * k)));
   QB_TRY(ensure(ctx, ctx->Ut, sizeof(double) * (size_t)(ldk * k)));
   QB_TRY(ensure(ctx, ctx->Vt, sizeof(double) * (size_t)(ldk * k)));
   QB_TRY(ensure(ctx, ctx->Ssv, sizeof(double) * (size_t)ldk));
   QB_TRY(ensure(ctx, ctx->Wsv, sizeof(double) * (size_t)(ldk * bp)));
-  QB_TRY(ensure(ctx, ctx->Usv, sizeof(double) * (size_t)(ldm * kk)));
-  QB_TRY(ensure(ctx, ctx->Vsv, sizeof(double) * (size_t)(ldn * kk)));
   QB_TRY(ensure(ctx, ctx->T1, sizeof(double) * (size_t)(round_up(std::max(m, n), 16) * kMaxB)));
   QB_TRY(ensure(ctx, ctx->G, sizeof(double) * bp * bp));
   QB_TRY(ensure(ctx, ctx->L, sizeof(double) * (bp * bp + 8 * 32 * 32)));
   QB_TRY(ensure(ctx, ctx->Rinv, sizeof(double) * bp * bp));
   QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)(16 * ctx->num_sms)));
+  QB_TRY(ensure(ctx, ctx->Jx, sizeof(double) * (size_t)(kp * kp)));
+  QB_TRY(ensure(ctx, ctx->Jj, sizeof(double) * (size_t)(kp * kp)));
+  QB_TRY(ensure(ctx, ctx->Jpart, sizeof(double) * (size_t)npairs * nch * JPW * JPW));
+  QB_TRY(ensure(ctx, ctx->Jw, sizeof(double) * (size_t)2 * npairs * JPW * JPW));
+  QB_TRY(ensure(ctx, ctx->Jint, sizeof(int) * (size_t)(2 * npairs + 2 * kp) + 64));
+  QB_TRY(ensure(ctx, ctx->Jsig, sizeof(double) * (size_t)kp + 64));
   double* QBm = ctx->QB.d();
   const double* Bbar = ctx->Bbar.d();  // row-major k x n (ld ldb) == B̄^T column-major n x k
   QB_TRY(reset_flags(ctx));
@@ -1416,102 +1401,170 @@ qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_ou
   // 2. R = Q_B^T B̄^T (k x k, column-major)
   QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)k, (int)k, (int)n, QBm, ldn, Bbar, ctx->ldb, ctx->R.d(), ldk, false,
               nullptr));
-  // 3. R = Ũ D Ṽ^T (cuSOLVER dgesvd: Ũ -> Ut, Ṽ^T -> Vt, both column-major ld ldk)
-  if (!ctx->solver) {
-    if (solver().create(&ctx->solver) != CUSOLVER_STATUS_SUCCESS) {
-      ctx->solver = nullptr;
-      return fail(ctx, QB_ERR_CUDA, "cusolverDnCreate failed");
-    }
+  double t_front = 0.0;
+  if (debug_env("QB_JAC_TRACE")) {  // diagnostics: host time of the front end (orth of B̄^T, R)
+    const double t0 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    t_front = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    fprintf(stderr, "[rqb_svd] front end done (waited %.2f ms)\n", t_front - t0);
   }
-  if (solver().setStream(ctx->solver, ctx->stream) != CUSOLVER_STATUS_SUCCESS)
-    return fail(ctx, QB_ERR_CUDA, "cusolverDnSetStream failed");
-  // method: 0 = dgesvd (QR iteration), 1 = gesvdj (Jacobi), 2 = Xgesvdp (polar decomposition);
-  // QB_SVD selects, default below.  Ut <- Ũ (column-major); Vt <- Ṽ^T (column-major) = Ṽ row-major.
-  static const int method = getenv("QB_SVD") ? atoi(getenv("QB_SVD")) : 2;
-  int* dinfo = nullptr;
-  if (method == 0) {
-    int lwork = 0;
-    if (solver().gesvdBufferSize(ctx->solver, (int)k, (int)k, &lwork) != CUSOLVER_STATUS_SUCCESS)
-      return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvd_bufferSize failed");
-    QB_TRY(ensure(ctx, ctx->Swork, sizeof(double) * (size_t)(lwork + ldk) + 64));
-    double* work = ctx->Swork.d();
-    dinfo = reinterpret_cast<int*>(work + lwork + ldk);
-    if (solver().gesvd(ctx->solver, 'S', 'S', (int)k, (int)k, ctx->R.d(), (int)ldk, ctx->Ssv.d(), ctx->Ut.d(),
-                       (int)ldk, ctx->Vt.d(), (int)ldk, work, lwork, work + lwork, dinfo) != CUSOLVER_STATUS_SUCCESS)
-      return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvd failed");
-  } else {
-    // V-returning methods write Ṽ (column-major) into Usv's storage first, transposed below
-    QB_TRY(ensure(ctx, ctx->Usv, sizeof(double) * (size_t)std::max(ldm * kk, ldk * k)));
-    double* Vcol = ctx->Usv.d();
-    if (method == 1) {
-      gesvdjInfo_t info = nullptr;
-      if (solver().createGesvdjInfo(&info) != CUSOLVER_STATUS_SUCCESS)
-        return fail(ctx, QB_ERR_CUDA, "cusolverDnCreateGesvdjInfo failed");
-      solver().gesvdjSetTol(info, 1e-15);
-      solver().gesvdjSetSweeps(info, 100);
-      int lwork = 0;
-      if (solver().gesvdjBufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 1, (int)k, (int)k, ctx->R.d(), (int)ldk,
-                                    ctx->Ssv.d(), ctx->Ut.d(), (int)ldk, Vcol, (int)ldk, &lwork,
-                                    info) != CUSOLVER_STATUS_SUCCESS)
-        return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvdj_bufferSize failed");
-      QB_TRY(ensure(ctx, ctx->Swork, sizeof(double) * (size_t)lwork + 64));
-      double* work = ctx->Swork.d();
-      dinfo = reinterpret_cast<int*>(work + lwork);
-      const cusolverStatus_t st = solver().gesvdj(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, 1, (int)k, (int)k,
-                                                  ctx->R.d(), (int)ldk, ctx->Ssv.d(), ctx->Ut.d(), (int)ldk, Vcol,
-                                                  (int)ldk, work, lwork, dinfo, info);
-      QB_CUDA(cudaStreamSynchronize(ctx->stream));
-      solver().destroyGesvdjInfo(info);
-      if (st != CUSOLVER_STATUS_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cusolverDnDgesvdj failed");
-    } else {
-      cusolverDnParams_t params = nullptr;
-      if (solver().createParams(&params) != CUSOLVER_STATUS_SUCCESS)
-        return fail(ctx, QB_ERR_CUDA, "cusolverDnCreateParams failed");
-      size_t dbytes = 0, hbytes = 0;
-      if (solver().gesvdpBufferSize(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 1, k, k, CUDA_R_64F, ctx->R.d(),
-                                    ldk, CUDA_R_64F, ctx->Ssv.d(), CUDA_R_64F, ctx->Ut.d(), ldk, CUDA_R_64F, Vcol,
-                                    ldk, CUDA_R_64F, &dbytes, &hbytes) != CUSOLVER_STATUS_SUCCESS)
-        return fail(ctx, QB_ERR_CUDA, "cusolverDnXgesvdp_bufferSize failed");
-      QB_TRY(ensure(ctx, ctx->Swork, dbytes + 64));
-      dinfo = reinterpret_cast<int*>(static_cast<char*>(ctx->Swork.p) + ((dbytes + 15) / 16) * 16);
-      std::vector<char> hwork(std::max<size_t>(hbytes, 1));
-      double err_sigma = 0.0;
-      const cusolverStatus_t st =
-          solver().gesvdp(ctx->solver, params, CUSOLVER_EIG_MODE_VECTOR, 1, k, k, CUDA_R_64F, ctx->R.d(), ldk,
-                          CUDA_R_64F, ctx->Ssv.d(), CUDA_R_64F, ctx->Ut.d(), ldk, CUDA_R_64F, Vcol, ldk, CUDA_R_64F,
-                          ctx->Swork.p, dbytes, hwork.data(), hbytes, dinfo, &err_sigma);
-      QB_CUDA(cudaStreamSynchronize(ctx->stream));  // hwork is host scratch of this call
-      solver().destroyParams(params);
-      if (st != CUSOLVER_STATUS_SUCCESS) return fail(ctx, QB_ERR_CUDA, "cusolverDnXgesvdp failed");
-    }
-    dim3 grid((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
-    transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(Vcol, ldk, k, k, ctx->Vt.d(), ldk);
-    QB_TRY(check_launch(ctx, "transpose"));
-  }
-  ++ctx->launches;
-  // 4. U = Q̄ Ṽ: Ṽ^T column-major is Ṽ row-major (the NN kernel's N-contiguous operand)
-  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)kk, (int)k, ctx->Qbar.d(), ctx->ldq, ctx->Vt.d(), ldk,
-              ctx->Usv.d(), ldm, false, nullptr));
-  //    V = Q_B Ũ: Ũ^T row-major = Ũ transposed into R's storage
+  // 3. one-sided Jacobi on X = R^T (kp x kp, zero-padded), J = I
+  double* X = ctx->Jx.d();
+  double* Jm = ctx->Jj.d();
+  QB_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * (size_t)(kp * kp), ctx->stream));
   {
     dim3 grid((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
-    transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->Ut.d(), ldk, k, k, ctx->R.d(), ldk);
+    transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->R.d(), ldk, k, k, X, kp);  // X(c, r) = R(r, c)
     QB_TRY(check_launch(ctx, "transpose"));
+    qrcp_identity_kernel<<<(int)std::min<int64_t>((kp * kp + 255) / 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
+        Jm, kp, (int)kp);
+    QB_TRY(check_launch(ctx, "identity"));
   }
-  QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)n, (int)kk, (int)k, QBm, ldn, ctx->R.d(), ldk, ctx->Vsv.d(), ldn,
-              false, nullptr));
-  int hinfo = 0;
-  QB_CUDA(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->jac_pairs_nblk != nblk) {  // the tournament schedule, uploaded once per block count
+    const std::vector<int2> sched = round_robin(nblk);
+    QB_TRY(ensure(ctx, ctx->Jpairs, sizeof(int2) * sched.size()));
+    QB_CUDA(cudaMemcpy(ctx->Jpairs.p, sched.data(), sizeof(int2) * sched.size(), cudaMemcpyHostToDevice));
+    ctx->jac_pairs_nblk = nblk;
+  }
+  QB_SMEM_ATTR(jac_gram_kernel, JGRAM_SMEM);
+  QB_SMEM_ATTR(jac_solve_kernel, JSOLVE_SMEM);
+  QB_SMEM_ATTR(jac_update_kernel, JUPD_SMEM);
+  int* jflag = static_cast<int*>(ctx->Jint.p);
+  int* jrank = jflag + 2 * npairs;
+  auto* offmax = reinterpret_cast<unsigned long long*>(ctx->Jsig.d() + kp);
+  const int2* pairs = static_cast<const int2*>(ctx->Jpairs.p);
+  // columns are orthogonal to this relative level at convergence (above the Gram's rounding ~ sqrt(k) u)
+  // (the Gram entries carry rounding up to ~k u relative to the column norms, so the threshold scales
+  // with k; at T, k u = 3e-13)
+  const double tol = std::max(1e-14, (double)k * 0x1p-53);
+  static const int inner = debug_env("QB_JAC_INNER") > 0 ? debug_env("QB_JAC_INNER") : 1;
+  const int max_sweeps = 40;
+  int sweeps = 0;
+  double off = 1.0;
+  // One sweep = nsteps x (Gram, solve, X update) on the main stream; the J update of step s runs on a
+  // second stream beside the next step's Gram and solve (J is read by nothing else).  Δ and the flags
+  // alternate between two slots: solve s+2 reuses slot s % 2 only after J update s (event).  The sweep
+  // is captured once into a CUDA graph (private capture streams; nothing runs during capture) and
+  // replayed per sweep on the context stream.
+  if (!ctx->aux_stream) QB_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+  if (!ctx->jev[0])
+    for (auto& e : ctx->jev) QB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const int nchj = nch;
+  auto enqueue_sweep = [&](cudaStream_t st, cudaStream_t st2) -> qb_status {
+    QB_CUDA(cudaMemsetAsync(offmax, 0, sizeof(unsigned long long), st));
+    for (int s = 0; s < nsteps; ++s) {
+      const int slot = s & 1;
+      const int2* pr = pairs + (size_t)s * npairs;
+      double* Dsl = ctx->Jw.d() + (size_t)slot * npairs * JPW * JPW;
+      int* fl = jflag + slot * npairs;
+      jac_gram_kernel<<<dim3(npairs, nch), JTHREADS, JGRAM_SMEM, st>>>(X, kp, (int)k, pr, nch, ctx->Jpart.d());
+      QB_TRY(check_launch(ctx, "jac_gram"));
+      if (s >= 2) QB_CUDA(cudaStreamWaitEvent(st, ctx->jev[2 + slot], 0));  // J update s-2 read this slot
+      jac_solve_kernel<<<npairs, JST, JSOLVE_SMEM, st>>>(ctx->Jpart.d(), nch, Dsl, fl, offmax, tol, inner);
+      QB_TRY(check_launch(ctx, "jac_solve"));
+      QB_CUDA(cudaEventRecord(ctx->jev[slot], st));
+      jac_update_kernel<<<dim3(npairs, nch), JTHREADS, JUPD_SMEM, st>>>(X, kp, (int)k, pr, Dsl, fl);
+      QB_TRY(check_launch(ctx, "jac_update_x"));
+      QB_CUDA(cudaStreamWaitEvent(st2, ctx->jev[slot], 0));
+      jac_update_kernel<<<dim3(npairs, nchj), JTHREADS, JUPD_SMEM, st2>>>(Jm, kp, (int)k, pr, Dsl, fl);
+      QB_TRY(check_launch(ctx, "jac_update_j"));
+      QB_CUDA(cudaEventRecord(ctx->jev[2 + slot], st2));
+    }
+    QB_CUDA(cudaStreamWaitEvent(st, ctx->jev[2 + ((nsteps - 1) & 1)], 0));  // join the J branch
+    return QB_OK;
+  };
+  static const int no_graph = debug_env("QB_JAC_NO_GRAPH");
+  cudaGraphExec_t gexec = nullptr;
+  const int per_sweep = 4 * nsteps;
+  if (!no_graph && !debug_env("QB_DEBUG_SYNC")) {
+    if (!ctx->cap_stream) QB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    if (!ctx->cap_stream2) QB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    QB_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    // fork the second capture stream into the capture
+    cudaError_t fe = cudaEventRecord(ctx->jev[4], ctx->cap_stream);
+    if (fe == cudaSuccess) fe = cudaStreamWaitEvent(ctx->cap_stream2, ctx->jev[4], 0);
+    const qb_status cs = fe == cudaSuccess ? enqueue_sweep(ctx->cap_stream, ctx->cap_stream2) : QB_ERR_CUDA;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    if (cs != QB_OK || fe != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return cs != QB_OK ? cs : fail(ctx, QB_ERR_CUDA, "rqb_svd: graph capture fork: %s", cudaGetErrorString(fe));
+    }
+    QB_CUDA(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    QB_CUDA(ie);
+    ctx->launches -= per_sweep;  // counted again per replay below
+  } else {
+    QB_CUDA(cudaEventRecord(ctx->jev[4], ctx->stream));  // the side stream starts after the setup
+    QB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->jev[4], 0));
+  }
+  for (; sweeps < max_sweeps && off > tol; ++sweeps) {
+    if (gexec) {
+      const cudaError_t le = cudaGraphLaunch(gexec, ctx->stream);
+      if (le != cudaSuccess) {
+        cudaGraphExecDestroy(gexec);
+        QB_CUDA(le);
+      }
+      ctx->launches += per_sweep;
+    } else {
+      QB_TRY(enqueue_sweep(ctx->stream, ctx->aux_stream));
+    }
+    unsigned long long bits = 0;
+    QB_CUDA(cudaMemcpyAsync(&bits, offmax, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(&off, &bits, sizeof(off));
+    static const int trace = debug_env("QB_JAC_TRACE");
+    if (trace) {
+      const double now = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      fprintf(stderr, "[rqb_svd] sweep %d: max scaled off-diagonal %.3e, %.2f ms since the front end\n", sweeps, off,
+              now - t_front);
+    }
+  }
+  if (gexec) cudaGraphExecDestroy(gexec);
+  ctx->jac_sweeps = sweeps;
+  if (off > tol) return fail(ctx, QB_ERR_UNSUPPORTED, "rqb_svd: Jacobi did not converge in %d sweeps (off %.3g)",
+                             max_sweeps, off);
+  // sorted triplets: S descending, Û (row-major, ld ldk) = X D^-1, J (row-major, ld ldk)
+  double* sig = ctx->Jsig.d();
+  jac_norms_kernel<<<(int)((k * 32 + 255) / 256), 256, 0, ctx->stream>>>(X, kp, (int)k, (int)k, sig);
+  QB_TRY(check_launch(ctx, "jac_norms"));
+  jac_rank_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(sig, (int)k, jrank);
+  QB_TRY(check_launch(ctx, "jac_rank"));
+  jac_finish_kernel<<<(int)std::min<int64_t>((k * k + 255) / 256, 16 * ctx->num_sms), 256, 0, ctx->stream>>>(
+      X, kp, Jm, kp, (int)k, sig, jrank, ctx->Ssv.d(), ctx->Ut.d(), ldk, ctx->Vt.d(), ldk);
+  QB_TRY(check_launch(ctx, "jac_finish"));
+  // 4. the kept rank: kkeep and / or the tail rule with eps
+  int64_t kk = k;
+  if (eps > 0.0) {
+    auto* kdev = reinterpret_cast<long long*>(ctx->Jsig.d() + kp + 1);
+    jac_tail_rank_kernel<<<1, 32, 0, ctx->stream>>>(ctx->Ssv.d(), (int)k, ctx->last_r2, eps * eps, kdev);
+    QB_TRY(check_launch(ctx, "jac_tail_rank"));
+    long long kh = k;
+    QB_CUDA(cudaMemcpyAsync(&kh, kdev, sizeof(kh), cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    kk = kh;
+  }
+  if (kkeep > 0 && kkeep < kk) kk = kkeep;
+  if (kk_out) *kk_out = kk;
+  const int64_t kkc = std::max<int64_t>(kk, 1);
+  QB_TRY(ensure(ctx, ctx->Usv, sizeof(double) * (size_t)(ldm * kkc)));
+  QB_TRY(ensure(ctx, ctx->Vsv, sizeof(double) * (size_t)(ldn * kkc)));
+  if (kk > 0) {
+    QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)kk, (int)k, ctx->Qbar.d(), ctx->ldq, ctx->Ut.d(), ldk,
+                ctx->Usv.d(), ldm, false, nullptr));
+    QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)n, (int)kk, (int)k, QBm, ldn, ctx->Vt.d(), ldk, ctx->Vsv.d(), ldn,
+                false, nullptr));
+  }
   QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->h_status[4]) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "rqb_svd: CholeskyQR of B^T failed");
-  if (hinfo != 0) return fail(ctx, QB_ERR_CUDA, "rqb_svd: dgesvd info = %d", hinfo);
   const void* Up = ctx->Usv.p;
   const void* Sp = ctx->Ssv.p;
   const void* Vp = ctx->Vsv.p;
   if (ctx->dtype == QB_F32) {
-    QB_TRY(ensure(ctx, ctx->Usv32, sizeof(float) * (size_t)(ldm * kk)));
-    QB_TRY(ensure(ctx, ctx->Vsv32, sizeof(float) * (size_t)(ldn * kk)));
+    QB_TRY(ensure(ctx, ctx->Usv32, sizeof(float) * (size_t)(ldm * kkc)));
+    QB_TRY(ensure(ctx, ctx->Vsv32, sizeof(float) * (size_t)(ldn * kkc)));
     QB_TRY(ensure(ctx, ctx->Ssv32, sizeof(float) * (size_t)ldk));
     QB_TRY(launch_convert(ctx, ctx->Usv.d(), ldm, m, kk, static_cast<float*>(ctx->Usv32.p), ldm));
     QB_TRY(launch_convert(ctx, ctx->Vsv.d(), ldn, n, kk, static_cast<float*>(ctx->Vsv32.p), ldn));
@@ -1521,13 +1574,15 @@ qb_status rqb_svd(qb_ctx ctx, int64_t kkeep, const void** U_out, int64_t* ldu_ou
     Sp = ctx->Ssv32.p;
     Vp = ctx->Vsv32.p;
   }
-  if (U_out) *U_out = Up;
+  if (U_out) *U_out = kk > 0 ? Up : nullptr;
   if (ldu_out) *ldu_out = ldm;
-  if (S_out) *S_out = Sp;
-  if (V_out) *V_out = Vp;
+  if (S_out) *S_out = kk > 0 ? Sp : nullptr;
+  if (V_out) *V_out = kk > 0 ? Vp : nullptr;
   if (ldv_out) *ldv_out = ldn;
   return QB_OK;
 }
+
+int qb_svd_sweeps(qb_ctx ctx) { return ctx ? ctx->jac_sweeps : 0; }
 
 qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int64_t* ldqh_out, const void** R_out,
                         int64_t* ldr_out) {
@@ -1793,9 +1848,11 @@ qb_status qb_fixed_rank(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_t lda
   QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->h_status[4]) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "qb_fixed_rank: CholeskyQR failed even with the shift");
+  ctx->last_r2 = 0.0;  // unknown unless requested: rqb_svd's tail rule then counts the kept triplets only
   if (resid_out) {
     r = std::sqrt(ctx->h_scal[0]);
     *resid_out = r;
+    ctx->last_r2 = ctx->h_scal[0];
   }
   ctx->last_m = m;
   ctx->last_n = n;
@@ -1822,6 +1879,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     ctx->last_m = m;
     ctx->last_n = n;
     ctx->last_k = 0;
+    ctx->last_r2 = 0.0;
     if (resid_out) *resid_out = 0.0;
     if (Q_out) *Q_out = nullptr;
     if (ldq_out) *ldq_out = round_up(std::max<int64_t>(m, 1), 16);
@@ -1917,6 +1975,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
   if (resid_out) *resid_out = std::sqrt(r2_0);
   ctx->last_k = -1;
   if (r2_0 <= eps2) {
+    ctx->last_r2 = r2_0;
     ctx->last_m = m;
     ctx->last_n = n;
     ctx->last_k = 0;
@@ -2183,6 +2242,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
   }
   QB_TRY(host_copy());  // kmax reached without the stop test firing
   *k_out = ell;
+  ctx->last_r2 = r2;
   ctx->last_m = m;
   ctx->last_n = n;
   ctx->last_k = ell;

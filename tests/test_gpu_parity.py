@@ -133,7 +133,7 @@ def test_factor_parity(qbmod, ctx, case):
     for sg, ho in zip(g["stats"], o.hist):
         assert sg["ell"] == ho[0] and sg["w"] == ho[1]
         assert abs(sg["r2"] - ho[2]) <= 1e-12 * nA2
-        assert abs(sg["ei"] - sg["r2"]) <= 6 * 2.0 ** -53 * nA2 * 4
+        assert abs(sg["ei"] - sg["r2"]) <= 6 * 2.0 ** -53 * nA2   # reading R1: 6 u ||A||^2
 
 
 def test_config_C2_parity(qbmod, ctx):
@@ -253,7 +253,7 @@ def test_target_config_properties(qbmod, ctx):
     st = g["stats"]
     assert st[-1]["r2"] <= cfg.eps ** 2 < st[-2]["r2"]
     for s in st:
-        assert abs(s["ei"] - s["r2"]) <= 6 * 2.0 ** -53 * nA ** 2 * 4
+        assert abs(s["ei"] - s["r2"]) <= 6 * 2.0 ** -53 * nA ** 2   # reading R1: 6 u ||A||^2
     # sampled Ω(rows, cols) at the full size against the oracle generator
     rng = np.random.default_rng(0)
     for c0 in (0, k - cfg.b):

@@ -154,12 +154,12 @@ def test_row_shards_match_unsharded_oracle(qbmod, P, q, dt):
 
 def test_column_shards_b256_reprojection(qbmod):
     """b = 256 (the target's block size) over 2 column shards, several blocks with re-projection."""
-    A = make(1500, 1400, "exp10_25", 47)
-    o = oqb.randqb_pb(A, 1e-9, 256, 0, seed=2)
-    out = run_loopback(qbmod, A, 2, "cols", 1e-9, 256, 0, 2)
+    A = make(1500, 1400, "exp_150", 47)
+    o = oqb.randqb_pb(A, 1e-3, 256, 0, seed=2)
+    out = run_loopback(qbmod, A, 2, "cols", 1e-3, 256, 0, 2)
     k, Q, B, stats, resid = assemble(out, "cols")
-    assert len(stats) >= 2
-    check_vs_oracle(A, o, k, Q, B, stats, resid, 1e-9, False)
+    assert len(stats) >= 3
+    check_vs_oracle(A, o, k, Q, B, stats, resid, 1e-3, False)
 
 
 def test_skip_power_orth_column_shards(qbmod):

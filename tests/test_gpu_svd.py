@@ -118,3 +118,53 @@ def test_svd_fp32_context(qbmod):
     assert np.abs(V.T @ V - np.eye(k)).max() <= 1e-5
     assert np.linalg.norm((U * S) @ V.T - Q @ B) <= 1e-5 * np.linalg.norm(A64)
     np.testing.assert_allclose(S[:50], np.linalg.svd(Q @ B, compute_uv=False)[:50], rtol=1e-5)
+
+
+@pytest.mark.parametrize("m,n,kind,eps,b", [(2500, 2200, "exp_150", 1e-4, 128), (1500, 1200, "poly2", 1e-5, 64)])
+def test_svd_large_k_parity(qbmod, m, n, kind, eps, b):
+    """k > 1024: many 32-column blocks in the Jacobi tournament, graded singular values spanning
+    several decades (the tail of a QB factorization); parity with the oracle's LAPACK SVD of its
+    own factors, orthonormal U and V, the definition U D V^T = QB."""
+    A = synth.make_matrix_np(m, n, synth.sigma(kind, min(m, n)), 90 + m)
+    nA = np.linalg.norm(A)
+    o = oqb.randqb_pb(A, eps, b, 0, seed=4)
+    Uo, So, Vo = oqb.qb_to_svd(o.Q, o.B)
+    c = qbmod.QB(0)
+    f = c.factor(to_dev(A), eps, b, 0, seed=4)
+    s = c.svd()
+    sweeps = qbmod.qb_svd_sweeps(c.ctx)
+    c.close()
+    k = f["k"]
+    assert k == o.k and k >= 640
+    Q, B = f["Q"].cpu().numpy(), f["B"].cpu().numpy()
+    U, S, V = s["U"].cpu().numpy(), s["S"].cpu().numpy(), s["V"].cpu().numpy()
+    assert (np.diff(S) <= 0).all() and S[-1] > 0
+    assert np.abs(U.T @ U - np.eye(k)).max() <= 1e-12
+    assert np.abs(V.T @ V - np.eye(k)).max() <= 1e-12
+    assert np.linalg.norm((U * S) @ V.T - Q @ B) <= 1e-13 * nA
+    assert np.abs(S - So).max() <= 1e-10 * nA
+    assert 1 <= sweeps <= 20
+
+
+def test_svd_eps_tail_rule(qbmod):
+    """rqb_svd(eps): the rank kept is the tail rule's (oracle.tail_rank on the oracle's own
+    factorization: ||A - U_k' D_k' V_k'^T||^2 = ||A - QB||^2 + sum_{j > k'} D_j^2 <= eps^2,
+    PAPER.md:398-406), and the truncated triplets meet eps against the pristine A."""
+    A = synth.make_matrix_np(900, 700, synth.sigma("exp10_20", 700), 8)
+    o = oqb.randqb_pb(A, 1e-6, 32, 0, seed=1)
+    _, So, _ = oqb.qb_to_svd(o.Q, o.B)
+    c = qbmod.QB(0)
+    f = c.factor(to_dev(A), 1e-6, 32, 0, seed=1)
+    assert f["k"] == o.k
+    for eps in (1e-6, 1e-4, 1e-2, 10.0):
+        kk_o = oqb.tail_rank(So, o.hist[-1][2], eps)
+        s = c.svd(eps=eps)
+        assert s["kk"] == kk_o, (eps, s["kk"], kk_o)
+        if kk_o > 0:
+            U, S, V = s["U"].cpu().numpy(), s["S"].cpu().numpy(), s["V"].cpu().numpy()
+            assert np.linalg.norm(A - (U * S) @ V.T) <= eps * (1 + 1e-8)
+    s = c.svd(eps=1e-4, kkeep=5)       # both: the smaller rank
+    assert s["kk"] == 5
+    with pytest.raises(qbmod.QBError):
+        c.svd(eps=-1.0)
+    c.close()

@@ -269,3 +269,35 @@ def test_skip_power_orth_floors(P, floor):
     r0 = qb.randqb_pb(A, 0.0, 20, 0, seed=1, kmax=60, skip_power_orth=True)
     r1 = qb.randqb_pb(A, 0.0, 20, 0, seed=1, kmax=60)
     assert np.array_equal(r0.Q, r1.Q)
+
+
+def test_tail_rank_worked_example():
+    """diag(3, 2, 1) with an exact QB (resid 0): dropping sigma = 1 costs 1, dropping 2 as well 5
+    (the SVD tail identity); eps = 1.5 keeps 2 triplets, eps^2 = 5 (<=, reading R4) keeps 1,
+    kkeep caps, eps = 0 keeps all."""
+    D = np.array([3.0, 2.0, 1.0])
+    assert qb.tail_rank(D, 0.0, 1.5) == 2
+    assert qb.tail_rank(D, 0.0, np.sqrt(5.0) * (1 + 1e-12)) == 1
+    assert qb.tail_rank(D, 0.0, 0.999) == 3
+    assert qb.tail_rank(D, 0.0, 100.0) == 0
+    assert qb.tail_rank(D, 0.0, 1.5, kkeep=1) == 1
+    assert qb.tail_rank(D, 0.0, 0.0) == 3
+    assert qb.tail_rank(D, 1.25, 1.5) == 2       # resid^2 + 1 = 2.25 <= eps^2 = 2.25: drop sigma = 1
+    assert qb.tail_rank(D, 1.2500001, 1.5) == 3  # 2.2500001 > 2.25: keep all
+
+
+def test_truncated_svd_error_identity():
+    """||A - U_k' D_k' V_k'^*||_F^2 = ||A - QB||_F^2 + sum_{j >= k'} D_j^2 for every k' (the
+    factorization's Q is orthonormal and the SVD of B is exact up to rounding)."""
+    A = synth.make_matrix_np(300, 240, synth.sigma("exp10_20", 240), 9)
+    r = qb.randqb_pb(A, 1e-5, 16)
+    U, D, V = qb.qb_to_svd(r.Q, r.B)
+    resid2 = r.hist[-1][2]
+    nA2 = qb.frob2(A)
+    for kk in (0, 5, 37, len(D)):
+        lhs = qb.frob2(A - (U[:, :kk] * D[:kk]) @ V[:, :kk].T)
+        assert abs(lhs - (resid2 + float(np.sum(D[kk:] ** 2)))) <= 1e-13 * nA2
+    eps = np.sqrt(resid2 + np.sum(D[60:] ** 2)) * (1 + 1e-9)
+    Ut, Dt, Vt = qb.qb_to_svd_truncated(r.Q, r.B, resid2, eps)
+    assert len(Dt) == 60 and Ut.shape == (300, 60) and Vt.shape == (240, 60)
+    assert qb.frob2(A - (Ut * Dt) @ Vt.T) <= eps ** 2 * (1 + 1e-9)
