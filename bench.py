@@ -288,6 +288,16 @@ def timed_steps(step, steps, warmup, stream, ws, dev, flush=None):
     return ms, g
 
 
+def replicated_share(stats, ms):
+    """rho of SURVEY §8(e): the share of a step spent in the work column sharding replicates on every
+    rank — CholeskyQR of the m-row panels, the re-projection, and (upper bound) the power steps'
+    CholeskyQR of Z, whose Gram and products are in fact sharded — from qb_stats' phase spans."""
+    rep = sum(s["ms_orth"] + s["ms_orth_z"] + s["ms_reproj"] for s in stats)
+    return {"rho": rep / ms, "orth_ms": sum(s["ms_orth"] for s in stats),
+            "orth_z_ms": sum(s["ms_orth_z"] for s in stats), "reproj_ms": sum(s["ms_reproj"] for s in stats),
+            "power_gemm_ms": sum(s["ms_power"] for s in stats)}
+
+
 RECORD_STEPS = {"C1": 20, "C2": 20, "C3": 5, "C4": 5, "C5": 2, "T1": 3, "T": 5}
 
 
@@ -320,6 +330,7 @@ def run_record(name, args, ws, rank, local):
            "k": k, "blocks": len(st), "status": g["status"], "m": inp["m_global"], "n": inp["n_global"],
            "b": cfg.b, "q": cfg.q, "eps": cfg.eps, "dtype": cfg.dtype, "steps": steps, "warmup": 3, "n_gpus": ws,
            "sharding": "single" if ws == 1 else ("rows" if inp["rows"] else "cols"), "l2": l2_note}
+    rec["replicated_share"] = replicated_share(st, ms)
     if f32:
         tf, tf_src = tf32x3_peak()
         hbm, _ = hbm_peak()
@@ -506,6 +517,7 @@ def run_ours(args, cfg):
                 "seconds_to_eps": ms * 1e-3,
                 "frac_fp64_peak": None if f32 else value / ws / (peak * 1e3),
                 "frac_cublas_dgemm": (value / ws / (cublas * 1e3)) if (cublas and not f32) else None,
+                "replicated_share": replicated_share(stats, ms),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "post": post,
                 "configs": records, "clocks": clk}
         print(json.dumps(line), flush=True)

@@ -79,6 +79,10 @@ typedef struct {
   double ms_down;     /* A -= Q_i B_i with the fused ||A^(i)||_F^2 epilogue (line (10))     */
   int32_t fallback;   /* number of shifted-CholeskyQR fallbacks taken in this block         */
   int32_t reserved;
+  double ms_orth;     /* CholeskyQR of m-row panels (lines (3), (6), (8)): replicated on column shards */
+  double ms_orth_z;   /* CholeskyQR of the power steps' n-row Z (line (5))                   */
+  double ms_reproj;   /* re-projection products W = Qbar^* Q_i, Q_i -= Qbar W (line (8))     */
+  double ms_power;    /* power-step products Z = A^* Q_i, Y = A Z (lines (5), (6)) + their sums */
 } qb_block_stats;
 
 /* Create a context on CUDA device `device` computing in `dtype`.  `cuda_stream` is a

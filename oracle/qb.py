@@ -186,3 +186,59 @@ def qb_to_svd_truncated(Q, B, resid2, eps=0.0, kkeep=0):
     U, D, V = qb_to_svd(Q, B)
     kk = tail_rank(D, resid2, eps, kkeep)
     return U[:, :kk], D[:kk], V[:, :kk]
+
+
+def pivoted_qr(B):
+    """QB -> partial pivoted QR: B P = Q~ R by Householder QR with column
+    pivoting, step by step in LAPACK dlaqp2's order (the order the paper's "pivoted QR" refers to,
+    P:242-279): at step i the pivot is the FIRST column of largest partial norm; the reflector
+    H_i = I - tau v v^T has v_0 = 1 and beta = -sign(alpha) ||x|| (dlarfg; tau = 0 when x below the
+    diagonal is zero); it is applied to the trailing columns; the partial norms are downdated with
+    R(i, j) and recomputed from scratch when the sqrt(eps) cancellation test fires.
+    Returns (perm, Q~ (l x l), R (l x n upper trapezoidal)): column j of B P is column perm[j] of B."""
+    R = np.array(B, dtype=np.float64, copy=True)
+    l, n = R.shape
+    kmin = min(l, n)
+    perm = np.arange(n)
+    vn1 = np.sqrt(np.sum(R * R, axis=0))
+    vn2 = vn1.copy()
+    tol3z = np.sqrt(np.finfo(np.float64).eps)
+    taus, vs = [], []
+    for i in range(kmin):
+        p = i + int(np.argmax(vn1[i:]))
+        if p != i:
+            R[:, [i, p]] = R[:, [p, i]]
+            perm[[i, p]] = perm[[p, i]]
+            vn1[p], vn2[p] = vn1[i], vn2[i]
+        alpha = R[i, i]
+        x = R[i + 1:, i].copy()
+        xnorm = float(np.sqrt(np.sum(x * x)))
+        v = np.zeros(l - i)
+        v[0] = 1.0
+        if xnorm == 0.0:
+            tau, beta = 0.0, alpha
+        else:
+            beta = -np.copysign(np.hypot(alpha, xnorm), alpha)
+            tau = (beta - alpha) / beta
+            v[1:] = x / (alpha - beta)
+        R[i, i] = beta
+        R[i + 1:, i] = 0.0
+        if tau != 0.0 and i + 1 < n:
+            w = v @ R[i:, i + 1:]
+            R[i:, i + 1:] -= tau * np.outer(v, w)
+        for j in range(i + 1, n):
+            if vn1[j] != 0.0:
+                temp = max(0.0, 1.0 - (abs(R[i, j]) / vn1[j]) ** 2)
+                temp2 = temp * (vn1[j] / vn2[j]) ** 2
+                if temp2 <= tol3z:
+                    vn1[j] = float(np.sqrt(np.sum(R[i + 1:, j] ** 2))) if i + 1 < l else 0.0
+                    vn2[j] = vn1[j]
+                else:
+                    vn1[j] *= np.sqrt(temp)
+        taus.append(tau)
+        vs.append(v)
+    Q = np.eye(l)
+    for i in range(kmin - 1, -1, -1):          # Q~ = H_0 H_1 ... H_{k-1}, applied to the identity
+        v = vs[i]
+        Q[i:, :] -= taus[i] * np.outer(v, v @ Q[i:, :])
+    return perm, Q, np.triu(R)

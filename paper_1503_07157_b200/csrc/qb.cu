@@ -123,6 +123,10 @@ struct qb_ctx_s {
   cudaEvent_t ev_gap = nullptr;  // QB_HOST_TIMING: end of the previous block (device gap between blocks)
   cudaEvent_t evp[6] = {};  // phase events: sketch, B, downdate (begin/end)
   std::vector<qb_block_stats> stats;
+  // per-block phase spans (qb_block_stats ms_orth ... ms_power): an event pool reused every block
+  std::vector<cudaEvent_t> tev;
+  std::vector<int> tcat;
+  int tused = 0;
   int64_t last_m = 0, last_n = 0, last_k = -1;  // the last qb_factor (for rqb_svd); -1: none
   // qb_factor_host: each finished block's Q_i / B_i is copied to these pinned host buffers on a
   // copy stream while the next block computes
@@ -483,7 +487,9 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   int bn = 64;
   p.tiles_n = (N + bn - 1) / bn;
   int splits = 1;
-  if (allow_split) splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 296);
+  // tiny products (< 2^22 multiply-adds) run unsplit: the split-K reduction launch would cost more
+  if (allow_split && (double)M * N * K >= 4194304.0)
+    splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 296);
   const bool subtract = epi == EPI_SUB_COL;
   static const int wide_env = debug_env("QB_WIDE_DOWNDATE");  // experiment: 1 = 128-wide tiles
   if (subtract && splits == 1 && wide_env > 0 && N >= 2048) {
@@ -677,7 +683,8 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   p.tiles_n = (N + bn - 1) / bn;
   const int tiles = p.tiles_m * p.tiles_n;
   int splits = 1;
-  if (allow_split && epi != TF_SUB_COL) splits = choose_splits(tiles, p.nkt, ctx->num_sms, 148);
+  if (allow_split && epi != TF_SUB_COL && (double)M * N * K >= 4194304.0)
+    splits = choose_splits(tiles, p.nkt, ctx->num_sms, 148);
   p.kt_per_split = (p.nkt + splits - 1) / splits;
   splits = std::max(1, (p.nkt + p.kt_per_split - 1) / p.kt_per_split);
   p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
@@ -786,6 +793,31 @@ qb_status reduce_to_scal(qb_ctx ctx, int64_t nparts, int slot) {
   return check_launch(ctx, "reduce");
 }
 
+// ---------------------------------------------------------------- phase spans (qb_stats)
+enum { PH_ORTH = 0, PH_ORTH_Z = 1, PH_REPROJ = 2, PH_POWER = 3, PH_N = 4 };
+qb_status span_mark(qb_ctx ctx, int cat) {  // cat >= 0 opens a span, cat < 0 closes the open one
+  if ((size_t)ctx->tused >= ctx->tev.size()) {
+    cudaEvent_t e = nullptr;
+    QB_CUDA(cudaEventCreate(&e));
+    ctx->tev.push_back(e);
+    ctx->tcat.push_back(-1);
+  }
+  ctx->tcat[ctx->tused] = cat;
+  QB_CUDA(cudaEventRecord(ctx->tev[ctx->tused], ctx->stream));
+  ++ctx->tused;
+  return QB_OK;
+}
+// after the block's host synchronisation: the spans' device times per category
+void span_collect(qb_ctx ctx, double* acc) {
+  for (int c = 0; c < PH_N; ++c) acc[c] = 0.0;
+  for (int i = 0; i + 1 < ctx->tused; i += 2) {
+    float ms = 0.f;
+    if (ctx->tcat[i] >= 0 && cudaEventElapsedTime(&ms, ctx->tev[i], ctx->tev[i + 1]) == cudaSuccess)
+      acc[ctx->tcat[i]] += ms;
+  }
+  ctx->tused = 0;
+}
+
 // ---------------------------------------------------------------- CholeskyQR2
 int* status_dev(qb_ctx ctx) { return static_cast<int*>(ctx->status.p); }
 
@@ -861,6 +893,15 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
 qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
                   bool row_distributed = false, bool single = false, const float* src32 = nullptr,
                   int64_t lds32 = 0, float* dst32 = nullptr, int64_t ldd32 = 0) {
+  static const int no_small = debug_env("QB_NO_SMALL_ORTH");
+  if (!row_distributed && !no_small && w <= SCQR_MAX_W && m * w <= SCQR_MAX_ELEMS) {
+    // the whole CholeskyQR2 (all passes, fallback included) in one CTA for a small panel
+    QB_SMEM_ATTR(small_cholqr_kernel, SCQR_SMEM);
+    const double ns_tol2 = ctx->dtype == QB_F32 ? 1e-8 : 1e-16;
+    small_cholqr_kernel<<<1, SCQR_THREADS, SCQR_SMEM, ctx->stream>>>(src, lds, dst, ldd, (int)m, w, single ? 1 : 0,
+                                                                     ns_tol2, 1e-13, status_dev(ctx), dst32, ldd32);
+    return check_launch(ctx, "small_cholqr");
+  }
   const int64_t ldt = round_up(m, 16);
   double* T = ctx->T1.d();
   float* T32 = nullptr;  // RN_32(T) when the caller wants dst32
@@ -1209,6 +1250,8 @@ void qb_destroy(qb_ctx ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev_gap) cudaEventDestroy(ctx->ev_gap);
   for (auto& e : ctx->evp)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->tev)
     if (e) cudaEventDestroy(e);
   if (ctx->comm) nccl().commDestroy(ctx->comm);
   if (ctx->copy_stream) {
@@ -2028,6 +2071,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
       }
     }
     QB_TRY(reset_flags(ctx));
+    ctx->tused = 0;
     double* Qbar = ctx->Qbar.d();
     double* Qi = Qbar + ell * ctx->ldq;
     double* Bi = ctx->Bbar.d() + ell * ctx->ldb;
@@ -2088,7 +2132,9 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     const bool reproj_follows = ell > 0 && !(flags & QB_NO_REPROJ) && !full_first_orth;
     // orth of a freshly sketched Y into Q_i (and Q̄32_i on FP32 contexts)
     auto orth_y_into = [&](bool single) -> qb_status {
-      return cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh, single, Y32, ldm, Qi32, ctx->ldq);
+      QB_TRY(span_mark(ctx, PH_ORTH));
+      QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh, single, Y32, ldm, Qi32, ctx->ldq));
+      return span_mark(ctx, -1);
     };
     auto orth_y = [&]() -> qb_status { return orth_y_into(reproj_follows); };
     phase("K4 orth + K3 power steps");
@@ -2099,20 +2145,28 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     // lines (4)-(7): power steps on the residual (reading R9), orth after each application (R10)
     const bool skip_orth = (flags & QB_SKIP_POWER_ORTH) != 0;
     for (int j = 0; j < q && skip_orth; ++j) {  // NEXT-3: Y = A (A^* Y), orth once
+      QB_TRY(span_mark(ctx, PH_POWER));
       QB_TRY(adjoint(ctx->Y.d(), ldm));
       if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->Z.d(), (size_t)(ldn * w)));  // Z = sum_p A_p^T Y_p
       QB_TRY(transpose_z());
       QB_TRY(sketch(ctx->Zt.p));
       if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
+      QB_TRY(span_mark(ctx, -1));
     }
     if (skip_orth && q > 0) QB_TRY(orth_y());
     for (int j = 0; j < q && !skip_orth; ++j) {
+      QB_TRY(span_mark(ctx, PH_POWER));
       QB_TRY(adjoint(Qi, ctx->ldq));
       if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->Z.d(), (size_t)(ldn * w)));  // Z = sum_p A_p^T Q_p
+      QB_TRY(span_mark(ctx, -1));
+      QB_TRY(span_mark(ctx, PH_ORTH_Z));
       QB_TRY(cholqr2(ctx, ctx->Z.d(), ldn, ctx->Z.d(), ldn, n, (int)w, colsh));
+      QB_TRY(span_mark(ctx, -1));
+      QB_TRY(span_mark(ctx, PH_POWER));
       QB_TRY(transpose_z());
       QB_TRY(sketch(ctx->Zt.p));
       if (!rowsh) QB_TRY(allreduce_sum(ctx, ctx->Y.d(), (size_t)(ldm * w)));
+      QB_TRY(span_mark(ctx, -1));
       if (j == q - 1) QB_TRY(orth_y());  // the last orth of the power scheme, line (6)
       else QB_TRY(orth_y_into(false));
     }
@@ -2120,6 +2174,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     if (ell > 0 && !(flags & QB_NO_REPROJ)) {
       phase("K5 re-projection + orth");
       QB_TRY(ensure(ctx, ctx->W, sizeof(double) * (size_t)(ell * bp)));
+      QB_TRY(span_mark(ctx, PH_REPROJ));
       if (is_f32) {  // on the FP32 copies: W = Q̄^T Q_i, Q_i -= Q̄ W (3xTF32), then orth in FP64
         QB_TRY(ensure(ctx, ctx->W32, sizeof(float) * (size_t)(ell * bp)));
         QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_ROW, (int)ell, (int)w, (int)m, Qbar32, ctx->ldq, Qi32, ctx->ldq,
@@ -2137,14 +2192,20 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
           convert_dual_kernel<<<grid, 256, 0, ctx->stream>>>(Qi32, ctx->ldq, m, w, ctx->Y.d(), ldm, X32, ldm);
           QB_TRY(check_launch(ctx, "convert_dual"));
         }
+        QB_TRY(span_mark(ctx, -1));
+        QB_TRY(span_mark(ctx, PH_ORTH));
         QB_TRY(cholqr2(ctx, ctx->Y.d(), ldm, Qi, ctx->ldq, m, (int)w, rowsh, false, X32, ldm, Qi32, ctx->ldq));
+        QB_TRY(span_mark(ctx, -1));
       } else {
         QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)ell, (int)w, (int)m, Qbar, ctx->ldq, Qi, ctx->ldq, ctx->W.d(),
                     bp, false, nullptr));
         if (rowsh) QB_TRY(allreduce_sum(ctx, ctx->W.d(), (size_t)(ell * bp)));  // W = sum_p Q̄_p^T Q_p
         QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)ell, Qbar, ctx->ldq, ctx->W.d(), bp, Qi,
                     ctx->ldq, false, nullptr));
+        QB_TRY(span_mark(ctx, -1));
+        QB_TRY(span_mark(ctx, PH_ORTH));
         QB_TRY(cholqr2(ctx, Qi, ctx->ldq, Qi, ctx->ldq, m, (int)w, rowsh));
+        QB_TRY(span_mark(ctx, -1));
       }
     }
     // line (9): B_i = Q_i^* A^(i-1) (reading R12), row-major into B̄, plus sum B_i^2 (the EI term)
@@ -2228,6 +2289,14 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     cudaEventElapsedTime(&ms, ctx->evp[4], ctx->evp[5]);
     st.ms_down = ms;
     st.fallback = ctx->block_fallbacks;
+    {
+      double acc[PH_N];
+      span_collect(ctx, acc);
+      st.ms_orth = acc[PH_ORTH];
+      st.ms_orth_z = acc[PH_ORTH_Z];
+      st.ms_reproj = acc[PH_REPROJ];
+      st.ms_power = acc[PH_POWER];
+    }
     ctx->stats.push_back(st);
     if (ctx->hout.Q && ell - w < ctx->hout.kcap) {
       // the block is final (host-synchronised above): its Q_i columns and B_i rows go to the

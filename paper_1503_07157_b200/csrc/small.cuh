@@ -593,3 +593,174 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
 }
 
 }  // namespace qbk
+
+namespace qbk {
+
+// ---------------------------------------------------------------- whole CholeskyQR2 in one CTA
+// For panels small enough to live in one CTA's shared memory (m w <= SCQR_MAX_ELEMS, w <= 64) the
+// complete orth of cholqr2() — every pass, the Newton-Schulz shortcut (reading R7b), the shifted
+// CholeskyQR3 fallback (R8) and the single-pass variant (R11b) — runs in ONE launch instead of the
+// ~15 launches (Gram GEMM + split-K reduction, cluster Cholesky, X T GEMM, gated copies, gated
+// fallback passes) of the general path, whose fixed costs dominate small problems (BASELINE
+// configs[0]: 400 x 10 panels).  Same algorithm and flags as the general path:
+//   pass:  G = X^T X (fixed-order sums);  ||G - I||_F^2 <= ns_tol2 -> T = I - (G - I)/2;  else
+//          G = R^T R (pivot d > tol G_jj, else retry with the shift 11 (m w + w (w+1)) u tr(G)),
+//          T = R^-1;  X <- X T.
+//   order: pass 1; pass 2 if pass 1 factorised (or, single, if it shifted); two more passes if a
+//          factorisation was shifted.  status[3] counts shifted retries, status[4] flags failure.
+constexpr int SCQR_MAX_W = 64;
+constexpr int SCQR_MAX_ELEMS = 8192;
+constexpr int SCQR_THREADS = 512;
+constexpr int SCQR_GLD = SCQR_MAX_W + 1;
+constexpr int SCQR_SMEM = (2 * SCQR_MAX_ELEMS + 2 * SCQR_MAX_W * SCQR_GLD) * 8;
+
+__global__ void __launch_bounds__(SCQR_THREADS) small_cholqr_kernel(const double* __restrict__ src, int64_t lds,
+                                                                    double* __restrict__ dst, int64_t ldd, int m,
+                                                                    int w, int single, double ns_tol2, double tol,
+                                                                    int* __restrict__ status,
+                                                                    float* __restrict__ dst32, int64_t ldd32) {
+  extern __shared__ double scq[];
+  double* X = scq;                         // [w][m] column-major (ld m)
+  double* X2 = X + SCQR_MAX_ELEMS;         // product buffer
+  double* G = X2 + SCQR_MAX_ELEMS;         // [w][GLD] Gram / Cholesky factor L (lower)
+  double* T = G + SCQR_MAX_W * SCQR_GLD;   // [w][GLD] T (row-major: T[i * GLD + j])
+  __shared__ double red[2][SCQR_THREADS / 32];
+  __shared__ double s_e2, s_tr, s_shift;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int idx = t; idx < m * w; idx += SCQR_THREADS) X[idx] = src[(idx / m) * lds + idx % m];
+  __syncthreads();
+  bool f_fact = false, f_shift = false, f_fail = false;
+  int fallbacks = 0;
+  auto pass = [&]() {
+    // G = X^T X: one warp per entry (i <= j), fixed-order warp sums
+    for (int e = warp; e < w * w; e += SCQR_THREADS / 32) {
+      const int i = e / w, j = e % w;
+      if (i > j) continue;
+      const double* xi = X + i * m;
+      const double* xj = X + j * m;
+      double s = 0.0;
+      for (int r = lane; r < m; r += 32) s = fma(xi[r], xj[r], s);
+      s = warp_sum(s);
+      if (lane == 0) {
+        G[i * SCQR_GLD + j] = s;
+        G[j * SCQR_GLD + i] = s;
+      }
+    }
+    __syncthreads();
+    double e2 = 0.0, tr = 0.0;
+    for (int e = t; e < w * w; e += SCQR_THREADS) {
+      const int i = e / w, j = e % w;
+      const double d = G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0);
+      e2 = fma(d, d, e2);
+      if (i == j) tr += G[i * SCQR_GLD + j];
+    }
+    e2 = warp_sum(e2);
+    tr = warp_sum(tr);
+    if (lane == 0) {
+      red[0][warp] = e2;
+      red[1][warp] = tr;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double a = 0.0, b = 0.0;
+      for (int k = 0; k < SCQR_THREADS / 32; ++k) {
+        a += red[0][k];
+        b += red[1][k];
+      }
+      s_e2 = a;
+      s_tr = b;
+      s_shift = 11.0 * (static_cast<double>(m) * w + static_cast<double>(w) * (w + 1)) * 0x1p-53 * b;
+    }
+    __syncthreads();
+    if (ns_tol2 >= 0.0 && s_e2 <= ns_tol2) {  // Newton-Schulz step towards the polar factor
+      for (int e = t; e < w * w; e += SCQR_THREADS) {
+        const int i = e / w, j = e % w;
+        T[i * SCQR_GLD + j] = (i == j ? 1.0 : 0.0) - 0.5 * (G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0));
+      }
+    } else {
+      f_fact = true;
+      // keep the Gram's diagonal (pivot tolerance reference) and the Gram itself for the retry in T
+      for (int e = t; e < w * w; e += SCQR_THREADS) T[(e / w) * SCQR_GLD + e % w] = G[(e / w) * SCQR_GLD + e % w];
+      __syncthreads();
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        if (attempt == 1) {
+          for (int e = t; e < w * w; e += SCQR_THREADS) {
+            const int i = e / w, j = e % w;
+            G[i * SCQR_GLD + j] = T[i * SCQR_GLD + j] + (i == j ? s_shift : 0.0);
+          }
+        }
+        if (t == 0) s_bad = 0;
+        __syncthreads();
+        // right-looking Cholesky G = L L^T in place (lower triangle)
+        for (int j = 0; j < w; ++j) {
+          if (t == 0) {
+            const double d = G[j * SCQR_GLD + j];
+            if (!(d > tol * T[j * SCQR_GLD + j]) || !(d > 0.0)) s_bad = 1;
+            G[j * SCQR_GLD + j] = sqrt(fmax(d, 0.0));
+          }
+          __syncthreads();
+          if (s_bad) break;
+          const double ljj = G[j * SCQR_GLD + j];
+          for (int i = j + 1 + t; i < w; i += SCQR_THREADS) G[i * SCQR_GLD + j] /= ljj;
+          __syncthreads();
+          for (int e = t; e < (w - j - 1) * (w - j - 1); e += SCQR_THREADS) {
+            const int i = j + 1 + e / (w - j - 1), k = j + 1 + e % (w - j - 1);
+            if (k <= i) G[i * SCQR_GLD + k] = fma(-G[i * SCQR_GLD + j], G[k * SCQR_GLD + j], G[i * SCQR_GLD + k]);
+          }
+          __syncthreads();
+        }
+        if (!s_bad) break;
+        if (attempt == 0) {
+          f_shift = true;
+          ++fallbacks;
+        } else {
+          f_fail = true;
+        }
+        __syncthreads();
+      }
+      if (f_fail) return;
+      // T = R^-1 = L^-T: column c of L^-1 by forward substitution (thread c), stored transposed
+      for (int c = t; c < w; c += SCQR_THREADS) {
+        for (int i = 0; i < w; ++i) {
+          if (i < c) {
+            T[c * SCQR_GLD + i] = 0.0;  // (L^-1)(i, c) = 0 above the diagonal -> T(c, i) = 0
+            continue;
+          }
+          double v = (i == c) ? 1.0 : 0.0;
+          for (int k = c; k < i; ++k) v = fma(-G[i * SCQR_GLD + k], T[c * SCQR_GLD + k], v);
+          T[c * SCQR_GLD + i] = v / G[i * SCQR_GLD + i];
+        }
+      }
+      // T now holds (L^-1)^T row c = column c of L^-1, i.e. T[c][i] = L^-1(i, c) = R^-1(c, i)
+    }
+    __syncthreads();
+    // X <- X T  (T row-major: T[i][j]; upper triangular after a factorisation, full after NS)
+    for (int e = t; e < m * w; e += SCQR_THREADS) {
+      const int j = e / m, r = e % m;
+      double s = 0.0;
+      for (int i = 0; i < w; ++i) s = fma(X[i * m + r], T[i * SCQR_GLD + j], s);
+      X2[j * m + r] = s;
+    }
+    __syncthreads();
+    for (int e = t; e < m * w; e += SCQR_THREADS) X[e] = X2[e];
+    __syncthreads();
+  };
+  pass();
+  if (!f_fail && (single ? f_shift : f_fact)) pass();
+  if (!f_fail && f_shift) {
+    pass();
+    if (!f_fail) pass();
+  }
+  if (t == 0) {
+    if (fallbacks) atomicAdd(status + 3, fallbacks);
+    if (f_fail) status[4] = 1;
+  }
+  for (int idx = t; idx < m * w; idx += SCQR_THREADS) {
+    const int j = idx / m, r = idx % m;
+    dst[j * ldd + r] = X[idx];
+    if (dst32 != nullptr) dst32[j * ldd32 + r] = static_cast<float>(X[idx]);
+  }
+}
+
+}  // namespace qbk

@@ -301,3 +301,37 @@ def test_truncated_svd_error_identity():
     Ut, Dt, Vt = qb.qb_to_svd_truncated(r.Q, r.B, resid2, eps)
     assert len(Dt) == 60 and Ut.shape == (300, 60) and Vt.shape == (240, 60)
     assert qb.frob2(A - (Ut * Dt) @ Vt.T) <= eps ** 2 * (1 + 1e-9)
+
+
+def test_pivoted_qr_hand_examples():
+    """Two cases worked by hand from LAPACK dlaqp2's definitions:
+    B = [[3, 1], [4, 2]]: no pivoting, alpha = 3, ||x|| = 5, beta = -5, tau = 1.6, v = (1, 0.5),
+    column 2 -> (1, 2) - 1.6 * 2 * (1, 0.5) = (-2.2, 0.4); the last reflector is trivial (tau = 0).
+    B = [[1, 0, 2], [0, 3, 0]]: pivot column 1 (norm 3), alpha = 0 -> beta = -3, tau = 1, v = (1, 1);
+    the trailing columns become (0, -1) and (0, -2), so step 2 pivots original column 2."""
+    perm, Q, R = qb.pivoted_qr(np.array([[3.0, 1.0], [4.0, 2.0]]))
+    assert list(perm) == [0, 1]
+    np.testing.assert_allclose(R, [[-5.0, -2.2], [0.0, 0.4]], atol=1e-15)
+    perm, Q, R = qb.pivoted_qr(np.array([[1.0, 0.0, 2.0], [0.0, 3.0, 0.0]]))
+    assert list(perm) == [1, 2, 0]
+    np.testing.assert_allclose(R, [[-3.0, 0.0, 0.0], [0.0, -2.0, -1.0]], atol=1e-15)
+    np.testing.assert_allclose(Q, [[0.0, -1.0], [-1.0, 0.0]], atol=1e-15)
+
+
+@pytest.mark.parametrize("shape", [(40, 70), (64, 64), (30, 200)])
+def test_pivoted_qr_matches_lapack_and_invariants(shape):
+    """An independent implementation (LAPACK dgeqp3 through scipy) picks the same permutation and
+    the same R up to row signs; B P = Q~ R, Q~ orthogonal, |R_ii| non-increasing."""
+    import scipy.linalg
+    l, n = shape
+    rng = np.random.default_rng(l + n)
+    B = (rng.standard_normal((l, n)) * np.exp(-np.arange(n) / 30.0)[None, :])[:, rng.permutation(n)]
+    perm, Q, R = qb.pivoted_qr(B)
+    Ql, Rl, pl = scipy.linalg.qr(B, mode="economic", pivoting=True)
+    assert list(perm[:min(l, n)]) == list(pl[:min(l, n)])
+    s = np.sign(np.diag(R)) * np.sign(np.diag(Rl))
+    np.testing.assert_allclose(s[:, None] * R[:min(l, n)], Rl, atol=1e-12 * np.linalg.norm(B))
+    np.testing.assert_allclose(B[:, perm], Q @ R, atol=1e-12 * np.linalg.norm(B))
+    np.testing.assert_allclose(Q.T @ Q, np.eye(l), atol=1e-13)
+    d = np.abs(np.diag(R))
+    assert (np.diff(d) <= 1e-12 * d[0]).all()
