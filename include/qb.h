@@ -61,8 +61,11 @@ enum {
                            "A^(j) can overwrite A^(j-1)"); requires lda even and A 16-byte
                            aligned, otherwise an internal copy is made anyway.              */
   QB_NO_REPROJ = 2u,    /* skip line (3')/(8) — for demonstrating P:684-696 only            */
-  QB_SKIP_POWER_ORTH = 4u /* q >= 1: Y = A (A^* Y) q times, one orth per block (P:915-931,
+  QB_SKIP_POWER_ORTH = 4u, /* q >= 1: Y = A (A^* Y) q times, one orth per block (P:915-931,
                              the blocked "skip re-orthonormalization" variant, NEXT-3)     */
+  QB_FORCE_GENERAL = 8u   /* diagnostics/tests: never take the one-launch small-problem path
+                             (FP64 A of at most 262144 entries that fits one cluster's shared
+                             memory, b <= 64); the result is the same loop either way       */
 };
 
 /* Per-block record (qb_stats).  r2 is the directly computed ||A^(i)||_F^2 (the stop test,

@@ -36,6 +36,7 @@ QB_LOOPBACK_MAX_RANKS = 8
 QB_OVERWRITE_A = 1
 QB_NO_REPROJ = 2
 QB_SKIP_POWER_ORTH = 4
+QB_FORCE_GENERAL = 8
 
 
 class QBError(RuntimeError):

@@ -38,6 +38,7 @@
 #include "omega.cuh"
 #include "qrcp.cuh"
 #include "small.cuh"
+#include "small_loop.cuh"
 #include "svd.cuh"
 
 namespace {
@@ -146,6 +147,7 @@ struct qb_ctx_s {
   DevBuf X32b;      // FP32 contexts: RN_32 of CholeskyQR2's scratch (when the caller takes an FP32 copy)
   DevBuf Bsp;       // FP32 GEMM: a small B operand split into hi / lo
   DevBuf Jx, Jj, Jpart, Jw, Jint, Jsig, Jpairs;  // rqb_svd: block one-sided Jacobi (svd.cuh)
+  DevBuf Srec, Strace;  // small_loop: results and per-block records; phase trace
   int jac_pairs_nblk = 0, jac_sweeps = 0;
   double last_r2 = 0.0;  // ||A - QB||_F^2 of the last factorization (rqb_svd's tail rule)
   int block_fallbacks = 0;
@@ -487,9 +489,7 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   int bn = 64;
   p.tiles_n = (N + bn - 1) / bn;
   int splits = 1;
-  // tiny products (< 2^22 multiply-adds) run unsplit: the split-K reduction launch would cost more
-  if (allow_split && (double)M * N * K >= 4194304.0)
-    splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 296);
+  if (allow_split) splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 296);
   const bool subtract = epi == EPI_SUB_COL;
   static const int wide_env = debug_env("QB_WIDE_DOWNDATE");  // experiment: 1 = 128-wide tiles
   if (subtract && splits == 1 && wide_env > 0 && N >= 2048) {
@@ -683,8 +683,7 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   p.tiles_n = (N + bn - 1) / bn;
   const int tiles = p.tiles_m * p.tiles_n;
   int splits = 1;
-  if (allow_split && epi != TF_SUB_COL && (double)M * N * K >= 4194304.0)
-    splits = choose_splits(tiles, p.nkt, ctx->num_sms, 148);
+  if (allow_split && epi != TF_SUB_COL) splits = choose_splits(tiles, p.nkt, ctx->num_sms, 148);
   p.kt_per_split = (p.nkt + splits - 1) / splits;
   splits = std::max(1, (p.nkt + p.kt_per_split - 1) / p.kt_per_split);
   p.raster_m_fast = p.tiles_m <= p.tiles_n ? 1 : 0;
@@ -1086,6 +1085,81 @@ qb_status init_comm(qb_ctx ctx, int rank, int nranks, const void* nccl_unique_id
   return QB_OK;
 }
 
+// The small-problem path (small_loop.cuh): the whole loop in one cluster launch when A fits in the
+// cluster's shared memory.  Returns QB_ERR_UNSUPPORTED (not an error: the caller takes the general
+// path) when the problem is not eligible.
+struct SmallPlan {
+  SmallLoopArgs a{};
+  int cl = 0;
+  size_t smem = 0;
+};
+
+bool small_plan(qb_ctx ctx, int64_t m, int64_t n, int64_t b, int q, int64_t kmax, SmallPlan* plan) {
+  if (m * n > 262144 || b > SCQR_MAX_W) return false;
+  int max_smem = 0;
+  if (cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) != cudaSuccess)
+    return false;
+  const size_t budget = (size_t)max_smem - 3072;  // static shared memory of the kernel and its helpers
+  static const int force_cl = debug_env("QB_SMALL_CL");
+  for (int cl : {8, 16}) {
+    if (force_cl && cl != force_cl) continue;
+    const int64_t mr = (m + cl - 1) / cl, nr = (n + cl - 1) / cl;
+    int64_t off = 0;
+    auto take = [&](int64_t cnt) {
+      const int64_t o = off;
+      off += (cnt + 1) / 2 * 2;
+      return (int)o;
+    };
+    SmallLoopArgs& a = plan->a;
+    a.oA = take(m * nr);
+    a.oOm = take(nr * b);
+    a.oYp = take(m * b);
+    a.oYs = take(mr * b);
+    a.oZs = take(q > 0 ? nr * b : 0);
+    a.oX2 = take(std::max(mr, nr) * b);
+    a.oGp = take(b * SCQR_GLD);
+    a.oG = take(b * SCQR_GLD);
+    a.oT = take(b * SCQR_GLD);
+    a.oWp = take(kmax * b);
+    a.oWr = take((kmax * b + cl - 1) / cl);
+    a.oQc = take(mr * kmax);
+    a.oBc = take(b * nr);
+    const size_t bytes = (size_t)off * 8;
+    int nclusters = 0;
+    if (bytes <= budget) {
+      // the cluster must be schedulable (16 CTAs of this size need a GPC with 16 free SMs)
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(cl, 1, 1);
+      lc.blockDim = dim3(SL_THREADS, 1, 1);
+      lc.dynamicSmemBytes = bytes;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cl;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      lc.attrs = attr;
+      lc.numAttrs = 1;
+      if (cudaFuncSetAttribute(small_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess ||
+          (cl > 8 && cudaFuncSetAttribute(small_loop_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) ||
+          cudaOccupancyMaxActiveClusters(&nclusters, small_loop_kernel, &lc) != cudaSuccess || nclusters < 1) {
+        const cudaError_t e = cudaGetLastError();  // clear a non-sticky launch-configuration error
+        if (debug_env("QB_SMALL_TRACE"))
+          fprintf(stderr, "[small_loop] cluster of %d not schedulable (%zu B): %s, %d clusters\n", cl, bytes,
+                  cudaGetErrorString(e), nclusters);
+        continue;
+      }
+    }
+    if (bytes <= budget) {
+      a.mr = (int)mr;
+      a.nr = (int)nr;
+      plan->cl = cl;
+      plan->smem = bytes;
+      return true;
+    }
+  }
+  return false;
+}
+
 qb_status publish_outputs(qb_ctx ctx, int64_t m, int64_t n, int64_t k, const void** Q_out, int64_t* ldq_out,
                           const void** B_out, int64_t* ldb_out) {
   const void* Qp = ctx->Qbar.p;
@@ -1241,7 +1315,7 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
                     &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32,
                     &ctx->Bsp,   &ctx->X32b, &ctx->Jx,    &ctx->Jj,   &ctx->Jpart, &ctx->Jw,
-                    &ctx->Jint,  &ctx->Jsig, &ctx->Jpairs};
+                    &ctx->Jint,  &ctx->Jsig, &ctx->Jpairs, &ctx->Srec, &ctx->Strace};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -1944,6 +2018,114 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
   const int64_t m_glob = (rowsh && ctx->nranks > 1) ? ctx->m_global : m;
   const int64_t kmax_eff = (kmax <= 0) ? std::min(m_glob, n_glob) : std::min(kmax, std::min(m_glob, n_glob));
   QB_CUDA(cudaSetDevice(ctx->device));
+
+  // ---- small problems: the whole loop in one cluster launch (small_loop.cuh)
+  static const int no_small_loop = debug_env("QB_NO_SMALL_LOOP");
+  SmallPlan plan;
+  if (!no_small_loop && !is_f32 && !ctx->dist && !(flags & (QB_SKIP_POWER_ORTH | QB_FORCE_GENERAL)) &&
+      small_plan(ctx, m, n, b, q, kmax_eff, &plan)) {
+    NvtxRange nv("small_loop (whole factorization)");
+    const bool overwrite = (flags & QB_OVERWRITE_A) != 0;
+    QB_TRY(grow_factors(ctx, m, n, kmax_eff, kmax_eff));
+    const int64_t nrec = (kmax_eff + b - 1) / b;
+    QB_TRY(ensure(ctx, ctx->Srec, sizeof(double) * (size_t)(4 * nrec + 8)));
+    SmallLoopArgs& a = plan.a;
+    a.A = static_cast<const double*>(Ain);
+    a.lda = lda;
+    a.Aout = overwrite ? static_cast<double*>(Ain) : nullptr;
+    a.ldo = lda;
+    a.m = (int)m;
+    a.n = (int)n;
+    a.b = (int)b;
+    a.q = q;
+    a.kmax = (int)kmax_eff;
+    a.reproj = (flags & QB_NO_REPROJ) ? 0 : 1;
+    a.full_first = debug_env("QB_FULL_FIRST_ORTH") ? 1 : 0;
+    a.eps2 = eps * eps;
+    a.ns_tol2 = 1e-16;
+    a.tol = 1e-13;
+    a.seed = seed;
+    a.Qbar = ctx->Qbar.d();
+    a.ldq = ctx->ldq;
+    a.Bbar = ctx->Bbar.d();
+    a.ldb = ctx->ldb;
+    a.out = ctx->Srec.d();
+    a.rec = ctx->Srec.d() + 8;
+    a.K = ctx->omega_consts;
+    QB_CUDA(cudaFuncSetAttribute(small_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
+    static const int trace = debug_env("QB_SMALL_TRACE");
+    a.trace = nullptr;
+    if (trace) {
+      QB_TRY(ensure(ctx, ctx->Strace, 32 * sizeof(unsigned long long)));
+      QB_CUDA(cudaMemsetAsync(ctx->Strace.p, 0, 32 * sizeof(unsigned long long), ctx->stream));
+      a.trace = static_cast<unsigned long long*>(ctx->Strace.p);
+    }
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(plan.cl, 1, 1);
+    lc.blockDim = dim3(SL_THREADS, 1, 1);
+    lc.dynamicSmemBytes = plan.smem;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = plan.cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    QB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    QB_CUDA(cudaLaunchKernelEx(&lc, small_loop_kernel, a));
+    QB_TRY(check_launch(ctx, "small_loop"));
+    QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    std::vector<double> hrec((size_t)(4 * nrec + 8));
+    QB_CUDA(cudaMemcpyAsync(hrec.data(), ctx->Srec.p, sizeof(double) * hrec.size(), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    QB_TRY(stream_wait(ctx));
+    const double r2_0 = hrec[0], r2 = hrec[1];
+    const int64_t k = (int64_t)hrec[2], nblk = (int64_t)hrec[5];
+    if (trace) {
+      unsigned long long tr[32];
+      QB_CUDA(cudaMemcpy(tr, ctx->Strace.p, sizeof(tr), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[small_loop] cluster %d CTAs, %zu B smem; block 2 phases (us):", plan.cl, plan.smem);
+      for (int i = 1; i < 12; ++i) fprintf(stderr, " %d:%.1f", i, tr[i] && tr[i - 1] ? (tr[i] - tr[i - 1]) * 1e-3 : -1.0);
+      fprintf(stderr, "; first orth pass (us):");
+      for (int i = 13; i < 19; ++i) fprintf(stderr, " %d:%.1f", i, tr[i] && tr[i - 1] ? (tr[i] - tr[i - 1]) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+    ctx->outQ = nullptr;
+    ctx->outB = nullptr;
+    if (!std::isfinite(r2_0)) return fail(ctx, QB_ERR_INVALID_ARG, "A contains NaN or Inf");
+    if (hrec[4] != 0.0) return fail(ctx, QB_ERR_ORTH_BREAKDOWN, "CholeskyQR failed even with the shift");
+    float total = 0.f;
+    cudaEventElapsedTime(&total, ctx->ev0, ctx->ev1);
+    for (int64_t i = 0; i < nblk; ++i) {
+      qb_block_stats st{};
+      st.ell = (int64_t)hrec[8 + 4 * i];
+      st.w = (int64_t)hrec[8 + 4 * i + 1];
+      st.r2 = hrec[8 + 4 * i + 2];
+      st.ei = hrec[8 + 4 * i + 3];
+      st.ms = total / (double)nblk;  // one launch for all blocks: the mean
+      st.fallback = i == nblk - 1 ? (int32_t)hrec[3] : 0;
+      ctx->stats.push_back(st);
+    }
+    ctx->block_fallbacks = (int)hrec[3];
+    if (resid_out) *resid_out = std::sqrt(r2);
+    if (!std::isfinite(r2)) return fail(ctx, QB_ERR_CUDA, "non-finite residual");
+    if (ctx->hout.Q && k > 0) {  // qb_factor_host: the factors to the caller's host buffers
+      const int64_t kc = std::min(k, ctx->hout.kcap);
+      QB_CUDA(cudaMemcpy2DAsync(ctx->hout.Q, ctx->hout.ldq * 8, ctx->Qbar.p, ctx->ldq * 8, m * 8, kc,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      QB_CUDA(cudaMemcpy2DAsync(ctx->hout.B, ctx->hout.ldb * 8, ctx->Bbar.p, ctx->ldb * 8, n * 8, kc,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      QB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    *k_out = k;
+    ctx->last_m = m;
+    ctx->last_n = n;
+    ctx->last_k = k;
+    ctx->last_r2 = r2;
+    QB_TRY(publish_outputs(ctx, m, n, k, Q_out, ldq_out, B_out, ldb_out));
+    return r2 <= eps * eps ? QB_OK : QB_NOT_CONVERGED;
+  }
 
   // ---- residual workspace A^(0) = A (A^(j) overwrites A^(j-1), :112)
   // FP32 contexts ("FP32 path"): the residual stays FP32 and its contractions run

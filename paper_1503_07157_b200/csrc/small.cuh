@@ -608,11 +608,149 @@ namespace qbk {
 //          T = R^-1;  X <- X T.
 //   order: pass 1; pass 2 if pass 1 factorised (or, single, if it shifted); two more passes if a
 //          factorisation was shifted.  status[3] counts shifted retries, status[4] flags failure.
+// The pieces are device functions of one CTA (all its threads call them) so that the cluster
+// loop of small_loop.cuh runs the same arithmetic on a row-distributed panel.
 constexpr int SCQR_MAX_W = 64;
 constexpr int SCQR_MAX_ELEMS = 8192;
 constexpr int SCQR_THREADS = 512;
 constexpr int SCQR_GLD = SCQR_MAX_W + 1;
 constexpr int SCQR_SMEM = (2 * SCQR_MAX_ELEMS + 2 * SCQR_MAX_W * SCQR_GLD) * 8;
+
+// G (w x w, ld SCQR_GLD, symmetric) = P^T P for the column-major rows x w panel P (ld): one warp
+// per entry i <= j, fixed-order warp sums.  Ends with __syncthreads.
+__device__ __forceinline__ void scq_gram(const double* P, int ld, int rows, int w, double* G) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int e = warp; e < w * w; e += nwarps) {
+    const int i = e / w, j = e % w;
+    if (i > j) continue;
+    const double* xi = P + static_cast<int64_t>(i) * ld;
+    const double* xj = P + static_cast<int64_t>(j) * ld;
+    double s = 0.0;
+    for (int r = lane; r < rows; r += 32) s = fma(xi[r], xj[r], s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      G[i * SCQR_GLD + j] = s;
+      G[j * SCQR_GLD + i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// T (w x w, row-major, ld SCQR_GLD) from the full Gram G of an m_rows-row panel: the Newton-Schulz
+// step when ||G - I||_F^2 <= ns_tol2, else R^-1 of G = R^T R with the shifted retry.  Updates the
+// pass flags (factorised, shifted, fallback count); returns true on failure (both attempts broke
+// down).  G is overwritten.  Uniform across the CTA; ends with __syncthreads.
+__device__ bool scq_factor(double* G, double* T, int w, double m_rows, double ns_tol2, double tol, bool& f_fact,
+                           bool& f_shift, int& fallbacks) {
+  __shared__ double red[2][32];
+  __shared__ double s_e2, s_shift;
+  __shared__ int s_bad;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nthr = blockDim.x;
+  double e2 = 0.0, tr = 0.0;
+  for (int e = t; e < w * w; e += nthr) {
+    const int i = e / w, j = e % w;
+    const double d = G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0);
+    e2 = fma(d, d, e2);
+    if (i == j) tr += G[i * SCQR_GLD + j];
+  }
+  e2 = warp_sum(e2);
+  tr = warp_sum(tr);
+  if (lane == 0) {
+    red[0][warp] = e2;
+    red[1][warp] = tr;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < (nthr >> 5); ++k) {
+      a += red[0][k];
+      b += red[1][k];
+    }
+    s_e2 = a;
+    s_shift = 11.0 * (m_rows * w + static_cast<double>(w) * (w + 1)) * 0x1p-53 * b;
+  }
+  __syncthreads();
+  if (ns_tol2 >= 0.0 && s_e2 <= ns_tol2) {  // Newton-Schulz step towards the polar factor
+    for (int e = t; e < w * w; e += nthr) {
+      const int i = e / w, j = e % w;
+      T[i * SCQR_GLD + j] = (i == j ? 1.0 : 0.0) - 0.5 * (G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0));
+    }
+    __syncthreads();
+    return false;
+  }
+  f_fact = true;
+  // T keeps the Gram (pivot tolerance reference, and the retry's input)
+  for (int e = t; e < w * w; e += nthr) T[(e / w) * SCQR_GLD + e % w] = G[(e / w) * SCQR_GLD + e % w];
+  __syncthreads();
+  bool failed = false;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (attempt == 1) {
+      for (int e = t; e < w * w; e += nthr) {
+        const int i = e / w, j = e % w;
+        G[i * SCQR_GLD + j] = T[i * SCQR_GLD + j] + (i == j ? s_shift : 0.0);
+      }
+    }
+    if (t == 0) s_bad = 0;
+    __syncthreads();
+    // right-looking Cholesky G = L L^T in place (lower triangle)
+    for (int j = 0; j < w; ++j) {
+      if (t == 0) {
+        const double d = G[j * SCQR_GLD + j];
+        if (!(d > tol * T[j * SCQR_GLD + j]) || !(d > 0.0)) s_bad = 1;
+        G[j * SCQR_GLD + j] = sqrt(fmax(d, 0.0));
+      }
+      __syncthreads();
+      if (s_bad) break;
+      const double ljj = G[j * SCQR_GLD + j];
+      for (int i = j + 1 + t; i < w; i += nthr) G[i * SCQR_GLD + j] /= ljj;
+      __syncthreads();
+      const int nt = w - j - 1;
+      for (int e = t; e < nt * nt; e += nthr) {
+        const int i = j + 1 + e / nt, k = j + 1 + e % nt;
+        if (k <= i) G[i * SCQR_GLD + k] = fma(-G[i * SCQR_GLD + j], G[k * SCQR_GLD + j], G[i * SCQR_GLD + k]);
+      }
+      __syncthreads();
+    }
+    const bool bad = s_bad != 0;
+    __syncthreads();
+    if (!bad) break;
+    if (attempt == 0) {
+      f_shift = true;
+      ++fallbacks;
+    } else {
+      failed = true;
+    }
+  }
+  if (failed) return true;
+  // T = R^-1 = L^-T: column c of L^-1 by forward substitution (thread c); T[c][i] = L^-1(i, c) = R^-1(c, i)
+  for (int c = t; c < w; c += nthr) {
+    for (int i = 0; i < w; ++i) {
+      if (i < c) {
+        T[c * SCQR_GLD + i] = 0.0;
+        continue;
+      }
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) v = fma(-G[i * SCQR_GLD + k], T[c * SCQR_GLD + k], v);
+      T[c * SCQR_GLD + i] = v / G[i * SCQR_GLD + i];
+    }
+  }
+  __syncthreads();
+  return false;
+}
+
+// P <- P T for the column-major rows x w panel P (ld), through the scratch X2 (ld rows).
+__device__ __forceinline__ void scq_apply(double* P, int ld, int rows, int w, const double* T, double* X2) {
+  const int t = threadIdx.x, nthr = blockDim.x;
+  for (int e = t; e < rows * w; e += nthr) {
+    const int j = e / rows, r = e % rows;
+    double s = 0.0;
+    for (int i = 0; i < w; ++i) s = fma(P[static_cast<int64_t>(i) * ld + r], T[i * SCQR_GLD + j], s);
+    X2[e] = s;
+  }
+  __syncthreads();
+  for (int e = t; e < rows * w; e += nthr) P[static_cast<int64_t>(e / rows) * ld + e % rows] = X2[e];
+  __syncthreads();
+}
 
 __global__ void __launch_bounds__(SCQR_THREADS) small_cholqr_kernel(const double* __restrict__ src, int64_t lds,
                                                                     double* __restrict__ dst, int64_t ldd, int m,
@@ -623,128 +761,16 @@ __global__ void __launch_bounds__(SCQR_THREADS) small_cholqr_kernel(const double
   double* X = scq;                         // [w][m] column-major (ld m)
   double* X2 = X + SCQR_MAX_ELEMS;         // product buffer
   double* G = X2 + SCQR_MAX_ELEMS;         // [w][GLD] Gram / Cholesky factor L (lower)
-  double* T = G + SCQR_MAX_W * SCQR_GLD;   // [w][GLD] T (row-major: T[i * GLD + j])
-  __shared__ double red[2][SCQR_THREADS / 32];
-  __shared__ double s_e2, s_tr, s_shift;
-  __shared__ int s_bad;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double* T = G + SCQR_MAX_W * SCQR_GLD;   // [w][GLD] T (row-major)
+  const int t = threadIdx.x;
   for (int idx = t; idx < m * w; idx += SCQR_THREADS) X[idx] = src[(idx / m) * lds + idx % m];
   __syncthreads();
   bool f_fact = false, f_shift = false, f_fail = false;
   int fallbacks = 0;
   auto pass = [&]() {
-    // G = X^T X: one warp per entry (i <= j), fixed-order warp sums
-    for (int e = warp; e < w * w; e += SCQR_THREADS / 32) {
-      const int i = e / w, j = e % w;
-      if (i > j) continue;
-      const double* xi = X + i * m;
-      const double* xj = X + j * m;
-      double s = 0.0;
-      for (int r = lane; r < m; r += 32) s = fma(xi[r], xj[r], s);
-      s = warp_sum(s);
-      if (lane == 0) {
-        G[i * SCQR_GLD + j] = s;
-        G[j * SCQR_GLD + i] = s;
-      }
-    }
-    __syncthreads();
-    double e2 = 0.0, tr = 0.0;
-    for (int e = t; e < w * w; e += SCQR_THREADS) {
-      const int i = e / w, j = e % w;
-      const double d = G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0);
-      e2 = fma(d, d, e2);
-      if (i == j) tr += G[i * SCQR_GLD + j];
-    }
-    e2 = warp_sum(e2);
-    tr = warp_sum(tr);
-    if (lane == 0) {
-      red[0][warp] = e2;
-      red[1][warp] = tr;
-    }
-    __syncthreads();
-    if (t == 0) {
-      double a = 0.0, b = 0.0;
-      for (int k = 0; k < SCQR_THREADS / 32; ++k) {
-        a += red[0][k];
-        b += red[1][k];
-      }
-      s_e2 = a;
-      s_tr = b;
-      s_shift = 11.0 * (static_cast<double>(m) * w + static_cast<double>(w) * (w + 1)) * 0x1p-53 * b;
-    }
-    __syncthreads();
-    if (ns_tol2 >= 0.0 && s_e2 <= ns_tol2) {  // Newton-Schulz step towards the polar factor
-      for (int e = t; e < w * w; e += SCQR_THREADS) {
-        const int i = e / w, j = e % w;
-        T[i * SCQR_GLD + j] = (i == j ? 1.0 : 0.0) - 0.5 * (G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0));
-      }
-    } else {
-      f_fact = true;
-      // keep the Gram's diagonal (pivot tolerance reference) and the Gram itself for the retry in T
-      for (int e = t; e < w * w; e += SCQR_THREADS) T[(e / w) * SCQR_GLD + e % w] = G[(e / w) * SCQR_GLD + e % w];
-      __syncthreads();
-      for (int attempt = 0; attempt < 2; ++attempt) {
-        if (attempt == 1) {
-          for (int e = t; e < w * w; e += SCQR_THREADS) {
-            const int i = e / w, j = e % w;
-            G[i * SCQR_GLD + j] = T[i * SCQR_GLD + j] + (i == j ? s_shift : 0.0);
-          }
-        }
-        if (t == 0) s_bad = 0;
-        __syncthreads();
-        // right-looking Cholesky G = L L^T in place (lower triangle)
-        for (int j = 0; j < w; ++j) {
-          if (t == 0) {
-            const double d = G[j * SCQR_GLD + j];
-            if (!(d > tol * T[j * SCQR_GLD + j]) || !(d > 0.0)) s_bad = 1;
-            G[j * SCQR_GLD + j] = sqrt(fmax(d, 0.0));
-          }
-          __syncthreads();
-          if (s_bad) break;
-          const double ljj = G[j * SCQR_GLD + j];
-          for (int i = j + 1 + t; i < w; i += SCQR_THREADS) G[i * SCQR_GLD + j] /= ljj;
-          __syncthreads();
-          for (int e = t; e < (w - j - 1) * (w - j - 1); e += SCQR_THREADS) {
-            const int i = j + 1 + e / (w - j - 1), k = j + 1 + e % (w - j - 1);
-            if (k <= i) G[i * SCQR_GLD + k] = fma(-G[i * SCQR_GLD + j], G[k * SCQR_GLD + j], G[i * SCQR_GLD + k]);
-          }
-          __syncthreads();
-        }
-        if (!s_bad) break;
-        if (attempt == 0) {
-          f_shift = true;
-          ++fallbacks;
-        } else {
-          f_fail = true;
-        }
-        __syncthreads();
-      }
-      if (f_fail) return;
-      // T = R^-1 = L^-T: column c of L^-1 by forward substitution (thread c), stored transposed
-      for (int c = t; c < w; c += SCQR_THREADS) {
-        for (int i = 0; i < w; ++i) {
-          if (i < c) {
-            T[c * SCQR_GLD + i] = 0.0;  // (L^-1)(i, c) = 0 above the diagonal -> T(c, i) = 0
-            continue;
-          }
-          double v = (i == c) ? 1.0 : 0.0;
-          for (int k = c; k < i; ++k) v = fma(-G[i * SCQR_GLD + k], T[c * SCQR_GLD + k], v);
-          T[c * SCQR_GLD + i] = v / G[i * SCQR_GLD + i];
-        }
-      }
-      // T now holds (L^-1)^T row c = column c of L^-1, i.e. T[c][i] = L^-1(i, c) = R^-1(c, i)
-    }
-    __syncthreads();
-    // X <- X T  (T row-major: T[i][j]; upper triangular after a factorisation, full after NS)
-    for (int e = t; e < m * w; e += SCQR_THREADS) {
-      const int j = e / m, r = e % m;
-      double s = 0.0;
-      for (int i = 0; i < w; ++i) s = fma(X[i * m + r], T[i * SCQR_GLD + j], s);
-      X2[j * m + r] = s;
-    }
-    __syncthreads();
-    for (int e = t; e < m * w; e += SCQR_THREADS) X[e] = X2[e];
-    __syncthreads();
+    scq_gram(X, m, m, w, G);
+    f_fail = scq_factor(G, T, w, static_cast<double>(m), ns_tol2, tol, f_fact, f_shift, fallbacks);
+    if (!f_fail) scq_apply(X, m, m, w, T, X2);
   };
   pass();
   if (!f_fail && (single ? f_shift : f_fact)) pass();

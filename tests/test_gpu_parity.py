@@ -452,3 +452,49 @@ def test_orth_fp32_context(qbmod):
     Qo = oqb.orth(X.astype(np.float64))
     assert np.abs(Q.T @ Q - np.eye(100)).max() <= 1e-6
     assert np.abs(Q - Qo).max() <= 1e-6
+
+
+@pytest.mark.parametrize("case", [("C1", 400, 300, "exp10_20", 1e-6, 10, 0), ("C1q1", 400, 300, "exp10_20", 1e-6, 10, 1),
+                                  ("ragged", 333, 517, "exp10_25", 1e-7, 17, 0), ("q2", 300, 200, "poly2", 1e-5, 24, 2),
+                                  ("b64", 500, 400, "exp10_25", 1e-8, 64, 0), ("b1", 120, 90, "exp10_20", 1e-3, 1, 0)],
+                         ids=lambda c: c[0])
+def test_small_loop_matches_general_path_and_oracle(qbmod, ctx, case):
+    """The one-launch cluster path (small_loop.cuh) for problems that fit in shared memory runs the
+    same loop as the general path: both against the oracle (k, products, per-block r^2) and
+    against each other (QB_FORCE_GENERAL)."""
+    name, m, n, kind, eps, b, q = case
+    A, _ = make(m, n, kind, 2000 + m)
+    o = oqb.randqb_pb(A, eps, b, q, seed=7)
+    g_small = ctx.factor(to_dev(A), eps, b, q, seed=7)
+    g_gen = ctx.factor(to_dev(A), eps, b, q, seed=7, flags=qbmod.QB_FORCE_GENERAL)
+    nA2 = np.linalg.norm(A) ** 2
+    for g in (g_small, g_gen):
+        check_parity(A, g, o, eps)
+        assert len(g["stats"]) == len(o.hist)
+        for sg, ho in zip(g["stats"], o.hist):
+            assert sg["ell"] == ho[0] and sg["w"] == ho[1]
+            assert abs(sg["r2"] - ho[2]) <= 1e-12 * nA2
+            assert abs(sg["ei"] - sg["r2"]) <= 6 * 2.0 ** -53 * nA2
+    d = np.hstack([g_small["Q"].cpu().numpy(), g_gen["Q"].cpu().numpy()]) @ \
+        np.vstack([g_small["B"].cpu().numpy(), -g_gen["B"].cpu().numpy()])
+    assert np.linalg.norm(d) <= 1e-12 * np.sqrt(nA2)
+    # bitwise reproducible from call to call
+    g2 = ctx.factor(to_dev(A), eps, b, q, seed=7)
+    assert torch.equal(g2["Q"], g_small["Q"]) and torch.equal(g2["B"], g_small["B"])
+
+
+def test_small_loop_overwrite_and_host_entry(qbmod, ctx):
+    """QB_OVERWRITE_A leaves the residual in A; qb_factor_host returns the same factors."""
+    A, _ = make(300, 200, "exp10_25", 5)
+    Ad = to_dev(A)
+    g = ctx.factor(Ad, 1e-6, 16, overwrite=True)
+    Qg, Bg = g["Q"].cpu().numpy(), g["B"].cpu().numpy()
+    assert np.linalg.norm(Ad.cpu().numpy() - (A - Qg @ Bg)) <= 1e-12 * np.linalg.norm(A)
+    Ah = np.asfortranarray(A)
+    k = g["k"]
+    Qh = np.full((k, 300), np.nan)
+    Bh = np.full((k, 200), np.nan)
+    r = qbmod.qb_factor_host(ctx.ctx, Ah.ctypes.data, 300, 200, 300, 1e-6, 16, 0, 1, 0, Qh.ctypes.data, 300,
+                             Bh.ctypes.data, 200, k)
+    assert r["k"] == k
+    assert np.array_equal(Qh.T, Qg) and np.array_equal(Bh, Bg)
