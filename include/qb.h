@@ -86,6 +86,8 @@ typedef struct {
   double ms_orth_z;   /* CholeskyQR of the power steps' n-row Z (line (5))                   */
   double ms_reproj;   /* re-projection products W = Qbar^* Q_i, Q_i -= Qbar W (line (8))     */
   double ms_power;    /* power-step products Z = A^* Q_i, Y = A Z (lines (5), (6)) + their sums */
+  double kappa_r;     /* kappa-proxy: max R_jj / min R_jj of the block's first CholeskyQR
+                         factorization (= the conditioning of the sketch Y_i; 0 if none ran)      */
 } qb_block_stats;
 
 /* Create a context on CUDA device `device` computing in `dtype`.  `cuda_stream` is a

@@ -50,7 +50,7 @@ class BlockStats(ctypes.Structure):
                 ("ei", ctypes.c_double), ("ms", ctypes.c_double), ("ms_sketch", ctypes.c_double),
                 ("ms_bmat", ctypes.c_double), ("ms_down", ctypes.c_double), ("fallback", ctypes.c_int32),
                 ("reserved", ctypes.c_int32), ("ms_orth", ctypes.c_double), ("ms_orth_z", ctypes.c_double),
-                ("ms_reproj", ctypes.c_double), ("ms_power", ctypes.c_double)]
+                ("ms_reproj", ctypes.c_double), ("ms_power", ctypes.c_double), ("kappa_r", ctypes.c_double)]
 
 
 class QBDist(ctypes.Structure):
@@ -265,7 +265,7 @@ def qb_stats(ctx):
     _check(ctx, lib().qb_stats(ctx, ctypes.cast(arr, ctypes.c_void_p), n.value, ctypes.byref(n)))
     return [dict(ell=a.ell, w=a.w, r2=a.r2, ei=a.ei, ms=a.ms, ms_sketch=a.ms_sketch, ms_bmat=a.ms_bmat,
                  ms_down=a.ms_down, fallback=a.fallback, ms_orth=a.ms_orth, ms_orth_z=a.ms_orth_z,
-                 ms_reproj=a.ms_reproj, ms_power=a.ms_power) for a in arr[:n.value]]
+                 ms_reproj=a.ms_reproj, ms_power=a.ms_power, kappa_r=a.kappa_r) for a in arr[:n.value]]
 
 
 def rqb_svd(ctx, kkeep=0, eps=0.0):

@@ -148,6 +148,7 @@ struct qb_ctx_s {
   DevBuf Bsp;       // FP32 GEMM: a small B operand split into hi / lo
   DevBuf Jx, Jj, Jpart, Jw, Jint, Jsig, Jpairs;  // rqb_svd: block one-sided Jacobi (svd.cuh)
   DevBuf Srec, Strace;  // small_loop: results and per-block records; phase trace
+  DevBuf Jq2, Jm2;      // rqb_svd QR preconditioning (experiment)
   int jac_pairs_nblk = 0, jac_sweeps = 0;
   double last_r2 = 0.0;  // ||A - QB||_F^2 of the last factorization (rqb_svd's tail rule)
   int block_fallbacks = 0;
@@ -829,7 +830,7 @@ qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) 
   // (step error <= 7.5e-9, below FP32 rounding; reading R18c)
   const double ns_tol2 = !ns ? -1.0 : (ctx->dtype == QB_F32 ? 1e-8 : 1e-16);
   chol_cluster_kernel<<<CHOL_CTAS, CHOL_THREADS, CHOL_SMEM, ctx->stream>>>(
-      ctx->G.d(), ld, w, m_rows, ctx->Rinv.d(), ld, status_dev(ctx), 1e-13, ns_tol2, gate);
+      ctx->G.d(), ld, w, m_rows, ctx->Rinv.d(), ld, status_dev(ctx), 1e-13, ns_tol2, gate, ctx->scal.d() + 4);
   return check_launch(ctx, "chol");
 }
 
@@ -898,7 +899,8 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
     QB_SMEM_ATTR(small_cholqr_kernel, SCQR_SMEM);
     const double ns_tol2 = ctx->dtype == QB_F32 ? 1e-8 : 1e-16;
     small_cholqr_kernel<<<1, SCQR_THREADS, SCQR_SMEM, ctx->stream>>>(src, lds, dst, ldd, (int)m, w, single ? 1 : 0,
-                                                                     ns_tol2, 1e-13, status_dev(ctx), dst32, ldd32);
+                                                                     ns_tol2, 1e-13, status_dev(ctx), dst32, ldd32,
+                                                                     ctx->scal.d() + 4);
     return check_launch(ctx, "small_cholqr");
   }
   const int64_t ldt = round_up(m, 16);
@@ -952,9 +954,10 @@ qb_status orth_blocked(qb_ctx ctx, double* X, int64_t ldx, int64_t m, int64_t l)
 
 bool skip_orth_flag(unsigned flags) { return (flags & QB_SKIP_POWER_ORTH) != 0; }
 
+// the block's device flags, and scal[4..5]: its kappa-proxy (max / min R diagonal of the first factorization)
 qb_status reset_flags(qb_ctx ctx) {
-  zero_ints_kernel<<<1, 32, 0, ctx->stream>>>(status_dev(ctx), 8);
-  return check_launch(ctx, "zero_flags");
+  reset_block_kernel<<<1, 32, 0, ctx->stream>>>(status_dev(ctx), ctx->scal.d() + 4);
+  return check_launch(ctx, "reset_block");
 }
 
 // kind 0: FP64 Ω; 1: FP32 Ω (qb_omega on an FP32 context); 2: FP64 buffer holding RN_32(Ω).
@@ -1315,7 +1318,7 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
                     &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32,
                     &ctx->Bsp,   &ctx->X32b, &ctx->Jx,    &ctx->Jj,   &ctx->Jpart, &ctx->Jw,
-                    &ctx->Jint,  &ctx->Jsig, &ctx->Jpairs, &ctx->Srec, &ctx->Strace};
+                    &ctx->Jint,  &ctx->Jsig, &ctx->Jpairs, &ctx->Srec, &ctx->Strace, &ctx->Jq2, &ctx->Jm2};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -1525,6 +1528,19 @@ qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const 
     t_front = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     fprintf(stderr, "[rqb_svd] front end done (waited %.2f ms)\n", t_front - t0);
   }
+  // 3'. optional QR preconditioning (QB_SVD_PRECOND=1, experiment): R^T = Q2 R2, Jacobi on R2^T instead
+  static const int precond = debug_env("QB_SVD_PRECOND");
+  if (precond) {
+    QB_TRY(ensure(ctx, ctx->Jq2, sizeof(double) * (size_t)(ldk * k)));
+    dim3 grid((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
+    transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->R.d(), ldk, k, k, ctx->Jq2.d(), ldk);
+    QB_TRY(check_launch(ctx, "transpose"));  // Jq2 = R^T (column-major)
+    QB_CUDA(cudaMemcpy2DAsync(ctx->Ut.p, ldk * 8, ctx->Jq2.p, ldk * 8, k * 8, k, cudaMemcpyDeviceToDevice, ctx->stream));
+    QB_TRY(orth_blocked(ctx, ctx->Jq2.d(), ldk, k, k));  // Jq2 = Q2
+    // R (column-major) <- R2 = Q2^T R^T
+    QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)k, (int)k, (int)k, ctx->Jq2.d(), ldk, ctx->Ut.d(), ldk, ctx->R.d(),
+                ldk, false, nullptr));
+  }
   // 3. one-sided Jacobi on X = R^T (kp x kp, zero-padded), J = I
   double* X = ctx->Jx.d();
   double* Jm = ctx->Jj.d();
@@ -1667,7 +1683,16 @@ qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const 
   const int64_t kkc = std::max<int64_t>(kk, 1);
   QB_TRY(ensure(ctx, ctx->Usv, sizeof(double) * (size_t)(ldm * kkc)));
   QB_TRY(ensure(ctx, ctx->Vsv, sizeof(double) * (size_t)(ldn * kkc)));
-  if (kk > 0) {
+  if (kk > 0 && precond) {
+    // R^T = Q2 R2 and R2^T J' = Û' D: B̄ = (Q2 J') D (Q_B Û')^T, so U = Q̄ (Q2 J'), V = Q_B Û'
+    QB_TRY(ensure(ctx, ctx->Jm2, sizeof(double) * (size_t)(ldk * k)));
+    QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_ROW, (int)k, (int)k, (int)k, ctx->Jq2.d(), ldk, ctx->Vt.d(), ldk, ctx->Jm2.d(),
+                ldk, false, nullptr));  // row-major Q2 J'
+    QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)kk, (int)k, ctx->Qbar.d(), ctx->ldq, ctx->Jm2.d(), ldk,
+                ctx->Usv.d(), ldm, false, nullptr));
+    QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)n, (int)kk, (int)k, QBm, ldn, ctx->Ut.d(), ldk, ctx->Vsv.d(), ldn,
+                false, nullptr));
+  } else if (kk > 0) {
     QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)kk, (int)k, ctx->Qbar.d(), ctx->ldq, ctx->Ut.d(), ldk,
                 ctx->Usv.d(), ldm, false, nullptr));
     QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)n, (int)kk, (int)k, QBm, ldn, ctx->Vt.d(), ldk, ctx->Vsv.d(), ldn,
@@ -2028,7 +2053,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     const bool overwrite = (flags & QB_OVERWRITE_A) != 0;
     QB_TRY(grow_factors(ctx, m, n, kmax_eff, kmax_eff));
     const int64_t nrec = (kmax_eff + b - 1) / b;
-    QB_TRY(ensure(ctx, ctx->Srec, sizeof(double) * (size_t)(4 * nrec + 8)));
+    QB_TRY(ensure(ctx, ctx->Srec, sizeof(double) * (size_t)(6 * nrec + 8)));
     SmallLoopArgs& a = plan.a;
     a.A = static_cast<const double*>(Ain);
     a.lda = lda;
@@ -2076,7 +2101,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     QB_CUDA(cudaLaunchKernelEx(&lc, small_loop_kernel, a));
     QB_TRY(check_launch(ctx, "small_loop"));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-    std::vector<double> hrec((size_t)(4 * nrec + 8));
+    std::vector<double> hrec((size_t)(6 * nrec + 8));
     QB_CUDA(cudaMemcpyAsync(hrec.data(), ctx->Srec.p, sizeof(double) * hrec.size(), cudaMemcpyDeviceToHost,
                             ctx->stream));
     QB_TRY(stream_wait(ctx));
@@ -2099,10 +2124,11 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     cudaEventElapsedTime(&total, ctx->ev0, ctx->ev1);
     for (int64_t i = 0; i < nblk; ++i) {
       qb_block_stats st{};
-      st.ell = (int64_t)hrec[8 + 4 * i];
-      st.w = (int64_t)hrec[8 + 4 * i + 1];
-      st.r2 = hrec[8 + 4 * i + 2];
-      st.ei = hrec[8 + 4 * i + 3];
+      st.ell = (int64_t)hrec[8 + 6 * i];
+      st.w = (int64_t)hrec[8 + 6 * i + 1];
+      st.r2 = hrec[8 + 6 * i + 2];
+      st.ei = hrec[8 + 6 * i + 3];
+      st.kappa_r = hrec[8 + 6 * i + 5] > 0.0 ? hrec[8 + 6 * i + 4] / hrec[8 + 6 * i + 5] : 0.0;
       st.ms = total / (double)nblk;  // one launch for all blocks: the mean
       st.fallback = i == nblk - 1 ? (int32_t)hrec[3] : 0;
       ctx->stats.push_back(st);
@@ -2431,7 +2457,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     QB_TRY(reduce_to_scal(ctx, na_parts, 0));
     // ||A^(i)||_F^2 (and, on column shards, ||B_i||_F^2) summed over the shards
     QB_TRY(allreduce_sum(ctx, ctx->scal.d(), rowsh ? 1 : 2));
-    QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    QB_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.p, 6 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     QB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     const double th1 = host_timing ? now_ms() : 0.0;
@@ -2471,6 +2497,7 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
     cudaEventElapsedTime(&ms, ctx->evp[4], ctx->evp[5]);
     st.ms_down = ms;
     st.fallback = ctx->block_fallbacks;
+    st.kappa_r = (ctx->h_status[5] && ctx->h_scal[5] > 0.0) ? ctx->h_scal[4] / ctx->h_scal[5] : 0.0;
     {
       double acc[PH_N];
       span_collect(ctx, acc);

@@ -169,6 +169,12 @@ __global__ void __launch_bounds__(256) convert_kernel(const Tin* __restrict__ in
 
 // p[0..n) = 0 (device flag words).  A kernel rather than cudaMemsetAsync: a memset may queue on
 // a copy engine behind qb_factor_host's block copies to the host and stall the next block.
+// status[0..7] = 0 and kappa[0..1] = 0 (the start of a block)
+__global__ void reset_block_kernel(int* __restrict__ status, double* __restrict__ kappa) {
+  if (threadIdx.x < 8) status[threadIdx.x] = 0;
+  if (threadIdx.x < 2) kappa[threadIdx.x] = 0.0;
+}
+
 __global__ void zero_ints_kernel(int* __restrict__ p, int n) {
   if (static_cast<int>(threadIdx.x) < n) p[threadIdx.x] = 0;
 }
@@ -312,7 +318,7 @@ __device__ __forceinline__ void chol_rows_times_bt(const double* A, const double
 __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS)
     chol_cluster_kernel(const double* __restrict__ G, int64_t ldg, int w, int64_t m_rows, double* __restrict__ Tout,
                         int64_t ldt, int* __restrict__ status, double tol, double ns_tol2,
-                        const int* __restrict__ gate) {
+                        const int* __restrict__ gate, double* __restrict__ kappa) {
   if (gate != nullptr && __ldcg(gate) == 0) return;  // same value in every CTA of the cluster
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -497,6 +503,21 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
     if (!failed) break;
   }
   if (cta == 0 && tid == 0) {
+    // kappa-proxy of the block (qb_stats): max / min diagonal of the first factorization's R
+    if (kappa != nullptr && attempt < 2 && atomicCAS(status + 5, 0, 1) == 0) {
+      double dmax = 0.0, dmin = 1e300;
+      for (int q = 0; q < nbk; ++q) {
+        const double* Pq = cluster.map_shared_rank(P, q);
+        const int nbq = min(CHOL_NB, w - q * CHOL_NB);
+        for (int i = 0; i < nbq; ++i) {
+          const double d = Pq[i * PLD + i];
+          dmax = fmax(dmax, d);
+          dmin = fmin(dmin, d);
+        }
+      }
+      kappa[0] = dmax;
+      kappa[1] = dmin;
+    }
     status[0] = attempt;  // 0, 1, or 2 (= failed twice)
     status[2] = 1;
     if (attempt == 1) {
@@ -620,12 +641,14 @@ constexpr int SCQR_SMEM = (2 * SCQR_MAX_ELEMS + 2 * SCQR_MAX_W * SCQR_GLD) * 8;
 // per entry i <= j, fixed-order warp sums.  Ends with __syncthreads.
 __device__ __forceinline__ void scq_gram(const double* P, int ld, int rows, int w, double* G) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  #pragma unroll 1
   for (int e = warp; e < w * w; e += nwarps) {
     const int i = e / w, j = e % w;
     if (i > j) continue;
     const double* xi = P + static_cast<int64_t>(i) * ld;
     const double* xj = P + static_cast<int64_t>(j) * ld;
     double s = 0.0;
+    #pragma unroll 1
     for (int r = lane; r < rows; r += 32) s = fma(xi[r], xj[r], s);
     s = warp_sum(s);
     if (lane == 0) {
@@ -641,12 +664,13 @@ __device__ __forceinline__ void scq_gram(const double* P, int ld, int rows, int 
 // pass flags (factorised, shifted, fallback count); returns true on failure (both attempts broke
 // down).  G is overwritten.  Uniform across the CTA; ends with __syncthreads.
 __device__ bool scq_factor(double* G, double* T, int w, double m_rows, double ns_tol2, double tol, bool& f_fact,
-                           bool& f_shift, int& fallbacks) {
+                           bool& f_shift, int& fallbacks, double* kdiag = nullptr) {
   __shared__ double red[2][32];
   __shared__ double s_e2, s_shift;
   __shared__ int s_bad;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nthr = blockDim.x;
   double e2 = 0.0, tr = 0.0;
+  #pragma unroll 1
   for (int e = t; e < w * w; e += nthr) {
     const int i = e / w, j = e % w;
     const double d = G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0);
@@ -671,6 +695,7 @@ __device__ bool scq_factor(double* G, double* T, int w, double m_rows, double ns
   }
   __syncthreads();
   if (ns_tol2 >= 0.0 && s_e2 <= ns_tol2) {  // Newton-Schulz step towards the polar factor
+    #pragma unroll 1
     for (int e = t; e < w * w; e += nthr) {
       const int i = e / w, j = e % w;
       T[i * SCQR_GLD + j] = (i == j ? 1.0 : 0.0) - 0.5 * (G[i * SCQR_GLD + j] - (i == j ? 1.0 : 0.0));
@@ -680,11 +705,13 @@ __device__ bool scq_factor(double* G, double* T, int w, double m_rows, double ns
   }
   f_fact = true;
   // T keeps the Gram (pivot tolerance reference, and the retry's input)
+  #pragma unroll 1
   for (int e = t; e < w * w; e += nthr) T[(e / w) * SCQR_GLD + e % w] = G[(e / w) * SCQR_GLD + e % w];
   __syncthreads();
   bool failed = false;
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (attempt == 1) {
+      #pragma unroll 1
       for (int e = t; e < w * w; e += nthr) {
         const int i = e / w, j = e % w;
         G[i * SCQR_GLD + j] = T[i * SCQR_GLD + j] + (i == j ? s_shift : 0.0);
@@ -705,6 +732,7 @@ __device__ bool scq_factor(double* G, double* T, int w, double m_rows, double ns
       for (int i = j + 1 + t; i < w; i += nthr) G[i * SCQR_GLD + j] /= ljj;
       __syncthreads();
       const int nt = w - j - 1;
+      #pragma unroll 1
       for (int e = t; e < nt * nt; e += nthr) {
         const int i = j + 1 + e / nt, k = j + 1 + e % nt;
         if (k <= i) G[i * SCQR_GLD + k] = fma(-G[i * SCQR_GLD + j], G[k * SCQR_GLD + j], G[i * SCQR_GLD + k]);
@@ -722,14 +750,25 @@ __device__ bool scq_factor(double* G, double* T, int w, double m_rows, double ns
     }
   }
   if (failed) return true;
+  if (kdiag != nullptr && t == 0) {  // max / min diagonal of R (the kappa-proxy of qb_stats)
+    double dmax = 0.0, dmin = 1e300;
+    for (int j = 0; j < w; ++j) {
+      dmax = fmax(dmax, G[j * SCQR_GLD + j]);
+      dmin = fmin(dmin, G[j * SCQR_GLD + j]);
+    }
+    kdiag[0] = dmax;
+    kdiag[1] = dmin;
+  }
   // T = R^-1 = L^-T: column c of L^-1 by forward substitution (thread c); T[c][i] = L^-1(i, c) = R^-1(c, i)
   for (int c = t; c < w; c += nthr) {
+    #pragma unroll 1
     for (int i = 0; i < w; ++i) {
       if (i < c) {
         T[c * SCQR_GLD + i] = 0.0;
         continue;
       }
       double v = (i == c) ? 1.0 : 0.0;
+      #pragma unroll 1
       for (int k = c; k < i; ++k) v = fma(-G[i * SCQR_GLD + k], T[c * SCQR_GLD + k], v);
       T[c * SCQR_GLD + i] = v / G[i * SCQR_GLD + i];
     }
@@ -741,13 +780,16 @@ __device__ bool scq_factor(double* G, double* T, int w, double m_rows, double ns
 // P <- P T for the column-major rows x w panel P (ld), through the scratch X2 (ld rows).
 __device__ __forceinline__ void scq_apply(double* P, int ld, int rows, int w, const double* T, double* X2) {
   const int t = threadIdx.x, nthr = blockDim.x;
+  #pragma unroll 1
   for (int e = t; e < rows * w; e += nthr) {
     const int j = e / rows, r = e % rows;
     double s = 0.0;
+    #pragma unroll 1
     for (int i = 0; i < w; ++i) s = fma(P[static_cast<int64_t>(i) * ld + r], T[i * SCQR_GLD + j], s);
     X2[e] = s;
   }
   __syncthreads();
+  #pragma unroll 1
   for (int e = t; e < rows * w; e += nthr) P[static_cast<int64_t>(e / rows) * ld + e % rows] = X2[e];
   __syncthreads();
 }
@@ -756,7 +798,8 @@ __global__ void __launch_bounds__(SCQR_THREADS) small_cholqr_kernel(const double
                                                                     double* __restrict__ dst, int64_t ldd, int m,
                                                                     int w, int single, double ns_tol2, double tol,
                                                                     int* __restrict__ status,
-                                                                    float* __restrict__ dst32, int64_t ldd32) {
+                                                                    float* __restrict__ dst32, int64_t ldd32,
+                                                                    double* __restrict__ kappa) {
   extern __shared__ double scq[];
   double* X = scq;                         // [w][m] column-major (ld m)
   double* X2 = X + SCQR_MAX_ELEMS;         // product buffer
@@ -767,9 +810,23 @@ __global__ void __launch_bounds__(SCQR_THREADS) small_cholqr_kernel(const double
   __syncthreads();
   bool f_fact = false, f_shift = false, f_fail = false;
   int fallbacks = 0;
+  __shared__ double kd[2];
+  __shared__ int krec;
+  if (t == 0) krec = (kappa != nullptr && atomicCAS(status + 5, 0, 1) == 0) ? 1 : 0;
+  __syncthreads();
+  bool kdone = krec == 0;
   auto pass = [&]() {
     scq_gram(X, m, m, w, G);
-    f_fail = scq_factor(G, T, w, static_cast<double>(m), ns_tol2, tol, f_fact, f_shift, fallbacks);
+    const bool was_fact = f_fact;
+    f_fail = scq_factor(G, T, w, static_cast<double>(m), ns_tol2, tol, f_fact, f_shift, fallbacks,
+                        kdone ? nullptr : kd);
+    if (!kdone && !was_fact && f_fact && !f_fail) {  // the first factorization of the block
+      kdone = true;
+      if (t == 0) {
+        kappa[0] = kd[0];
+        kappa[1] = kd[1];
+      }
+    }
     if (!f_fail) scq_apply(X, m, m, w, T, X2);
   };
   pass();

@@ -40,7 +40,7 @@ struct SmallLoopArgs {
   int64_t ldq;
   double* Bbar;
   int64_t ldb;
-  double* rec;  // per block: ell (after), w, r2, ei
+  double* rec;  // per block: ell (after), w, r2, ei, max and min R diagonal of the first factorization
   double* out;  // [0] r2_0, [1] final r2, [2] k, [3] fallbacks, [4] 1 = orth breakdown, [5] blocks
   OmegaConsts K;
   int mr, nr;   // rows (of Y, Q) / columns (of A, rows of Ω, Z) per CTA
@@ -58,15 +58,17 @@ __device__ __forceinline__ unsigned long long sl_now() {
 namespace sl {
 namespace cg = cooperative_groups;
 
-// sum_k ptr_k[idx] over the cluster's CTAs in rank order, all remote loads issued first
-__device__ __forceinline__ double rank_sum(cg::cluster_group& cl, const double* ptr, int idx, unsigned ncta) {
-  double v[SL_MAXCL];
-#pragma unroll
-  for (int k = 0; k < SL_MAXCL; ++k) v[k] = (static_cast<unsigned>(k) < ncta) ? cl.map_shared_rank(ptr, k)[idx] : 0.0;
+// sum_k ptr_k[idx] over the cluster's CTAs in rank order, four remote loads in flight at a time
+__device__ __noinline__ double rank_sum(cg::cluster_group& cl, const double* ptr, int idx, unsigned ncta) {
   double s = 0.0;
+  for (unsigned k = 0; k < ncta; k += 4) {
+    double v[4];
 #pragma unroll
-  for (int k = 0; k < SL_MAXCL; ++k)
-    if (static_cast<unsigned>(k) < ncta) s += v[k];
+    for (int u = 0; u < 4; ++u) v[u] = (k + u < ncta) ? cl.map_shared_rank(ptr, k + u)[idx] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (k + u < ncta) s += v[u];
+  }
   return s;
 }
 
@@ -87,7 +89,7 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
 // Two cluster barriers per pass.  Returns true on breakdown (uniform over the cluster).
 __device__ __noinline__ bool dist_orth(cg::cluster_group& cl, double* P, int ld, int rows, double global_rows, int w, bool single,
                           double* Gp, double* G, double* T, double* X2, const SmallLoopArgs& a, int* sf, int* sfl,
-                          int& fallbacks) {
+                          int& fallbacks, double* kap, int* kset) {
   const unsigned c = cl.block_rank(), ncta = cl.num_blocks();
   const int t = threadIdx.x;
   bool f_fact = false, f_shift = false, fail = false;
@@ -99,18 +101,21 @@ __device__ __noinline__ bool dist_orth(cg::cluster_group& cl, double* P, int ld,
     cl.sync();  // every Gram partial is complete
     if (tr && !tr[14]) tr[14] = sl_now();
     if (c == 0) {
+      #pragma unroll 1
       for (int e = t; e < w * w; e += SL_THREADS)
         G[(e / w) * SCQR_GLD + e % w] = rank_sum(cl, Gp, (e / w) * SCQR_GLD + e % w, ncta);
       __syncthreads();
       if (tr && !tr[15]) tr[15] = sl_now();
       bool ff = false, fs = false;
       int fb = 0;
-      const bool fl = scq_factor(G, T, w, global_rows, a.ns_tol2, a.tol, ff, fs, fb);
+      const bool first = *kset == 0;
+      const bool fl = scq_factor(G, T, w, global_rows, a.ns_tol2, a.tol, ff, fs, fb, first ? kap : nullptr);
       if (t == 0) {
         sf[0] = ff;
         sf[1] = fs;
         sf[2] = fl;
         fallbacks += fb;
+        if (first && ff && !fl) *kset = 1;  // kap holds the block's first factorization's R diagonal range
       }
     }
     if (tr && !tr[16]) tr[16] = sl_now();
@@ -124,6 +129,7 @@ __device__ __noinline__ bool dist_orth(cg::cluster_group& cl, double* P, int ld,
     }
     if (c != 0) {
       const double* T0 = cl.map_shared_rank(T, 0);
+      #pragma unroll 1
       for (int e = t; e < w * w; e += SL_THREADS) T[(e / w) * SCQR_GLD + e % w] = T0[(e / w) * SCQR_GLD + e % w];
     }
     __syncthreads();
@@ -146,6 +152,7 @@ __device__ __noinline__ bool dist_orth(cg::cluster_group& cl, double* P, int ld,
 __device__ __forceinline__ void gather_rows(cg::cluster_group& cl, double* Qf, const double* Ys, int m, int mr,
                                             int w) {
   const unsigned ncta = cl.num_blocks();
+  #pragma unroll 1
   for (int e = threadIdx.x; e < m * w; e += SL_THREADS) {
     const int tt = e / m, i = e % m;
     const unsigned r = static_cast<unsigned>(i / mr);
@@ -158,6 +165,7 @@ __device__ __forceinline__ void gather_rows(cg::cluster_group& cl, double* Qf, c
 __device__ __forceinline__ void sum_rows(cg::cluster_group& cl, double* Ys, const double* Yp, int m, int r0, int rr,
                                          int mr, int w) {
   const unsigned ncta = cl.num_blocks();
+  #pragma unroll 1
   for (int e = threadIdx.x; e < rr * w; e += SL_THREADS) {
     const int tt = e / rr, r = e % rr;
     Ys[tt * mr + r] = rank_sum(cl, Yp, tt * m + r0 + r, ncta);
@@ -169,12 +177,15 @@ __device__ __forceinline__ void sum_rows(cg::cluster_group& cl, double* Ys, cons
 // thread per row, SL_CHUNK accumulators in registers, the X entries broadcast.
 __device__ __forceinline__ void rows_times(const double* M, int m, int k, const double* X, int xs, int xt, int w,
                                            double* Out) {
+  #pragma unroll 1
   for (int t0 = 0; t0 < w; t0 += SL_CHUNK) {
     const int tw = min(SL_CHUNK, w - t0);
+    #pragma unroll 1
     for (int i = threadIdx.x; i < m; i += SL_THREADS) {
       double acc[SL_CHUNK];
 #pragma unroll
       for (int u = 0; u < SL_CHUNK; ++u) acc[u] = 0.0;
+      #pragma unroll 1
       for (int j = 0; j < k; ++j) {
         const double v = M[j * m + i];
 #pragma unroll
@@ -195,12 +206,15 @@ __device__ __forceinline__ void rows_times(const double* M, int m, int k, const 
 template <typename F>
 __device__ __forceinline__ void cols_dot(const double* M, int m, int k, const double* P, int w, F&& out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  #pragma unroll 1
   for (int t0 = 0; t0 < w; t0 += SL_CHUNK) {
     const int tw = min(SL_CHUNK, w - t0);
+    #pragma unroll 1
     for (int jj = warp; jj < k; jj += SL_THREADS / 32) {
       double acc[SL_CHUNK];
 #pragma unroll
       for (int u = 0; u < SL_CHUNK; ++u) acc[u] = 0.0;
+      #pragma unroll 1
       for (int i = lane; i < m; i += 32) {
         const double v = M[jj * m + i];
 #pragma unroll
@@ -243,6 +257,8 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
   __shared__ double s_tot[2];
   __shared__ int sf[4];         // CTA 0: pass flags
   __shared__ int sfl[4];        // local copy of CTA 0's flags
+  __shared__ double s_kap[2];   // CTA 0: R diagonal range of the block's first factorization
+  __shared__ int s_kset;
   const unsigned c = cl.block_rank(), ncta = cl.num_blocks();
   const int t = threadIdx.x;
   const int m = a.m, n = a.n, mr = a.mr, nr = a.nr;
@@ -264,6 +280,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
 
   // A_c and r_0^2 = ||A||_F^2 (a0; Algorithm 1 line (2), reading R3)
   double s2 = 0.0;
+  #pragma unroll 1
   for (int e = t; e < m * cc; e += SL_THREADS) {
     const double v = a.A[static_cast<int64_t>(c0 + e / m) * a.lda + e % m];
     Ac[e] = v;
@@ -284,10 +301,16 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
   while (!stop && ell < a.kmax) {
     const int w = min(a.b, a.kmax - ell);
     mark(0);
+    if (t == 0) {
+      s_kset = 0;
+      s_kap[0] = s_kap[1] = 0.0;
+    }
+    __syncthreads();
     const bool reproj_follows = ell > 0 && a.reproj && !a.full_first;
     // line (2): Ω_i rows [c0, c0 + cc) of global columns ell .. ell + w - 1 (row-major, ld w)
     if (cc > 0) {
       const int p0 = c0 >> 1, p1 = (c0 + cc - 1) >> 1;
+      #pragma unroll 1
       for (int e = t; e < (p1 - p0 + 1) * w; e += SL_THREADS) {
         const int p = p0 + e / w, tt = e % w;
         double ev, od;
@@ -305,26 +328,28 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
     sl::sum_rows(cl, Ys, Yp, m, r0, rr, mr, w);
     mark(3);
     fail = sl::dist_orth(cl, Ys, mr, rr, m, w, a.q == 0 ? reproj_follows : false, Gp, G, T, X2, a, sf, sfl,
-                         fallbacks);
+                         fallbacks, s_kap, &s_kset);
     mark(4);
     // lines (4)-(7): power steps on the residual (readings R9, R10)
     for (int j = 0; j < a.q && !fail; ++j) {
       cl.sync();
       sl::gather_rows(cl, Yp, Ys, m, mr, w);  // Q_i in full (ld m)
       sl::cols_dot(Ac, m, cc, Yp, w, [&](int jj, int tt, double v) { Zs[tt * nr + jj] = v; });  // Z_c = A_c^T Q_i
-      fail = sl::dist_orth(cl, Zs, nr, cc, n, w, false, Gp, G, T, X2, a, sf, sfl, fallbacks);
+      fail = sl::dist_orth(cl, Zs, nr, cc, n, w, false, Gp, G, T, X2, a, sf, sfl, fallbacks, s_kap, &s_kset);
       if (fail) break;
       sl::rows_times(Ac, m, cc, Zs, 1, nr, w, Yp);  // Y = A Z (partials); Yp free: every gather done
       cl.sync();
       sl::sum_rows(cl, Ys, Yp, m, r0, rr, mr, w);
       fail = sl::dist_orth(cl, Ys, mr, rr, m, w, j == a.q - 1 ? reproj_follows : false, Gp, G, T, X2, a, sf, sfl,
-                           fallbacks);
+                           fallbacks, s_kap, &s_kset);
     }
     // line (8) / (3'): Q_i = orth(Q_i - Q̄ (Q̄^* Q_i)), on this CTA's rows of Q̄ (kept in Qc)
     if (!fail && ell > 0 && a.reproj) {
+      #pragma unroll 1
       for (int e = t; e < ell * w; e += SL_THREADS) {  // W_c = Q̄(rows_c, :)^T Q_i(rows_c)
         const int tt = e / ell, l = e % ell;
         double s = 0.0;
+        #pragma unroll 1
         for (int r = 0; r < rr; ++r) s = fma(Qc[l * mr + r], Ys[tt * mr + r], s);
         Wp[e] = s;
       }
@@ -332,27 +357,32 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
       cl.sync();
       // reduce-scatter: CTA k sums entries [k S, (k+1) S) over the ranks; then every CTA gathers W
       const int S = (ell * w + static_cast<int>(ncta) - 1) / static_cast<int>(ncta);
+      #pragma unroll 1
       for (int e = t; e < S; e += SL_THREADS) {
         const int g = static_cast<int>(c) * S + e;
         if (g < ell * w) Wr[e] = sl::rank_sum(cl, Wp, g, ncta);
       }
       cl.sync();
       double* Wf = Yp;  // free until the gather below; ell <= m
+      #pragma unroll 1
       for (int e = t; e < ell * w; e += SL_THREADS) Wf[e] = cl.map_shared_rank(Wr, e / S)[e % S];
       __syncthreads();
+      #pragma unroll 1
       for (int e = t; e < rr * w; e += SL_THREADS) {  // Q_i(rows_c) -= Q̄(rows_c, :) W
         const int tt = e / rr, r = e % rr;
         double s = 0.0;
+        #pragma unroll 1
         for (int l = 0; l < ell; ++l) s = fma(Qc[l * mr + r], Wf[tt * ell + l], s);
         Ys[tt * mr + r] -= s;
       }
       __syncthreads();
       mark(6);
-      fail = sl::dist_orth(cl, Ys, mr, rr, m, w, false, Gp, G, T, X2, a, sf, sfl, fallbacks);
+      fail = sl::dist_orth(cl, Ys, mr, rr, m, w, false, Gp, G, T, X2, a, sf, sfl, fallbacks, s_kap, &s_kset);
     }
     mark(7);
     if (fail) break;
     // Q̄ = [Q̄ Q_i]: this CTA's rows (shared and global); Q_i in full for B_i and the downdate
+    #pragma unroll 1
     for (int e = t; e < rr * w; e += SL_THREADS) {
       const int tt = e / rr, r = e % rr;
       const double v = Ys[tt * mr + r];
@@ -372,13 +402,16 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
     mark(9);
     // line (10): A^(i) = A^(i-1) - Q_i B_i, and ||A^(i)||_F^2 (the stop test, reading R1): thread per row
     double as = 0.0;
+    #pragma unroll 1
     for (int i = t; i < m; i += SL_THREADS) {
+      #pragma unroll 1
       for (int t0 = 0; t0 < w; t0 += SL_CHUNK) {
         const int tw = min(SL_CHUNK, w - t0);
         double qrow[SL_CHUNK];
 #pragma unroll
         for (int u = 0; u < SL_CHUNK; ++u) qrow[u] = u < tw ? Yp[(t0 + u) * m + i] : 0.0;
         const bool last = t0 + SL_CHUNK >= w;
+        #pragma unroll 1
         for (int jj = 0; jj < cc; ++jj) {
           double s = 0.0;
 #pragma unroll
@@ -402,10 +435,12 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
     ei -= s_tot[1];
     ell += w;
     if (c == 0 && t == 0) {
-      a.rec[4 * nblk + 0] = ell;
-      a.rec[4 * nblk + 1] = w;
-      a.rec[4 * nblk + 2] = r2;
-      a.rec[4 * nblk + 3] = ei;
+      a.rec[6 * nblk + 0] = ell;
+      a.rec[6 * nblk + 1] = w;
+      a.rec[6 * nblk + 2] = r2;
+      a.rec[6 * nblk + 3] = ei;
+      a.rec[6 * nblk + 4] = s_kset ? s_kap[0] : 0.0;
+      a.rec[6 * nblk + 5] = s_kset ? s_kap[1] : 0.0;
     }
     mark(11);
     ++nblk;
@@ -413,6 +448,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1) small_loop_kernel(const SmallLo
     cl.sync();              // s_part and the gathered panel are reused next block
   }
   if (a.Aout != nullptr)
+    #pragma unroll 1
     for (int e = t; e < m * cc; e += SL_THREADS) a.Aout[static_cast<int64_t>(c0 + e / m) * a.ldo + e % m] = Ac[e];
   if (c == 0 && t == 0) {
     a.out[0] = r2_0;

@@ -498,3 +498,22 @@ def test_small_loop_overwrite_and_host_entry(qbmod, ctx):
                              Bh.ctypes.data, 200, k)
     assert r["k"] == k
     assert np.array_equal(Qh.T, Qg) and np.array_equal(Bh, Bg)
+
+
+@pytest.mark.parametrize("force_general", [False, True])
+def test_kappa_proxy_matches_oracle_sketch(qbmod, ctx, force_general):
+    """qb_stats' kappa-proxy: max R_jj / min R_jj of the block's first CholeskyQR
+    factorization, i.e. of the sketch Y_i = A^(i-1) Omega_i, equals the ratio of |diag R| of the
+    economy QR of the oracle's Y_i (the R of a full-rank QR is unique up to row signs)."""
+    A, _ = make(400, 300, "exp10_20", 1400)
+    eps, b = 1e-6, 10
+    o = oqb.randqb_pb(A, eps, b, 0, seed=1)
+    g = ctx.factor(to_dev(A), eps, b, 0, seed=1, flags=qbmod.QB_FORCE_GENERAL if force_general else 0)
+    assert g["k"] == o.k
+    for i, st in enumerate(g["stats"]):
+        ell = i * b
+        R = A - o.Q[:, :ell] @ o.B[:ell]                      # A^(i-1) from the oracle's factors
+        Y = R @ oqb.omega(1, A.shape[1], ell, b)
+        d = np.abs(np.diag(np.linalg.qr(Y, mode="r")))
+        assert st["kappa_r"] > 1.0
+        assert abs(st["kappa_r"] - d.max() / d.min()) <= 1e-6 * d.max() / d.min(), (i, st["kappa_r"], d.max() / d.min())
