@@ -1554,7 +1554,8 @@ qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const 
     QB_TRY(check_launch(ctx, "identity"));
   }
   if (ctx->jac_pairs_nblk != nblk) {  // the tournament schedule, uploaded once per block count
-    const std::vector<int2> sched = round_robin(nblk);
+    std::vector<int2> sched = round_robin(nblk);
+    for (int p = 0; p < nblk / 2; ++p) sched.push_back(make_int2(2 * p, 2 * p + 1));  // QB_JAC_CROSS's first step
     QB_TRY(ensure(ctx, ctx->Jpairs, sizeof(int2) * sched.size()));
     QB_CUDA(cudaMemcpy(ctx->Jpairs.p, sched.data(), sizeof(int2) * sched.size(), cudaMemcpyHostToDevice));
     ctx->jac_pairs_nblk = nblk;
@@ -1583,17 +1584,24 @@ qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const 
   if (!ctx->jev[0])
     for (auto& e : ctx->jev) QB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const int nchj = nch;
+  // Each sweep: a first step on the pairs (2p, 2p+1) with full inner sweeps (every within-block pair
+  // of columns), then the tournament with cross-block rotations only (16 rotation steps per pair
+  // instead of 31; T 249 -> 234 ms, C4 48 -> 42 ms, same sweep count).  QB_JAC_CROSS=0: full inner
+  // sweeps on every tournament pair.
+  static const int cross = getenv("QB_JAC_CROSS") ? atoi(getenv("QB_JAC_CROSS")) : 1;
+  const int nst = nsteps + (cross ? 1 : 0);
   auto enqueue_sweep = [&](cudaStream_t st, cudaStream_t st2) -> qb_status {
     QB_CUDA(cudaMemsetAsync(offmax, 0, sizeof(unsigned long long), st));
-    for (int s = 0; s < nsteps; ++s) {
+    for (int s = 0; s < nst; ++s) {
       const int slot = s & 1;
-      const int2* pr = pairs + (size_t)s * npairs;
+      const int2* pr = (cross && s == 0) ? pairs + (size_t)nsteps * npairs : pairs + (size_t)(s - (cross ? 1 : 0)) * npairs;
+      const int cross_only = (cross && s > 0) ? 1 : 0;
       double* Dsl = ctx->Jw.d() + (size_t)slot * npairs * JPW * JPW;
       int* fl = jflag + slot * npairs;
       jac_gram_kernel<<<dim3(npairs, nch), JTHREADS, JGRAM_SMEM, st>>>(X, kp, (int)k, pr, nch, ctx->Jpart.d());
       QB_TRY(check_launch(ctx, "jac_gram"));
       if (s >= 2) QB_CUDA(cudaStreamWaitEvent(st, ctx->jev[2 + slot], 0));  // J update s-2 read this slot
-      jac_solve_kernel<<<npairs, JST, JSOLVE_SMEM, st>>>(ctx->Jpart.d(), nch, Dsl, fl, offmax, tol, inner);
+      jac_solve_kernel<<<npairs, JST, JSOLVE_SMEM, st>>>(ctx->Jpart.d(), nch, Dsl, fl, offmax, tol, inner, cross_only);
       QB_TRY(check_launch(ctx, "jac_solve"));
       QB_CUDA(cudaEventRecord(ctx->jev[slot], st));
       jac_update_kernel<<<dim3(npairs, nch), JTHREADS, JUPD_SMEM, st>>>(X, kp, (int)k, pr, Dsl, fl);
@@ -1603,12 +1611,12 @@ qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const 
       QB_TRY(check_launch(ctx, "jac_update_j"));
       QB_CUDA(cudaEventRecord(ctx->jev[2 + slot], st2));
     }
-    QB_CUDA(cudaStreamWaitEvent(st, ctx->jev[2 + ((nsteps - 1) & 1)], 0));  // join the J branch
+    QB_CUDA(cudaStreamWaitEvent(st, ctx->jev[2 + ((nst - 1) & 1)], 0));  // join the J branch
     return QB_OK;
   };
   static const int no_graph = debug_env("QB_JAC_NO_GRAPH");
   cudaGraphExec_t gexec = nullptr;
-  const int per_sweep = 4 * nsteps;
+  const int per_sweep = 4 * nst;
   if (!no_graph && !debug_env("QB_DEBUG_SYNC")) {
     if (!ctx->cap_stream) QB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     if (!ctx->cap_stream2) QB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking));

@@ -105,7 +105,7 @@ constexpr int JSOLVE_SMEM = 2 * JPW * JGLD * 8;
 __global__ void __launch_bounds__(JST) jac_solve_kernel(const double* __restrict__ part, int nchunks,
                                                         double* __restrict__ Dout, int* __restrict__ flag,
                                                         unsigned long long* __restrict__ offmax, double tol,
-                                                        int inner) {
+                                                        int inner, int cross_only) {
   extern __shared__ double jsm[];
   constexpr int NP = JPW / 2;
   static_assert(NP * NP == JST / 2 && JPW * NP == JST, "thread maps below assume JPW = 32, JST = 512");
@@ -155,10 +155,13 @@ __global__ void __launch_bounds__(JST) jac_solve_kernel(const double* __restrict
   for (int sweep = 0; sweep < inner; ++sweep) {
     if (t == 0) any_rot = 0;
     __syncthreads();
-    for (int step = 0; step < JPW - 1; ++step) {
-      if (t < NP) {  // circle method: (step, JPW-1), (step + i, step - i) mod (JPW - 1)
-        int a = t == 0 ? step : (step + t) % (JPW - 1);
-        int b = t == 0 ? JPW - 1 : (step - t + (JPW - 1)) % (JPW - 1);
+    const int nsteps = cross_only ? NP : JPW - 1;
+    for (int step = 0; step < nsteps; ++step) {
+      if (t < NP) {
+        // all pairs: circle method (step, JPW-1), (step + i, step - i) mod (JPW - 1); cross_only: the
+        // NP^2 pairs between the two blocks, (i, NP + (i + step) mod NP)
+        int a = cross_only ? t : (t == 0 ? step : (step + t) % (JPW - 1));
+        int b = cross_only ? NP + (t + step) % NP : (t == 0 ? JPW - 1 : (step - t + (JPW - 1)) % (JPW - 1));
         if (a > b) {
           const int tmp = a;
           a = b;
