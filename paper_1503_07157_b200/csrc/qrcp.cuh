@@ -352,30 +352,51 @@ __global__ void __launch_bounds__(1024) qrcp_la_pivot_kernel(double* __restrict_
   }
   __syncthreads();
   const int p = s_p;
-  // the deferred update of step i-1 on the two columns that move (rows >= i)
-  if (i > 0) {
-    const double tp = tau[i - 1];
-    const double wi = wprev[i], wp = wprev[p];
-    for (int r = i + tid; r < l; r += blockDim.x) {
-      double* a = B + static_cast<int64_t>(r) * ldb;
+  // One pass over the two columns that move (rows >= i; each element is a separate DRAM row, so the
+  // phases are latency-bound): the deferred update of step i-1, the swap, and the sum of squares of
+  // the new column i below the diagonal; the first PIV_REG rows per thread stay in registers for
+  // the scaling pass.  Rows < i of the swapped columns are swapped as they are (no pending update).
+  constexpr int PIV_REG = 4;
+  const double tp = i > 0 ? tau[i - 1] : 0.0;
+  const double wi = i > 0 ? wprev[i] : 0.0, wp = i > 0 ? wprev[p] : 0.0;
+  double keep[PIV_REG];
+  double ss = 0.0;
+  auto move = [&](int r) -> double {
+    double* a = B + static_cast<int64_t>(r) * ldb;
+    double xi = a[i], xp = a[p];
+    if (i > 0) {
       const double tv = tp * vprev[r - (i - 1)];
-      a[i] = fma(-tv, wi, a[i]);
-      if (p != i) a[p] = fma(-tv, wp, a[p]);
+      xi = fma(-tv, wi, xi);
+      xp = fma(-tv, wp, xp);
     }
-    __syncthreads();
-    if (tid == 0) {
-      wprev[i] = 0.0;
-      wprev[p] = 0.0;
-    }
+    if (p != i) a[p] = xi;
+    const double x = p != i ? xp : xi;  // the new column i
+    if (r > i) ss = fma(x, x, ss);
+    return x;
+  };
+#pragma unroll
+  for (int u = 0; u < PIV_REG; ++u) {
+    const int r = i + tid + u * static_cast<int>(blockDim.x);
+    keep[u] = r < l ? move(r) : 0.0;
   }
-  if (p != i) {
-    for (int r = tid; r < l; r += blockDim.x) {
+  for (int r = i + tid + PIV_REG * static_cast<int>(blockDim.x); r < l; r += blockDim.x)
+    B[static_cast<int64_t>(r) * ldb + i] = move(r);  // re-read by the scaling pass
+  if (p != i)
+    for (int r = tid; r < i; r += blockDim.x) {
       double* a = B + static_cast<int64_t>(r) * ldb;
       const double t = a[i];
       a[i] = a[p];
       a[p] = t;
     }
-    if (tid == 0) {
+  ss = warp_sum(ss);
+  if (lane == 0) s_red[warp] = ss;
+  __syncthreads();
+  if (tid == 0) {
+    if (i > 0) {
+      wprev[i] = 0.0;
+      wprev[p] = 0.0;
+    }
+    if (p != i) {
       double t = vn1[i];
       vn1[i] = vn1[p];
       vn1[p] = t;
@@ -386,20 +407,10 @@ __global__ void __launch_bounds__(1024) qrcp_la_pivot_kernel(double* __restrict_
       perm[i] = perm[p];
       perm[p] = q;
     }
-  }
-  __syncthreads();
-  double ss = 0.0;
-  for (int r = i + 1 + tid; r < l; r += blockDim.x) {
-    const double x = B[static_cast<int64_t>(r) * ldb + i];
-    ss = fma(x, x, ss);
-  }
-  ss = warp_sum(ss);
-  if (lane == 0) s_red[warp] = ss;
-  __syncthreads();
-  if (tid == 0) {
     double t = 0.0;
     for (int w = 0; w < static_cast<int>(blockDim.x) / 32; ++w) t += s_red[w];
-    const double alpha = B[static_cast<int64_t>(i) * ldb + i];
+    // alpha: the new B(i, i) — thread 0 holds it in keep[0] (row i is its first row)
+    const double alpha = keep[0];
     if (t == 0.0) {
       tau[i] = 0.0;
       s_beta = alpha;
@@ -414,17 +425,24 @@ __global__ void __launch_bounds__(1024) qrcp_la_pivot_kernel(double* __restrict_
   }
   __syncthreads();
   const double scale = s_scale;
-  for (int r = i + tid; r < l; r += blockDim.x) {
+  auto put = [&](int r, double x) {
     double* a = B + static_cast<int64_t>(r) * ldb + i;
     if (r == i) {
       *a = s_beta;
       vbuf[0] = 1.0;
     } else {
-      const double v = *a * scale;
+      const double v = x * scale;
       *a = v;
       vbuf[r - i] = v;
     }
+  };
+#pragma unroll
+  for (int u = 0; u < PIV_REG; ++u) {
+    const int r = i + tid + u * static_cast<int>(blockDim.x);
+    if (r < l) put(r, keep[u]);
   }
+  for (int r = i + tid + PIV_REG * static_cast<int>(blockDim.x); r < l; r += blockDim.x)
+    put(r, B[static_cast<int64_t>(r) * ldb + i]);
 }
 
 // rows [r0, r1) of the trailing block (r >= i, columns j > i): B -= tau_{i-1} v_{i-1} w_{i-1}^T, then
