@@ -1778,7 +1778,64 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
                                                                                                  (int)n, vn1, vn2, perm);
   QB_TRY(check_launch(ctx, "qrcp_init"));
   static const int unfused = debug_env("QB_QRCP_UNFUSED");
-  if (unfused) {  // reference schedule: reflector, w, rank-1 update, renorm per step
+  static const int lookahead = debug_env("QB_QRCP_LOOKAHEAD");
+  if (!unfused && !lookahead) {  // blocked (dlaqps): panels of QRCP_NB pivots, trailing GEMM per panel
+    const int64_t nblk = (n + QRCP_THREADS - 1) / QRCP_THREADS + 8;
+    const int64_t ldf = ldp, ldv = ldqt;
+    QB_TRY(ensure(ctx, ctx->qw, sizeof(double) * (size_t)(QRCP_NB * ldf + QRCP_NB * ldv + 2 * nblk + 8)));
+    double* F = ctx->qw.d();
+    double* Vt = F + QRCP_NB * ldf;
+    double* pmax = Vt + QRCP_NB * ldv;
+    int* pidx = reinterpret_cast<int*>(pmax + nblk);
+    int* piv = pidx + 2 * nblk;  // step i's pivot column
+    const int kmin = (int)std::min<int64_t>(l, n);
+    static const int ptrace = debug_env("QB_QRCP_TRACE");  // diagnostics: per-panel device time
+    cudaEvent_t pev[2] = {nullptr, nullptr};
+    if (ptrace) {
+      cudaEventCreate(&pev[0]);
+      cudaEventCreate(&pev[1]);
+    }
+    for (int i0 = 0; i0 < kmin; i0 += QRCP_NB) {
+      const int nb = std::min(QRCP_NB, kmin - i0);
+      if (ptrace) cudaEventRecord(pev[0], ctx->stream);
+      for (int i = i0; i < i0 + nb; ++i) {
+        const int npart = i > 0 ? (int)((n - i + QRCP_THREADS - 1) / QRCP_THREADS) : 0;
+        qrcp_bk_pivot_kernel<<<1, BKP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, i0, vn1, tau, F, ldf, vb,
+                                                                 piv, pmax, pidx, npart);
+        QB_TRY(check_launch(ctx, "qrcp_bk_pivot"));
+        if (i + 1 >= n) continue;  // then p = i: no swap is pending
+        const int rch = (int)((l - i + QRCP_WROWS - 1) / QRCP_WROWS);
+        dim3 wgrid((unsigned)((n - i0 + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
+        qrcp_bk_w_kernel<<<wgrid, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, i0, vb, parts, ldp);
+        QB_TRY(check_launch(ctx, "qrcp_bk_w"));
+        const int rblocks = (int)((n - i - 1 + QRCP_THREADS - 1) / QRCP_THREADS);
+        qrcp_bk_row_kernel<<<rblocks, QRCP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, i0, tau, parts, ldp,
+                                                                      rch, F, ldf, vn1, vn2, perm, piv, tol3z, pmax, pidx);
+        QB_TRY(check_launch(ctx, "qrcp_bk_row"));
+      }
+      // trailing block below and right of the panel: A -= V F^T (one GEMM; K = nb)
+      const int r0 = i0 + nb;
+      if (r0 < l && r0 < n) {
+        const int rows = (int)(l - r0);
+        qrcp_bk_vt_kernel<<<(int)std::min<int64_t>(((int64_t)rows * nb + 255) / 256, 4 * ctx->num_sms), 256, 0,
+                            ctx->stream>>>(R, ldr, r0, rows, i0, nb, Vt, ldv);
+        QB_TRY(check_launch(ctx, "qrcp_bk_vt"));
+        QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)(n - r0), rows, nb, F + r0, ldf, Vt, ldv,
+                    R + (int64_t)r0 * ldr + r0, ldr, false, nullptr));
+      }
+      if (ptrace) {
+        float ms = 0.f;
+        cudaEventRecord(pev[1], ctx->stream);
+        cudaEventSynchronize(pev[1]);
+        cudaEventElapsedTime(&ms, pev[0], pev[1]);
+        std::fprintf(stderr, "qrcp panel %d: %.3f ms\n", i0, ms);
+      }
+    }
+    if (ptrace) {
+      cudaEventDestroy(pev[0]);
+      cudaEventDestroy(pev[1]);
+    }
+  } else if (unfused) {  // reference schedule: reflector, w, rank-1 update, renorm per step
     for (int i = 0; i < (int)l; ++i) {
       qrcp_pivot_kernel<<<1, 1024, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, vn1, vn2, perm, tau, vb);
       QB_TRY(check_launch(ctx, "qrcp_pivot"));

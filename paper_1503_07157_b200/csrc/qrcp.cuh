@@ -559,3 +559,400 @@ __global__ void __launch_bounds__(QRCP_THREADS) qrcp_la_row_kernel(double* __res
 }
 
 }  // namespace qbk
+
+namespace qbk {
+
+// ---------------------------------------------------------------- blocked (dlaqps-style) schedule
+// Panels of QRCP_NB pivots; inside a panel the trailing block is NOT updated.  The pending update of
+// the panel's reflectors is carried by F (n x nb, F[kk * ldf + j] = F(j, kk)) as in LAPACK's
+// dlaqps: the trailing block after kk reflectors is A - V F^T, with V the panel's Householder
+// vectors.  Per step i = i0 + kk:
+//   pivot: first column of largest partial norm; swap columns (and F rows); the pivot column gets
+//          its pending update A(i:, i) -= A(i:, i0:i) F(i, 0:kk)^T; reflector (dlarfg);
+//   w:     partials of A(i:, j)^T v over the (stale) trailing block — a read-only pass — and over
+//          the panel's own columns (V(i:, q)^T v, for the incremental F update);
+//   row:   aux(q) = -tau V(i:, q)^T v; F(j, kk) = tau w_j + F(j, 0:kk) aux; row i of the trailing block
+//          A(i, j) -= A(i, i0:i) F(j, 0:kk)^T - F(j, kk); the dlaqp2 norm downdate (an exact norm
+//          with the pending update applied on cancellation), and the next step's pivot partials.
+// At the end of a panel the trailing block gets A -= V F^T as one GEMM.  Same pivots and R as the
+// unblocked order in exact arithmetic; the trailing block is read once per step instead of read
+// and written.
+constexpr int QRCP_NB = 32;
+
+constexpr int QRCP_WROWS = 64;   // rows per CTA of the blocked w pass (partials per column: (l - i) / 64)
+constexpr int BKP_THREADS = 512;  // pivot kernel
+constexpr int BKP_REG = 6;        // rows per pivot thread kept in registers (l - i <= 3072 fully)
+
+// Step i's pivot (one CTA): the first column of largest partial norm p (from the previous row
+// kernel's per-block maxima), published in piv[0]; columns i and p swapped in rows >= i only —
+// rows < i (finished rows of R) are swapped by the row kernel, F's rows and the norms are read
+// through the swap there too; the pivot column's pending update
+// A(i:, i) = A(i:, p) - A(i:, i0:i) F(p, 0:kk)^T; the reflector (dlarfg): beta on the diagonal,
+// v below it and in vbuf, tau[i].
+__global__ void __launch_bounds__(BKP_THREADS) qrcp_bk_pivot_kernel(double* __restrict__ B, int64_t ldb, int l, int n,
+                                                                    int i, int i0, const double* __restrict__ vn1,
+                                                                    double* __restrict__ tau,
+                                                                    const double* __restrict__ F, int64_t ldf,
+                                                                    double* __restrict__ vbuf, int* __restrict__ piv,
+                                                                    const double* __restrict__ pmax,
+                                                                    const int* __restrict__ pidx, int npart) {
+  __shared__ double s_val[BKP_THREADS / 32];
+  __shared__ int s_idx[BKP_THREADS / 32];
+  __shared__ int s_p;
+  __shared__ double s_red[BKP_THREADS / 32];
+  __shared__ double s_fi[QRCP_NB];
+  __shared__ double s_alpha, s_beta, s_scale;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kk = i - i0;
+  double best = -1.0;
+  int bi = n;
+  if (npart > 0) {
+    for (int c = tid; c < npart; c += BKP_THREADS) {
+      const double v = pmax[c];
+      if (v > best || (v == best && pidx[c] < bi)) {
+        best = v;
+        bi = pidx[c];
+      }
+    }
+  } else {
+    for (int j = i + tid; j < n; j += BKP_THREADS) {
+      const double v = vn1[j];
+      if (v > best) {
+        best = v;
+        bi = j;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_val[warp] = best;
+    s_idx[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double b = s_val[0];
+    int x = s_idx[0];
+    for (int w = 1; w < BKP_THREADS / 32; ++w)
+      if (s_val[w] > b || (s_val[w] == b && s_idx[w] < x)) {
+        b = s_val[w];
+        x = s_idx[w];
+      }
+    s_p = x;
+    piv[0] = x;
+  }
+  __syncthreads();
+  const int p = s_p;
+  if (tid < kk) s_fi[tid] = F[tid * ldf + p];  // F(i, :) after the swap = F(p, :) before it
+  __syncthreads();
+  // rows >= i: swap, the pending update of the new column i, the sum of squares below the diagonal
+  double keep[BKP_REG], old[BKP_REG];
+  double ss = 0.0;
+#pragma unroll
+  for (int u = 0; u < BKP_REG; ++u) {  // loads only (the swap's stores follow), so rows overlap
+    const int r = i + tid + u * BKP_THREADS;
+    keep[u] = 0.0;
+    old[u] = 0.0;
+    if (r < l) {
+      const double* a = B + static_cast<int64_t>(r) * ldb;
+      double x = a[p], y = 0.0;
+      old[u] = a[i];
+#pragma unroll
+      for (int q = 0; q < QRCP_NB; q += 2)
+        if (q < kk) {
+          x = fma(-a[i0 + q], s_fi[q], x);
+          if (q + 1 < kk) y = fma(-a[i0 + q + 1], s_fi[q + 1], y);
+        }
+      x += y;
+      keep[u] = x;
+      if (r == i) s_alpha = x;
+      else ss = fma(x, x, ss);
+    }
+  }
+  if (p != i)
+#pragma unroll
+    for (int u = 0; u < BKP_REG; ++u) {
+      const int r = i + tid + u * BKP_THREADS;
+      if (r < l) B[static_cast<int64_t>(r) * ldb + p] = old[u];
+    }
+  for (int r = i + tid + BKP_REG * BKP_THREADS; r < l; r += BKP_THREADS) {  // beyond the register rows
+    double* a = B + static_cast<int64_t>(r) * ldb;
+    double x = a[p];
+    if (p != i) a[p] = a[i];
+    for (int q = 0; q < kk; ++q) x = fma(-a[i0 + q], s_fi[q], x);
+    a[i] = x;
+    ss = fma(x, x, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) s_red[warp] = ss;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < BKP_THREADS / 32; ++w) t += s_red[w];
+    const double alpha = s_alpha;
+    double tv;
+    if (t == 0.0) {
+      tv = 0.0;
+      s_beta = alpha;
+      s_scale = 0.0;
+    } else {
+      const double nrm = sqrt(fma(alpha, alpha, t));
+      const double beta = alpha >= 0.0 ? -nrm : nrm;
+      tv = (beta - alpha) / beta;
+      s_beta = beta;
+      s_scale = 1.0 / (alpha - beta);
+    }
+    tau[i] = tv;
+  }
+  __syncthreads();
+  const double scale = s_scale;
+#pragma unroll
+  for (int u = 0; u < BKP_REG; ++u) {
+    const int r = i + tid + u * BKP_THREADS;
+    if (r < l) {
+      const double v = r == i ? 1.0 : keep[u] * scale;
+      B[static_cast<int64_t>(r) * ldb + i] = r == i ? s_beta : v;
+      vbuf[r - i] = v;
+    }
+  }
+  for (int r = i + tid + BKP_REG * BKP_THREADS; r < l; r += BKP_THREADS) {
+    double* a = B + static_cast<int64_t>(r) * ldb;
+    const double v = a[i] * scale;
+    a[i] = v;
+    vbuf[r - i] = v;
+  }
+}
+
+// partials[c][j] = sum over chunk c (QRCP_WROWS rows from row i) of A(r, j) v_{r-i}, columns
+// j >= j0 (j0 = the panel's first column: the panel's own columns give V(i:, q)^T v for F's
+// incremental update).  Four rows in flight per thread.
+__global__ void __launch_bounds__(QRCP_THREADS) qrcp_bk_w_kernel(const double* __restrict__ B, int64_t ldb, int l,
+                                                               int n, int i, int j0, const double* __restrict__ vbuf,
+                                                               double* __restrict__ partials, int64_t ldp) {
+  const int j = j0 + blockIdx.x * QRCP_THREADS + threadIdx.x;
+  const int r0 = i + blockIdx.y * QRCP_WROWS, r1 = min(l, r0 + QRCP_WROWS);
+  if (j >= n) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int r = r0;
+  for (; r + 3 < r1; r += 4) {
+    const double* a = B + static_cast<int64_t>(r) * ldb + j;
+    const double a0 = a[0], a1 = a[ldb], a2 = a[2 * ldb], a3 = a[3 * ldb];
+    s0 = fma(vbuf[r - i], a0, s0);
+    s1 = fma(vbuf[r + 1 - i], a1, s1);
+    s2 = fma(vbuf[r + 2 - i], a2, s2);
+    s3 = fma(vbuf[r + 3 - i], a3, s3);
+  }
+  for (; r < r1; ++r) s0 = fma(vbuf[r - i], B[static_cast<int64_t>(r) * ldb + j], s0);
+  partials[blockIdx.y * ldp + j] = (s0 + s1) + (s2 + s3);
+}
+
+// Step i after the w pass, columns j > i (thread j reads F's row and the norms of column j
+// through the pivot swap: from index i when j = p):
+//   aux(q) = -tau_i V(i:, q)^T v (the panel columns' partials, fixed order);
+//   F(j, kk) = tau_i w_j + F(j, 0:kk) aux;
+//   row i: A(i, j) -= A(i, i0:i) F(j, 0:kk)^T + F(j, kk);
+//   the dlaqp2 partial-norm downdate; where it lost accuracy, the exact norm of the updated column
+//   ||A(i+1:, j) - V(i+1:, 0:kk+1) F(j, 0:kk+1)^T|| (the CTA's flagged columns packed into groups
+//   of 32, all warps over slices of the rows: the trailing norms decay together, so over a stretch
+//   of steps nearly every column needs this once);
+//   per-block (max, first index) of the norms for the next pivot.
+// Also the deferred swap of columns i and p in rows < i, and perm.
+__global__ void __launch_bounds__(QRCP_THREADS) qrcp_bk_row_kernel(double* __restrict__ B, int64_t ldb, int l, int n,
+                                                                 int i, int i0, const double* __restrict__ tau,
+                                                                 const double* __restrict__ partials, int64_t ldp,
+                                                                 int nchunks, double* __restrict__ F, int64_t ldf,
+                                                                 double* __restrict__ vn1, double* __restrict__ vn2,
+                                                                 int* __restrict__ perm, const int* __restrict__ piv,
+                                                                 double tol3z, double* __restrict__ pmax,
+                                                                 int* __restrict__ pidx) {
+  __shared__ double s_val[QRCP_THREADS / 32];
+  __shared__ int s_idx[QRCP_THREADS / 32];
+  __shared__ double s_aux[QRCP_NB], s_ai[QRCP_NB];
+  __shared__ double s_grp[QRCP_THREADS / 32][QRCP_NB];
+  __shared__ int s_cnt[QRCP_THREADS / 32], s_list[QRCP_THREADS];
+  __shared__ double s_part[QRCP_THREADS / 32][32], s_res[QRCP_THREADS];
+  const int kk = i - i0;
+  const int p = piv[0];
+  const double t = tau[i];
+  {
+    const int q = threadIdx.x & 31, g = threadIdx.x >> 5;
+    double a = 0.0;
+    if (q < kk)
+      for (int c = g; c < nchunks; c += QRCP_THREADS / 32) a += partials[c * ldp + i0 + q];
+    s_grp[g][q] = a;
+  }
+  if (static_cast<int>(threadIdx.x) < kk)
+    s_ai[threadIdx.x] = B[static_cast<int64_t>(i) * ldb + i0 + threadIdx.x];  // A(i, i0 + q): v entries
+  if (p != i) {  // rows < i of columns i and p (finished rows of R)
+    for (int r = blockIdx.x * QRCP_THREADS + threadIdx.x; r < i; r += gridDim.x * QRCP_THREADS) {
+      double* a = B + static_cast<int64_t>(r) * ldb;
+      const double x = a[i];
+      a[i] = a[p];
+      a[p] = x;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const int x = perm[i];
+      perm[i] = perm[p];
+      perm[p] = x;
+    }
+  }
+  __syncthreads();
+  if (static_cast<int>(threadIdx.x) < kk) {
+    double a = 0.0;
+    for (int g = 0; g < QRCP_THREADS / 32; ++g) a += s_grp[g][threadIdx.x];
+    s_aux[threadIdx.x] = -t * a;
+  }
+  __syncthreads();
+  const int j = i + 1 + blockIdx.x * QRCP_THREADS + threadIdx.x;
+  const int js = j == p ? i : j;  // where column j's F row and norms were before the swap
+  double best = -1.0, n1 = 0.0, n2 = 0.0;
+  int bi = n;
+  bool recompute = false;
+  if (j < n) {
+    double w = 0.0;
+#pragma unroll 16
+    for (int c = 0; c < nchunks; ++c) w += partials[c * ldp + j];
+    double f = t * w, rowsum = 0.0;
+#pragma unroll
+    for (int q = 0; q < QRCP_NB; ++q)
+      if (q < kk) {
+        const double fq = F[q * ldf + js];
+        if (js != j) F[q * ldf + j] = fq;  // F's row follows the swap
+        f = fma(fq, s_aux[q], f);
+        rowsum = fma(s_ai[q], fq, rowsum);
+      }
+    F[kk * ldf + j] = f;
+    double* bij = B + static_cast<int64_t>(i) * ldb + j;
+    const double rij = *bij - rowsum - f;
+    *bij = rij;
+    n1 = vn1[js];
+    n2 = vn2[js];
+    if (n1 != 0.0) {
+      double temp = fabs(rij) / n1;
+      temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+      const double ratio = n1 / n2;
+      if (temp * ratio * ratio <= tol3z) recompute = true;
+      else n1 = n1 * sqrt(temp);
+    }
+  }
+  // Exact norms for the flagged columns, packed 32 to a group (lanes over columns, the 8 warps over
+  // slices of the rows), partial sums combined in warp order.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    const unsigned ballot = __ballot_sync(0xffffffffu, recompute);
+    if (lane == 0) s_cnt[warp] = __popc(ballot);
+    __syncthreads();
+    int base = 0, total = 0;
+    for (int w = 0; w < QRCP_THREADS / 32; ++w) {
+      if (w < warp) base += s_cnt[w];
+      total += s_cnt[w];
+    }
+    if (recompute) s_list[base + __popc(ballot & ((1u << lane) - 1u))] = threadIdx.x;
+    __syncthreads();
+    const int rows = l - i - 1, slice = (rows + QRCP_THREADS / 32 - 1) / (QRCP_THREADS / 32);
+    const int ra = i + 1 + warp * slice, rz = min(l, ra + slice);
+    for (int g = 0; g < total; g += 32) {
+      const bool act = g + lane < total;
+      const int tl = act ? s_list[g + lane] : 0;
+      const int col = act ? i + 1 + blockIdx.x * QRCP_THREADS + tl : i;
+      double f2[QRCP_NB];
+#pragma unroll
+      for (int q = 0; q < QRCP_NB; ++q) f2[q] = act && q <= kk ? F[q * ldf + col] : 0.0;
+      double sa = 0.0, sb = 0.0;
+      int r = ra;
+      for (; r + 1 < rz; r += 2) {
+        const double* a0 = B + static_cast<int64_t>(r) * ldb;
+        const double* a1 = a0 + ldb;
+        double x0 = a0[col], x1 = a1[col];
+        const double2* v0 = reinterpret_cast<const double2*>(a0 + i0);
+        const double2* v1 = reinterpret_cast<const double2*>(a1 + i0);
+#pragma unroll
+        for (int q = 0; q < QRCP_NB; q += 2)
+          if (q <= kk) {
+            const double2 u0 = v0[q / 2], u1 = v1[q / 2];
+            x0 = fma(-u0.x, f2[q], x0);
+            x1 = fma(-u1.x, f2[q], x1);
+            x0 = fma(-u0.y, f2[q + 1], x0);
+            x1 = fma(-u1.y, f2[q + 1], x1);
+          }
+        sa = fma(x0, x0, sa);
+        sb = fma(x1, x1, sb);
+      }
+      if (r < rz) {
+        const double* a0 = B + static_cast<int64_t>(r) * ldb;
+        double x0 = a0[col];
+        const double2* v0 = reinterpret_cast<const double2*>(a0 + i0);
+#pragma unroll
+        for (int q = 0; q < QRCP_NB; q += 2)
+          if (q <= kk) {
+            const double2 u0 = v0[q / 2];
+            x0 = fma(-u0.x, f2[q], x0);
+            x0 = fma(-u0.y, f2[q + 1], x0);
+          }
+        sa = fma(x0, x0, sa);
+      }
+      s_part[warp][lane] = sa + sb;
+      __syncthreads();
+      if (warp == 0 && act) {
+        double t2 = 0.0;
+        for (int w = 0; w < QRCP_THREADS / 32; ++w) t2 += s_part[w][lane];
+        s_res[tl] = sqrt(t2);
+      }
+      __syncthreads();
+    }
+    if (recompute) {
+      n1 = s_res[threadIdx.x];
+      n2 = n1;
+    }
+  }
+  if (j < n) {
+    vn1[j] = n1;
+    vn2[j] = n2;
+    best = n1;
+    bi = j;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    s_val[warp] = best;
+    s_idx[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < QRCP_THREADS / 32; ++w2)
+      if (s_val[w2] > best || (s_val[w2] == best && s_idx[w2] < bi)) {
+        best = s_val[w2];
+        bi = s_idx[w2];
+      }
+    pmax[blockIdx.x] = best;
+    pidx[blockIdx.x] = bi;
+  }
+}
+
+// Vt[q][r'] = A(r0 + r', i0 + q), r' < rows, q < nb: the panel's Householder vectors below row r0,
+// as the N-contiguous operand of the trailing GEMM.
+__global__ void qrcp_bk_vt_kernel(const double* __restrict__ B, int64_t ldb, int r0, int rows, int i0, int nb,
+                                  double* __restrict__ Vt, int64_t ldv) {
+  const int64_t total = static_cast<int64_t>(rows) * nb;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / nb), q = static_cast<int>(idx % nb);
+    Vt[q * ldv + r] = B[static_cast<int64_t>(r0 + r) * ldb + i0 + q];
+  }
+}
+
+}  // namespace qbk

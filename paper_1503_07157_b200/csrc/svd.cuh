@@ -22,7 +22,10 @@
 
 namespace qbk {
 
-constexpr int JNB = 16;           // block width
+#ifndef QB_JAC_NB
+#define QB_JAC_NB 16
+#endif
+constexpr int JNB = QB_JAC_NB;    // block width (16 or 32)
 constexpr int JPW = 2 * JNB;      // pair width
 constexpr int JRC = 128;          // rows per chunk (Gram partials, panel updates)
 constexpr int JLDR = JRC + 4;     // row stride of a transposed chunk T[col][row] (= 4 mod 16 words:
@@ -33,7 +36,9 @@ constexpr int JTHREADS = 256;
 constexpr int JLOADS = JRC * JPW / JTHREADS;  // panel elements loaded per thread
 constexpr int JGRAM_SMEM = JPW * JLDR * 8;
 constexpr int JUPD_SMEM = (JPW * JLDR + JPW * JLDD) * 8;
-static_assert(JPW == 32 && JTHREADS == 256 && JRC == 128, "fragment maps below assume these");
+constexpr int JTN = JPW / 8;                  // 8 x 8 DMMA tiles per dimension of a pair
+constexpr int JTPW = JTN * JTN / (JTHREADS / 32);  // Gram tiles per warp (same row tile)
+static_assert((JPW == 32 || JPW == 64) && JTHREADS == 256 && JRC == 128, "fragment maps below assume these");
 
 // Column j (0..JPW-1) of pair p's panel: block I or J of the pair, as a global column index.
 __device__ __forceinline__ int jac_col(const int2 pr, int j) {
@@ -72,24 +77,27 @@ __global__ void __launch_bounds__(JTHREADS) jac_gram_kernel(const double* __rest
   const int r0 = c * JRC, rows = min(JRC, nrows - r0);
   jac_load_panel(T, X, ldx, pr, r0, rows, t);
   __syncthreads();
-  const int ib = w & 3, jb0 = 2 * (w >> 2);
+  const int ib = (w * JTPW) / JTN, jb0 = (w * JTPW) % JTN;
   const int m = lane >> 2, kk = lane & 3;
-  double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+  double d[JTPW][2];
+#pragma unroll
+  for (int u = 0; u < JTPW; ++u) d[u][0] = d[u][1] = 0.0;
   const double* Ta = T + (8 * ib + m) * JLDR + kk;
-  const double* Tb0 = T + (8 * jb0 + m) * JLDR + kk;
-  const double* Tb1 = Tb0 + 8 * JLDR;
-#pragma unroll 8
+  const double* Tb = T + (8 * jb0 + m) * JLDR + kk;
+#pragma unroll 4
   for (int r = 0; r < JRC; r += 4) {  // zero-padded rows contribute nothing
     const double a = Ta[r];
-    dmma_8x8x4(d00, d01, a, Tb0[r]);
-    dmma_8x8x4(d10, d11, a, Tb1[r]);
+#pragma unroll
+    for (int u = 0; u < JTPW; ++u) dmma_8x8x4(d[u][0], d[u][1], a, Tb[u * 8 * JLDR + r]);
   }
   double* out = part + (static_cast<int64_t>(p) * nchunks + c) * JPW * JPW;
-  const int gi = 8 * ib + m, gj = 8 * jb0 + 2 * kk;
-  out[gi * JPW + gj] = d00;
-  out[gi * JPW + gj + 1] = d01;
-  out[gi * JPW + gj + 8] = d10;
-  out[gi * JPW + gj + 9] = d11;
+  const int gi = 8 * ib + m;
+#pragma unroll
+  for (int u = 0; u < JTPW; ++u) {
+    const int gj = 8 * (jb0 + u) + 2 * kk;
+    out[gi * JPW + gj] = d[u][0];
+    out[gi * JPW + gj + 1] = d[u][1];
+  }
 }
 
 // One pair per CTA of JST = 512 threads: G = sum of the chunk partials (chunk order); if some
@@ -108,7 +116,6 @@ __global__ void __launch_bounds__(JST) jac_solve_kernel(const double* __restrict
                                                         int inner, int cross_only) {
   extern __shared__ double jsm[];
   constexpr int NP = JPW / 2;
-  static_assert(NP * NP == JST / 2 && JPW * NP == JST, "thread maps below assume JPW = 32, JST = 512");
   double* G = jsm;                    // [JPW][JGLD]
   double* Dl = G + JPW * JGLD;        // Δ = W - I
   __shared__ double cs[NP][3];        // c, s, c - 1
@@ -189,8 +196,8 @@ __global__ void __launch_bounds__(JST) jac_solve_kernel(const double* __restrict
         prs[t][1] = b;
       }
       __syncthreads();
-      if (t < NP * NP) {  // G <- J^T G J, the 2 x 2 block (pair qa rows, pair qb columns)
-        const int qa = t / NP, qb = t % NP;
+      for (int idx = t; idx < NP * NP; idx += JST) {  // G <- J^T G J, the 2 x 2 block (pair qa rows, pair qb columns)
+        const int qa = idx / NP, qb = idx % NP;
         const double c1 = cs[qa][0], s1 = cs[qa][1], c2 = cs[qb][0], s2 = cs[qb][1];
         if (s1 != 0.0 || s2 != 0.0) {
           const int a1 = prs[qa][0], b1 = prs[qa][1], a2 = prs[qb][0], b2 = prs[qb][1];
@@ -203,28 +210,24 @@ __global__ void __launch_bounds__(JST) jac_solve_kernel(const double* __restrict
           G[a1 * JGLD + b2] = c1 * h12 - s1 * h22;
           G[b1 * JGLD + b2] = s1 * h12 + c1 * h22;
         }
-      } else {  // Δ <- (I + Δ) J - I: rows r and r + JPW/2 of column pair q
-        const int u = t - NP * NP, q = u % NP;
+      }
+      for (int idx = t; idx < JPW * NP; idx += JST) {  // Δ <- (I + Δ) J - I: row r of column pair q
+        const int q = idx % NP, r = idx / NP;
         const double s = cs[q][1];
-        if (s != 0.0) {
-          const double cm1 = cs[q][2];
-          const int a = prs[q][0], b = prs[q][1];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = u / NP + h * (JPW / 2);
-            const double da = Dl[r * JGLD + a], db = Dl[r * JGLD + b];
-            double na = fma(cm1, da, da) - s * db, nb = fma(cm1, db, db) + s * da;
-            if (r == a) {
-              na += cm1;
-              nb += s;
-            } else if (r == b) {
-              na -= s;
-              nb += cm1;
-            }
-            Dl[r * JGLD + a] = na;
-            Dl[r * JGLD + b] = nb;
-          }
+        if (s == 0.0) continue;
+        const double cm1 = cs[q][2];
+        const int a = prs[q][0], b = prs[q][1];
+        const double da = Dl[r * JGLD + a], db = Dl[r * JGLD + b];
+        double na = fma(cm1, da, da) - s * db, nb = fma(cm1, db, db) + s * da;
+        if (r == a) {
+          na += cm1;
+          nb += s;
+        } else if (r == b) {
+          na -= s;
+          nb += cm1;
         }
+        Dl[r * JGLD + a] = na;
+        Dl[r * JGLD + b] = nb;
       }
       __syncthreads();
     }
@@ -255,14 +258,18 @@ __global__ void __launch_bounds__(JTHREADS) jac_update_kernel(double* __restrict
   jac_load_panel(T, M, ld, pr, r0, rows, t);
   __syncthreads();
   const int m = lane >> 2, kk = lane & 3;
-  double acc[2][4][2] = {};
+  double acc[2][JTN][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int cb = 0; cb < JTN; ++cb) acc[h][cb][0] = acc[h][cb][1] = 0.0;
 #pragma unroll
   for (int ks = 0; ks < JPW; ks += 4) {
     // A(m, kk) = chunk(8 rb + m, ks + kk) = T[ks + kk][8 rb + m];  B(kk, n) = Δ(ks + kk, 8 cb + n), n = lane >> 2
     const double a0 = T[(ks + kk) * JLDR + 16 * w + m];
     const double a1 = T[(ks + kk) * JLDR + 16 * w + 8 + m];
 #pragma unroll
-    for (int cb = 0; cb < 4; ++cb) {
+    for (int cb = 0; cb < JTN; ++cb) {
       const double b = D[(ks + kk) * JLDD + 8 * cb + m];
       dmma_8x8x4(acc[0][cb][0], acc[0][cb][1], a0, b);
       dmma_8x8x4(acc[1][cb][0], acc[1][cb][1], a1, b);
@@ -272,7 +279,7 @@ __global__ void __launch_bounds__(JTHREADS) jac_update_kernel(double* __restrict
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int cb = 0; cb < 4; ++cb) {
+    for (int cb = 0; cb < JTN; ++cb) {
       const int row = 16 * w + 8 * h + m, col = 8 * cb + 2 * kk;
       T[col * JLDR + row] += acc[h][cb][0];
       T[(col + 1) * JLDR + row] += acc[h][cb][1];
