@@ -37,6 +37,7 @@
 #include "gemm_tf32.cuh"
 #include "omega.cuh"
 #include "qrcp.cuh"
+#include "qrcp_persist.cuh"
 #include "small.cuh"
 #include "small_loop.cuh"
 #include "svd.cuh"
@@ -142,7 +143,7 @@ struct qb_ctx_s {
   cudaEvent_t jev[5] = {};
   cudaEvent_t ev_copy = nullptr;
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
-  DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw;  // qb_pivoted_qr
+  DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw, qw2;  // qb_pivoted_qr
   DevBuf X32, T32;  // FP32 contexts: FP32 copies of a CholeskyQR pass's X and T
   DevBuf X32b;      // FP32 contexts: RN_32 of CholeskyQR2's scratch (when the caller takes an FP32 copy)
   DevBuf Bsp;       // FP32 GEMM: a small B operand split into hi / lo
@@ -1316,7 +1317,7 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->QB,    &ctx->R,    &ctx->Usv,    &ctx->Vsv,  &ctx->Ssv, &ctx->Wsv,    &ctx->Ut,
                     &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
-                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->X32,   &ctx->T32,
+                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->qw2,   &ctx->X32,   &ctx->T32,
                     &ctx->Bsp,   &ctx->X32b, &ctx->Jx,    &ctx->Jj,   &ctx->Jpart, &ctx->Jw,
                     &ctx->Jint,  &ctx->Jsig, &ctx->Jpairs, &ctx->Srec, &ctx->Strace, &ctx->Jq2, &ctx->Jm2};
   for (DevBuf* b : bufs)
@@ -1795,10 +1796,77 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
       cudaEventCreate(&pev[0]);
       cudaEventCreate(&pev[1]);
     }
+    // one persistent cooperative launch per panel (qrcp_persist.cuh) when v fits in shared memory
+    // and every CTA owns at most QP_THREADS columns
+    static const int no_persist = debug_env("QB_QRCP_NO_PERSIST");
+    const int G = ctx->num_sms;
+    const size_t qp_smem = sizeof(double) * (size_t)std::max<int64_t>(l + 2 * QP_THREADS, 33 * G);
+    bool persist = !no_persist && l <= QP_MAX_L && (n + G - 1) / G <= QP_THREADS;
+    if (persist) {
+      QB_SMEM_ATTR(qrcp_panel_kernel, (int)(sizeof(double) * (QP_MAX_L + 2 * QP_THREADS)));  // the largest launch
+      if (33 * G > QP_MAX_L + 2 * QP_THREADS) persist = false;
+      int per_sm = 0;
+      QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_panel_kernel, QP_THREADS, qp_smem));
+      persist = per_sm >= 1;
+    }
+    QrcpPanelArgs pa{};
+    if (persist) {
+      QB_TRY(ensure(ctx, ctx->qw2, sizeof(double) * (size_t)(l + 64 + 38 * G + 64)));
+      double* pw = ctx->qw2.d();
+      pa.B = R;
+      pa.ldb = ldr;
+      pa.l = (int)l;
+      pa.n = (int)n;
+      pa.vn1 = vn1;
+      pa.vn2 = vn2;
+      pa.perm = perm;
+      pa.tau = tau;
+      pa.F = F;
+      pa.ldf = ldf;
+      pa.xbuf = pw;
+      pa.alpha = pw + l;
+      pa.bar = reinterpret_cast<unsigned*>(pw + l + 8);
+      pa.ssp = pw + l + 64;
+      pa.auxp = pa.ssp + G;
+      pa.pmax = pa.auxp + 32 * G;
+      pa.pidx = reinterpret_cast<int*>(pa.pmax + G);
+      pa.tol3z = tol3z;
+    }
     for (int i0 = 0; i0 < kmin; i0 += QRCP_NB) {
       const int nb = std::min(QRCP_NB, kmin - i0);
       if (ptrace) cudaEventRecord(pev[0], ctx->stream);
-      for (int i = i0; i < i0 + nb; ++i) {
+      if (persist) {
+        pa.i0 = i0;
+        pa.nb = nb;
+        pa.first = i0 == 0;
+        QB_CUDA(cudaMemsetAsync(pa.bar, 0, sizeof(unsigned), ctx->stream));
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3((unsigned)G);
+        lc.blockDim = dim3(QP_THREADS);
+        lc.dynamicSmemBytes = qp_smem;
+        lc.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        static const int ptr = debug_env("QB_QRCP_PTRACE");  // diagnostics: phase marks of panels 0 and mid
+        const bool trace_this = ptr && (i0 == 0 || i0 == (kmin / 2 / QRCP_NB) * QRCP_NB || i0 + QRCP_NB >= kmin);
+        pa.trace = trace_this ? reinterpret_cast<unsigned long long*>(pa.pidx + 2 * G) : nullptr;
+        QB_CUDA(cudaLaunchKernelEx(&lc, qrcp_panel_kernel, pa));
+        QB_TRY(check_launch(ctx, "qrcp_panel"));
+        if (trace_this) {
+          unsigned long long tr[64];
+          QB_CUDA(cudaMemcpy(tr, pa.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+          for (int s2 = 0; s2 < 4; ++s2) {
+            std::fprintf(stderr, "qrcp panel %d step %d:", i0, s2);
+            for (int k2 = 1; k2 <= 10; ++k2)
+              std::fprintf(stderr, " %.2f", (double)(tr[s2 * 16 + k2] - tr[s2 * 16 + k2 - 1]) * 1e-3);
+            std::fprintf(stderr, " us\n");
+          }
+        }
+      }
+      for (int i = i0; i < i0 + nb && !persist; ++i) {
         const int npart = i > 0 ? (int)((n - i + QRCP_THREADS - 1) / QRCP_THREADS) : 0;
         qrcp_bk_pivot_kernel<<<1, BKP_THREADS, 0, ctx->stream>>>(R, ldr, (int)l, (int)n, i, i0, vn1, tau, F, ldf, vb,
                                                                  piv, pmax, pidx, npart);
@@ -1885,13 +1953,41 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
   qrcp_identity_kernel<<<(int)std::min<int64_t>((l * l + 255) / 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
       Qt, ldqt, (int)l);
   QB_TRY(check_launch(ctx, "qrcp_identity"));
-  for (int i = (int)l - 1; i >= 0; --i) {
-    const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
-    dim3 grid((unsigned)((l - i + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
-    qrcp_q_w_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, parts, ldp);
-    QB_TRY(check_launch(ctx, "qrcp_q_w"));
-    qrcp_q_update_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, tau, parts, ldp, rch);
-    QB_TRY(check_launch(ctx, "qrcp_q_update"));
+  static const int q_unblocked = debug_env("QB_QRCP_Q_UNBLOCKED");
+  if (q_unblocked) {  // reference schedule: one reflector at a time
+    for (int i = (int)l - 1; i >= 0; --i) {
+      const int rch = (int)((l - i + QRCP_ROWS - 1) / QRCP_ROWS);
+      dim3 grid((unsigned)((l - i + QRCP_THREADS - 1) / QRCP_THREADS), (unsigned)rch);
+      qrcp_q_w_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, parts, ldp);
+      QB_TRY(check_launch(ctx, "qrcp_q_w"));
+      qrcp_q_update_kernel<<<grid, QRCP_THREADS, 0, ctx->stream>>>(Qt, ldqt, (int)l, i, R, ldr, tau, parts, ldp,
+                                                                   rch);
+      QB_TRY(check_launch(ctx, "qrcp_q_update"));
+    }
+  } else {  // panels of QRCP_NB reflectors, last to first: Q~(i0:, i0:) -= V (T (V^T Q~(i0:, i0:)))
+    const int64_t ldw = ldqt;
+    QB_TRY(ensure(ctx, ctx->qw, sizeof(double) * (size_t)(QRCP_NB * l + 3 * QRCP_NB * ldw + QRCP_NB * QRCP_NB)));
+    double* Vx = ctx->qw.d();
+    double* Vtp = Vx + QRCP_NB * l;
+    double* Wt = Vtp + QRCP_NB * ldw;
+    double* Zt = Wt + QRCP_NB * ldw;
+    double* Tm = Zt + QRCP_NB * ldw;
+    for (int i0 = (int)((l - 1) / QRCP_NB) * QRCP_NB; i0 >= 0; i0 -= QRCP_NB) {
+      const int nb = (int)std::min<int64_t>(QRCP_NB, l - i0), rows = (int)(l - i0);
+      qrcp_vpanel_kernel<<<(int)std::min<int64_t>(((int64_t)rows * QRCP_NB + 255) / 256, 4 * ctx->num_sms), 256, 0,
+                           ctx->stream>>>(R, ldr, i0, rows, nb, Vx, Vtp, ldw);
+      QB_TRY(check_launch(ctx, "qrcp_vpanel"));
+      qrcp_tmat_kernel<<<1, 1024, 0, ctx->stream>>>(Vx, rows, nb, tau + i0, Tm);
+      QB_TRY(check_launch(ctx, "qrcp_tmat"));
+      // W^T = Q~(i0:, i0:)^T V (column-major views of the row-major Q~ and V)
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, rows, QRCP_NB, rows, Qt + (int64_t)i0 * ldqt + i0, ldqt, Vx, QRCP_NB,
+                  Wt, ldw, false, nullptr));
+      qrcp_tz_kernel<<<(rows + 127) / 128, 128, 0, ctx->stream>>>(Tm, Wt, ldw, rows, Zt);
+      QB_TRY(check_launch(ctx, "qrcp_tz"));
+      // Q~(i0:, i0:)^T -= Z^T V^T
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, rows, rows, QRCP_NB, Zt, ldw, Vtp, ldw, Qt + (int64_t)i0 * ldqt + i0,
+                  ldqt, false, nullptr));
+    }
   }
   qrcp_zero_lower_kernel<<<(int)std::min<int64_t>((l * l + 255) / 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
       R, ldr, (int)l);

@@ -956,3 +956,75 @@ __global__ void qrcp_bk_vt_kernel(const double* __restrict__ B, int64_t ldb, int
 }
 
 }  // namespace qbk
+
+namespace qbk {
+
+// ---------------------------------------------------------------- blocked Q~ accumulation
+// Q~ = H_0 ... H_{l-1} I backward by panels of QRCP_NB reflectors (LAPACK dorgqr/dlarft):
+// H_{i0} ... H_{i0+nb-1} = I - V T V^T with T upper triangular (forward, columnwise), applied as
+// Q~(i0:, i0:) -= V (T (V^T Q~(i0:, i0:))) — two GEMMs on the DMMA path per panel.
+
+// V of the panel (rows i0.., unit diagonal, zero above it, the Householder vectors below — stored
+// below R's diagonal) in two layouts: Vx[r'][q] (ld QRCP_NB) and Vt[q][r'] (ld ldv); q >= nb: 0.
+__global__ void qrcp_vpanel_kernel(const double* __restrict__ B, int64_t ldb, int i0, int rows, int nb,
+                                   double* __restrict__ Vx, double* __restrict__ Vt, int64_t ldv) {
+  const int64_t total = static_cast<int64_t>(rows) * QRCP_NB;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / QRCP_NB), q = static_cast<int>(idx % QRCP_NB);
+    const double v = q >= nb || r < q ? 0.0 : (r == q ? 1.0 : B[static_cast<int64_t>(i0 + r) * ldb + i0 + q]);
+    Vx[idx] = v;
+    Vt[q * ldv + r] = v;
+  }
+}
+
+// T (QRCP_NB x QRCP_NB, row-major, upper) of the panel: G = V^T V, then dlarft's forward
+// columnwise recurrence T(0:j, j) = T(0:j, 0:j) (-tau_j G(0:j, j)), T(j, j) = tau_j.
+__global__ void __launch_bounds__(1024) qrcp_tmat_kernel(const double* __restrict__ Vx, int rows, int nb,
+                                                         const double* __restrict__ tau, double* __restrict__ Tm) {
+  __shared__ double Gs[QRCP_NB][QRCP_NB + 1];
+  __shared__ double Ts[QRCP_NB][QRCP_NB + 1];
+  __shared__ double col[QRCP_NB];
+  const int tid = threadIdx.x, a = tid >> 5, b = tid & 31;  // G(a, b) per thread
+  double s = 0.0;
+  if (a <= b)
+    for (int r = 0; r < rows; ++r) s = fma(Vx[r * QRCP_NB + a], Vx[r * QRCP_NB + b], s);
+  Gs[a][b] = s;
+  Ts[a][b] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double tj = tau[j];
+    if (tid < j) col[tid] = -tj * Gs[tid][j];
+    __syncthreads();
+    if (tid < j) {
+      double t = 0.0;
+      for (int k = tid; k < j; ++k) t = fma(Ts[tid][k], col[k], t);
+      Ts[tid][j] = t;
+    }
+    if (tid == 0) Ts[j][j] = tj;
+    __syncthreads();
+  }
+  Tm[a * QRCP_NB + b] = Ts[a][b];
+}
+
+// Zt[j' + q ldw] = sum_{s >= q} T(q, s) Wt[j' + s ldw] (Z = T W, stored transposed like W).
+__global__ void qrcp_tz_kernel(const double* __restrict__ Tm, const double* __restrict__ Wt, int64_t ldw, int ncol,
+                               double* __restrict__ Zt) {
+  __shared__ double Ts[QRCP_NB * QRCP_NB];
+  for (int e = threadIdx.x; e < QRCP_NB * QRCP_NB; e += blockDim.x) Ts[e] = Tm[e];
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncol) return;
+  double w[QRCP_NB];
+#pragma unroll
+  for (int s = 0; s < QRCP_NB; ++s) w[s] = Wt[j + s * ldw];
+#pragma unroll
+  for (int q = 0; q < QRCP_NB; ++q) {
+    double z = 0.0;
+#pragma unroll
+    for (int s = q; s < QRCP_NB; ++s) z = fma(Ts[q * QRCP_NB + s], w[s], z);
+    Zt[j + q * ldw] = z;
+  }
+}
+
+}  // namespace qbk

@@ -1,0 +1,452 @@
+// qrcp_persist.cuh — one panel of the blocked pivoted QR (qrcp.cuh's dlaqps-style schedule) in ONE
+// persistent cooperative launch: one CTA per SM, two grid-wide barriers per pivot step instead of
+// three kernel boundaries, and the per-step work spread over the whole GPU.
+//
+// Per step i = i0 + kk (same arithmetic as qrcp_bk_*, LAPACK dlaqps/dlaqp2):
+//   phase A (rows >= i partitioned over the CTAs, a warp per row):
+//     p = argmax of the previous step's per-CTA maxima (first index on ties);
+//     x_r = A(r, p) - A(r, i0:i) F(p, 0:kk)^T (the pivot column's pending update), the swap of
+//     columns i and p in rows >= i (rows < i: the finished rows of R, swapped here too), perm;
+//     per-CTA partials of sum_{r>i} x_r^2 and of V(r, q) x_r (for F's incremental update).
+//   barrier
+//   phase B (columns >= i0 partitioned over the CTAs):
+//     every CTA forms the reflector (dlarfg) from the partials in the same order: beta, tau,
+//     v = [1; x / (alpha - beta)], and aux(q) = -tau V(i:, q)^T v;
+//     w_j = A(i:, j)^T v over the CTA's columns (the read-only pass over the stale trailing block);
+//     F(j, kk) = tau w_j + F(j, 0:kk) aux; row i: A(i, j) -= A(i, i0:i) F(j, 0:kk)^T + F(j, kk);
+//     the dlaqp2 norm downdate, exact recompute of flagged columns (CTA-wide, packed); the CTA's
+//     (max, first index) for the next pivot; v into column i, beta on the diagonal.
+//   barrier
+// Data written by one CTA and read by another inside the launch is read with ld.global.cg (L2;
+// the SMs' L1 is not coherent).
+#pragma once
+
+#include "common.cuh"
+#include "qrcp.cuh"
+
+namespace qbk {
+
+constexpr int QP_THREADS = 512;
+constexpr int QP_WARPS = QP_THREADS / 32;
+constexpr int QP_MAX_L = 12288;  // v staged in shared memory (96 KB)
+
+struct QrcpPanelArgs {
+  double* B;
+  int64_t ldb;
+  int l, n, i0, nb;
+  double* vn1;
+  double* vn2;
+  int* perm;
+  double* tau;
+  double* F;
+  int64_t ldf;
+  double* xbuf;   // l: x of the current step
+  double* ssp;    // G: per-CTA sum of squares
+  double* auxp;   // G x 32: per-CTA V^T x partials
+  double* alpha;  // 1: x_i
+  double* pmax;   // G
+  int* pidx;      // G
+  unsigned* bar;  // grid barrier counter (zeroed before the launch)
+  double tol3z;
+  int first;      // step i0 == 0: pick the first pivot from vn1 itself
+  unsigned long long* trace;  // diagnostics (QB_QRCP_PTRACE): %globaltimer marks of CTA 0, steps 0-3
+};
+
+#define QP_MARK(k)                                                                 \
+  do {                                                                             \
+    if (a.trace && c == 0 && tid == 0 && kk < 4) {                                 \
+      unsigned long long t_;                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                       \
+      a.trace[kk * 16 + (k)] = t_;                                                 \
+    }                                                                              \
+  } while (0)
+
+__device__ __forceinline__ void qp_grid_sync(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (*reinterpret_cast<volatile unsigned*>(bar) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+__global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPanelArgs a) {
+  extern __shared__ __align__(16) double qp_sm[];
+  double* xs = qp_sm;  // v (rows >= i), l - i entries
+  __shared__ double s_red[QP_WARPS][33];
+  __shared__ double s_fp[QRCP_NB], s_aux[QRCP_NB], s_ai[QRCP_NB];
+  __shared__ double s_scal[4];  // beta, tau, scale
+  __shared__ int s_p;
+  __shared__ double s_bv[QP_WARPS];
+  __shared__ int s_bi[QP_WARPS];
+  __shared__ int s_cnt[QP_WARPS], s_list[QP_THREADS];
+  __shared__ double s_res[QP_THREADS];
+  __shared__ double s_tot[33];
+
+  double* __restrict__ B = a.B;
+  const int64_t ldb = a.ldb, ldf = a.ldf;
+  const int l = a.l, n = a.n, i0 = a.i0;
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // columns owned in phase B: [cj0, cj1), fixed for the panel
+  const int ncols = n - i0, cw = (ncols + G - 1) / G;
+  const int cj0 = i0 + c * cw, cj1 = min(n, cj0 + cw);
+  unsigned target = 0;
+
+  for (int kk = 0; kk < a.nb; ++kk) {
+    const int i = i0 + kk;
+    QP_MARK(0);
+    // ---------------- phase A
+    {
+      double best = -1.0;
+      int bi = n;
+      if (a.first && kk == 0) {
+        for (int j = i + tid; j < n; j += QP_THREADS) {
+          const double v = ldcg(a.vn1 + j);
+          if (v > best) {
+            best = v;
+            bi = j;
+          }
+        }
+      } else {
+        for (int q = tid; q < G; q += QP_THREADS) {
+          const double v = ldcg(a.pmax + q);
+          const int x = __ldcg(a.pidx + q);
+          if (v > best || (v == best && x < bi)) {
+            best = v;
+            bi = x;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_bv[warp] = best;
+        s_bi[warp] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double b = s_bv[0];
+        int x = s_bi[0];
+        for (int w = 1; w < QP_WARPS; ++w)
+          if (s_bv[w] > b || (s_bv[w] == b && s_bi[w] < x)) {
+            b = s_bv[w];
+            x = s_bi[w];
+          }
+        s_p = x;
+      }
+      __syncthreads();
+    }
+    const int p = s_p;
+    QP_MARK(1);
+    if (tid < kk) s_fp[tid] = ldcg(a.F + tid * ldf + p);  // F(i, :) after the swap
+    __syncthreads();
+    {
+      const int rows = l - i, rc = (rows + G - 1) / G;
+      const int ra = i + c * rc, rz = min(l, ra + rc);
+      double ss = 0.0, ax = 0.0;  // ax: lane q's sum of V(r, q) x_r
+      for (int r0 = ra + warp; r0 < rz; r0 += 2 * QP_WARPS) {  // two rows per warp in flight
+        double vq[2], ap[2], aiv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = r0 + u * QP_WARPS;
+          const double* ar = B + static_cast<int64_t>(min(r, rz - 1)) * ldb;
+          vq[u] = lane < kk ? ldcg(ar + i0 + lane) : 0.0;
+          ap[u] = ldcg(ar + p);
+          aiv[u] = ldcg(ar + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = r0 + u * QP_WARPS;
+          if (r >= rz) break;
+          // lane 0's sum for every lane (the xor tree's lanes may differ in the last bit)
+          const double x = __shfl_sync(0xffffffffu, ap[u] - warp_sum(lane < kk ? vq[u] * s_fp[lane] : 0.0), 0);
+          if (r > i) {
+            if (lane == 0) ss = fma(x, x, ss);
+            ax = fma(vq[u], x, ax);
+          } else if (lane == 0) {
+            a.alpha[0] = x;
+          }
+          if (lane == 0) {
+            a.xbuf[r - i] = x;
+            if (p != i) B[static_cast<int64_t>(r) * ldb + p] = aiv[u];
+          }
+        }
+      }
+      // rows < i (finished rows of R): columns i and p swapped
+      if (p != i) {
+        const int rc2 = (i + G - 1) / G;
+        for (int r = c * rc2 + tid; r < min(i, (c + 1) * rc2); r += QP_THREADS) {
+          double* ar = B + static_cast<int64_t>(r) * ldb;
+          const double t0 = ldcg(ar + i), t1 = ldcg(ar + p);
+          ar[i] = t1;
+          ar[p] = t0;
+        }
+        if (c == 0 && tid == 0) {
+          const int t = a.perm[i];
+          a.perm[i] = a.perm[p];
+          a.perm[p] = t;
+        }
+      }
+      s_red[warp][lane] = ax;
+      ss = warp_sum(ss);
+      if (lane == 0) s_red[warp][32] = ss;
+      __syncthreads();
+      if (tid < 33) {
+        double t = 0.0;
+        for (int w = 0; w < QP_WARPS; ++w) t += s_red[w][tid];
+        if (tid < 32) a.auxp[c * 32 + tid] = t;
+        else a.ssp[c] = t;
+      }
+    }
+    QP_MARK(2);
+    target += G;
+    qp_grid_sync(a.bar, target);
+    QP_MARK(3);
+
+    // ---------------- phase B
+    // this thread's column (independent of the reflector): F's row, A(i, j) and the norms, read
+    // through the swap, issued before the reductions so that their latency overlaps them
+    const int ja = max(cj0, i + 1), jn = cj1 - ja;
+    const bool own = tid < jn;
+    const int jt = ja + tid, js = own && jt == p ? i : jt;
+    double fr[QRCP_NB];
+#pragma unroll
+    for (int q = 0; q < QRCP_NB; ++q) fr[q] = own && q < kk ? ldcg(a.F + q * ldf + js) : 0.0;
+    const double bij_old = own ? ldcg(B + static_cast<int64_t>(i) * ldb + jt) : 0.0;
+    double n1 = own ? ldcg(a.vn1 + js) : 0.0, n2 = own ? ldcg(a.vn2 + js) : 1.0;
+    // reflector and aux, every CTA in the same order: warp w sums the partials of CTAs
+    // [w*cpw, (w+1)*cpw) (lane q: aux partial q; lane 0 also the sum of squares), then 33 threads
+    // sum the warps in order
+    {
+      const int cpw = (G + QP_WARPS - 1) / QP_WARPS, ca = warp * cpw, cz = min(G, ca + cpw);
+      double t = 0.0, s2 = 0.0;
+#pragma unroll 4
+      for (int cc = ca; cc < cz; ++cc) {
+        if (lane < kk) t += ldcg(a.auxp + cc * 32 + lane);
+        if (lane == 0) s2 += ldcg(a.ssp + cc);
+      }
+      s_red[warp][lane] = t;
+      if (lane == 0) s_red[warp][32] = s2;
+      __syncthreads();
+      if (tid < 33) {
+        double u = 0.0;
+        for (int w = 0; w < QP_WARPS; ++w) u += s_red[w][tid];
+        s_tot[tid] = u;
+      }
+      __syncthreads();
+    }
+    if (tid < 32) {
+      const double t = s_tot[32], aq = s_tot[tid];
+      const double alpha = ldcg(a.alpha);
+      double beta, tv, scale;
+      if (t == 0.0) {
+        tv = 0.0;
+        beta = alpha;
+        scale = 0.0;
+      } else {
+        const double nrm = sqrt(fma(alpha, alpha, t));
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tv = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      if (tid < kk) {
+        const double vi = ldcg(B + static_cast<int64_t>(i) * ldb + i0 + tid);  // V(i, q)
+        s_ai[tid] = vi;
+        s_aux[tid] = -tv * (vi + scale * aq);
+      }
+      if (tid == 0) {
+        s_scal[0] = beta;
+        s_scal[1] = tv;
+        s_scal[2] = scale;
+        if (c == 0) a.tau[i] = tv;
+      }
+    }
+    __syncthreads();
+    QP_MARK(4);
+    const double beta = s_scal[0], tv = s_scal[1], scale = s_scal[2];
+    double f0 = 0.0, rowsum = 0.0;  // F(j, 0:kk) aux and A(i, i0:i) F(j, 0:kk)^T
+#pragma unroll
+    for (int q = 0; q < QRCP_NB; ++q)
+      if (q < kk) {
+        f0 = fma(fr[q], s_aux[q], f0);
+        rowsum = fma(s_ai[q], fr[q], rowsum);
+        if (own && js != jt) a.F[q * ldf + jt] = fr[q];  // F's row follows the swap
+      }
+    for (int r = i + tid; r < l; r += QP_THREADS) xs[r - i] = r == i ? 1.0 : ldcg(a.xbuf + r - i) * scale;
+    __syncthreads();
+    QP_MARK(5);
+    // v into column i (phase A's row partition), beta on the diagonal
+    {
+      const int rows = l - i, rc = (rows + G - 1) / G;
+      const int ra = i + c * rc, rz = min(l, ra + rc);
+      for (int r = ra + tid; r < rz; r += QP_THREADS)
+        B[static_cast<int64_t>(r) * ldb + i] = r == i ? beta : xs[r - i];
+    }
+    // w over the owned columns j > i: warps over (32-column chunk, row split)
+    const int nch = jn > 0 ? (jn + 31) / 32 : 0;
+    const int S = nch > 0 ? max(1, QP_WARPS / nch) : 1;
+    double* wp = xs + (l - i);  // S x nch*32 partials
+    for (int u = warp; u < nch * S; u += QP_WARPS) {
+      const int ch = u % nch, sp = u / nch;
+      const int j = ja + ch * 32 + lane;
+      const int jc = j < cj1 ? j : ja;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      const int rows = l - i, rs = (rows + S - 1) / S;
+      const int r0 = i + sp * rs, r1 = min(l, r0 + rs);
+      int r = r0;
+      for (; r + 15 < r1; r += 16) {
+        const double* ar = B + static_cast<int64_t>(r) * ldb + jc;
+        double t[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) t[e] = ldcg(ar + e * ldb);
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          s0 = fma(xs[r + e - i], t[e], s0);
+          s1 = fma(xs[r + e + 1 - i], t[e + 1], s1);
+          s2 = fma(xs[r + e + 2 - i], t[e + 2], s2);
+          s3 = fma(xs[r + e + 3 - i], t[e + 3], s3);
+        }
+      }
+      for (; r < r1; ++r) s0 = fma(xs[r - i], ldcg(B + static_cast<int64_t>(r) * ldb + jc), s0);
+      wp[sp * (nch * 32) + ch * 32 + lane] = (s0 + s1) + (s2 + s3);  // slot (row split, column)
+    }
+    __syncthreads();
+    QP_MARK(6);
+    // per owned column j > i (one per thread: a CTA owns at most QP_THREADS columns, checked on the
+    // host): w, F, the row update, the norm downdate
+    bool recompute = false;
+    if (own) {
+      double w = 0.0;
+      for (int sp = 0; sp < S; ++sp) w += wp[sp * (nch * 32) + tid];
+      const double f = fma(tv, w, f0);
+      a.F[kk * ldf + jt] = f;
+      const double rij = bij_old - rowsum - f;
+      B[static_cast<int64_t>(i) * ldb + jt] = rij;
+      if (n1 != 0.0) {
+        double temp = fabs(rij) / n1;
+        temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+        const double ratio = n1 / n2;
+        if (temp * ratio * ratio <= a.tol3z) recompute = true;
+        else n1 = n1 * sqrt(temp);
+      }
+    }
+    QP_MARK(7);
+    // exact norms of the flagged columns (packed 32 to a group, warps over row slices)
+    {
+      const unsigned ballot = __ballot_sync(0xffffffffu, recompute);
+      if (lane == 0) s_cnt[warp] = __popc(ballot);
+      __syncthreads();
+      int base = 0, total = 0;
+      for (int w = 0; w < QP_WARPS; ++w) {
+        if (w < warp) base += s_cnt[w];
+        total += s_cnt[w];
+      }
+      if (recompute) s_list[base + __popc(ballot & ((1u << lane) - 1u))] = tid;
+      __syncthreads();
+      const int rows = l - i - 1, slice = (rows + QP_WARPS - 1) / QP_WARPS;
+      const int ra = i + 1 + warp * slice, rz = min(l, ra + slice);
+      for (int g = 0; g < total; g += 32) {
+        const bool act = g + lane < total;
+        const int tl = act ? s_list[g + lane] : 0;
+        const int col = act ? ja + tl : i;
+        double f2[QRCP_NB];
+#pragma unroll
+        for (int q = 0; q < QRCP_NB; ++q) f2[q] = act && q < kk ? ldcg(a.F + q * ldf + col) : 0.0;
+        const double fk = act ? ldcg(a.F + kk * ldf + col) : 0.0;
+        double sa = 0.0, sb = 0.0;
+        int r = ra;
+        for (; r + 1 < rz; r += 2) {  // two rows in flight
+          const double* a0 = B + static_cast<int64_t>(r) * ldb;
+          const double* a1 = a0 + ldb;
+          double x0 = fma(-xs[r - i], fk, ldcg(a0 + col)), x1 = fma(-xs[r + 1 - i], fk, ldcg(a1 + col));
+#pragma unroll
+          for (int q = 0; q < QRCP_NB; q += 2)
+            if (q < kk) {
+              const double2 u0 = __ldcg(reinterpret_cast<const double2*>(a0 + i0 + q));
+              const double2 u1 = __ldcg(reinterpret_cast<const double2*>(a1 + i0 + q));
+              x0 = fma(-u0.x, f2[q], x0);
+              x1 = fma(-u1.x, f2[q], x1);
+              x0 = fma(-u0.y, f2[q + 1], x0);
+              x1 = fma(-u1.y, f2[q + 1], x1);
+            }
+          sa = fma(x0, x0, sa);
+          sb = fma(x1, x1, sb);
+        }
+        if (r < rz) {
+          const double* a0 = B + static_cast<int64_t>(r) * ldb;
+          double x0 = fma(-xs[r - i], fk, ldcg(a0 + col));
+#pragma unroll
+          for (int q = 0; q < QRCP_NB; q += 2)
+            if (q < kk) {
+              const double2 u0 = __ldcg(reinterpret_cast<const double2*>(a0 + i0 + q));
+              x0 = fma(-u0.x, f2[q], x0);
+              x0 = fma(-u0.y, f2[q + 1], x0);
+            }
+          sa = fma(x0, x0, sa);
+        }
+        sa += sb;
+        s_red[warp][lane] = sa;
+        __syncthreads();
+        if (warp == 0 && act) {
+          double t2 = 0.0;
+          for (int w = 0; w < QP_WARPS; ++w) t2 += s_red[w][lane];
+          s_res[tl] = sqrt(t2);
+        }
+        __syncthreads();
+      }
+    }
+    QP_MARK(8);
+    double best = -1.0;
+    int bi = n;
+    if (own) {
+      if (recompute) {
+        n1 = s_res[tid];
+        n2 = n1;
+      }
+      a.vn1[jt] = n1;
+      a.vn2[jt] = n2;
+      best = n1;
+      bi = jt;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      s_bv[warp] = best;
+      s_bi[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < QP_WARPS; ++w)
+        if (s_bv[w] > best || (s_bv[w] == best && s_bi[w] < bi)) {
+          best = s_bv[w];
+          bi = s_bi[w];
+        }
+      a.pmax[c] = best;
+      a.pidx[c] = bi;
+    }
+    QP_MARK(9);
+    target += G;
+    qp_grid_sync(a.bar, target);
+    QP_MARK(10);
+  }
+}
+
+}  // namespace qbk
