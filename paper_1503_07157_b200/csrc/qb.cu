@@ -1801,7 +1801,7 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
     static const int no_persist = debug_env("QB_QRCP_NO_PERSIST");
     const int G = ctx->num_sms;
     const size_t qp_smem = sizeof(double) * (size_t)std::max<int64_t>(l + 2 * QP_THREADS, 33 * G);
-    bool persist = !no_persist && l <= QP_MAX_L && (n + G - 1) / G <= QP_THREADS;
+    bool persist = !no_persist && l <= QP_MAX_L && (n + G - 1) / G <= QP_THREADS && G <= QP_WARPS * QP_CPW;
     if (persist) {
       QB_SMEM_ATTR(qrcp_panel_kernel, (int)(sizeof(double) * (QP_MAX_L + 2 * QP_THREADS)));  // the largest launch
       if (33 * G > QP_MAX_L + 2 * QP_THREADS) persist = false;
@@ -1811,7 +1811,7 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
     }
     QrcpPanelArgs pa{};
     if (persist) {
-      QB_TRY(ensure(ctx, ctx->qw2, sizeof(double) * (size_t)(l + 64 + 38 * G + 64)));
+      QB_TRY(ensure(ctx, ctx->qw2, sizeof(double) * (size_t)(l + 64 + 38 * G + 512)));
       double* pw = ctx->qw2.d();
       pa.B = R;
       pa.ldb = ldr;
@@ -1856,8 +1856,22 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
         QB_CUDA(cudaLaunchKernelEx(&lc, qrcp_panel_kernel, pa));
         QB_TRY(check_launch(ctx, "qrcp_panel"));
         if (trace_this) {
-          unsigned long long tr[64];
+          unsigned long long tr[64 + 320];
           QB_CUDA(cudaMemcpy(tr, pa.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+          for (int h = 0; h < 2; ++h) {  // arrival spread at the barriers of step 1 (h = 0: second, 1: first)
+            const unsigned long long* ar = tr + 64 + 160 * h;
+            unsigned long long mn = ~0ull, mx = 0;
+            int cmx = 0;
+            for (int cc = 0; cc < G; ++cc) {
+              mn = std::min(mn, ar[cc]);
+              if (ar[cc] > mx) {
+                mx = ar[cc];
+                cmx = cc;
+              }
+            }
+            std::fprintf(stderr, "qrcp panel %d step 1 barrier %d arrival spread %.2f us (last CTA %d)\n", i0, 2 - h,
+                         (double)(mx - mn) * 1e-3, cmx);
+          }
           for (int s2 = 0; s2 < 4; ++s2) {
             std::fprintf(stderr, "qrcp panel %d step %d:", i0, s2);
             for (int k2 = 1; k2 <= 10; ++k2)
@@ -1953,6 +1967,12 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
   qrcp_identity_kernel<<<(int)std::min<int64_t>((l * l + 255) / 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
       Qt, ldqt, (int)l);
   QB_TRY(check_launch(ctx, "qrcp_identity"));
+  static const int qtrace = debug_env("QB_QRCP_TRACE");
+  cudaEvent_t qev[3] = {nullptr, nullptr, nullptr};
+  if (qtrace) {
+    for (auto& e : qev) cudaEventCreate(&e);
+    cudaEventRecord(qev[0], ctx->stream);
+  }
   static const int q_unblocked = debug_env("QB_QRCP_Q_UNBLOCKED");
   if (q_unblocked) {  // reference schedule: one reflector at a time
     for (int i = (int)l - 1; i >= 0; --i) {
@@ -1966,18 +1986,22 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
     }
   } else {  // panels of QRCP_NB reflectors, last to first: Q~(i0:, i0:) -= V (T (V^T Q~(i0:, i0:)))
     const int64_t ldw = ldqt;
-    QB_TRY(ensure(ctx, ctx->qw, sizeof(double) * (size_t)(QRCP_NB * l + 3 * QRCP_NB * ldw + QRCP_NB * QRCP_NB)));
+    QB_TRY(ensure(ctx, ctx->qw, sizeof(double) * (size_t)(QRCP_NB * l + 3 * QRCP_NB * ldw + 2 * QRCP_NB * QRCP_NB)));
     double* Vx = ctx->qw.d();
     double* Vtp = Vx + QRCP_NB * l;
     double* Wt = Vtp + QRCP_NB * ldw;
     double* Zt = Wt + QRCP_NB * ldw;
     double* Tm = Zt + QRCP_NB * ldw;
+    double* Gq = Tm + QRCP_NB * QRCP_NB;
     for (int i0 = (int)((l - 1) / QRCP_NB) * QRCP_NB; i0 >= 0; i0 -= QRCP_NB) {
       const int nb = (int)std::min<int64_t>(QRCP_NB, l - i0), rows = (int)(l - i0);
       qrcp_vpanel_kernel<<<(int)std::min<int64_t>(((int64_t)rows * QRCP_NB + 255) / 256, 4 * ctx->num_sms), 256, 0,
                            ctx->stream>>>(R, ldr, i0, rows, nb, Vx, Vtp, ldw);
       QB_TRY(check_launch(ctx, "qrcp_vpanel"));
-      qrcp_tmat_kernel<<<1, 1024, 0, ctx->stream>>>(Vx, rows, nb, tau + i0, Tm);
+      // G = V^T V (the DMMA GEMM on the column-major view of the row-major Vx), then T
+      QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, QRCP_NB, QRCP_NB, rows, Vx, QRCP_NB, Vx, QRCP_NB, Gq, QRCP_NB, false,
+                  nullptr));
+      qrcp_tmat_kernel<<<1, 32, 0, ctx->stream>>>(Gq, nb, tau + i0, Tm);
       QB_TRY(check_launch(ctx, "qrcp_tmat"));
       // W^T = Q~(i0:, i0:)^T V (column-major views of the row-major Q~ and V)
       QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, rows, QRCP_NB, rows, Qt + (int64_t)i0 * ldqt + i0, ldqt, Vx, QRCP_NB,
@@ -1993,8 +2017,18 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
       R, ldr, (int)l);
   QB_TRY(check_launch(ctx, "qrcp_zero_lower"));
   QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)(16 * ctx->num_sms)));
+  if (qtrace) cudaEventRecord(qev[1], ctx->stream);
   QB_TRY(gemm(ctx, GEMM_NN, EPI_STORE_COL, (int)m, (int)l, (int)l, ctx->Qbar.d(), ctx->ldq, Qt, ldqt, ctx->Qh.d(), ldm,
               false, nullptr));
+  if (qtrace) {
+    float t1 = 0.f, t2 = 0.f;
+    cudaEventRecord(qev[2], ctx->stream);
+    cudaEventSynchronize(qev[2]);
+    cudaEventElapsedTime(&t1, qev[0], qev[1]);
+    cudaEventElapsedTime(&t2, qev[1], qev[2]);
+    std::fprintf(stderr, "qrcp Q~ accumulation %.3f ms, Q^ = Q Q~ GEMM %.3f ms\n", t1, t2);
+    for (auto& e : qev) cudaEventDestroy(e);
+  }
   std::vector<int> hperm((size_t)n);
   QB_CUDA(cudaMemcpyAsync(hperm.data(), perm, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
   QB_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -978,33 +978,28 @@ __global__ void qrcp_vpanel_kernel(const double* __restrict__ B, int64_t ldb, in
   }
 }
 
-// T (QRCP_NB x QRCP_NB, row-major, upper) of the panel: G = V^T V, then dlarft's forward
-// columnwise recurrence T(0:j, j) = T(0:j, 0:j) (-tau_j G(0:j, j)), T(j, j) = tau_j.
-__global__ void __launch_bounds__(1024) qrcp_tmat_kernel(const double* __restrict__ Vx, int rows, int nb,
-                                                         const double* __restrict__ tau, double* __restrict__ Tm) {
+// T (QRCP_NB x QRCP_NB, row-major, upper) of the panel from G = V^T V (column-major, ld QRCP_NB)
+// and tau: the "UT transform" form of dlarft's T, T^{-1} = diag(1/tau) + striu(G) (Joffrain et al.
+// 2006), solved by back substitution T(i, j) = tau_i (delta_ij - sum_{k>i} G(i, k) T(k, j)) — one
+// warp, lane j owns column j in registers (tau_i = 0 gives a zero row, as dlarft does).
+__global__ void __launch_bounds__(32) qrcp_tmat_kernel(const double* __restrict__ Gm, int nb,
+                                                       const double* __restrict__ tau, double* __restrict__ Tm) {
   __shared__ double Gs[QRCP_NB][QRCP_NB + 1];
-  __shared__ double Ts[QRCP_NB][QRCP_NB + 1];
-  __shared__ double col[QRCP_NB];
-  const int tid = threadIdx.x, a = tid >> 5, b = tid & 31;  // G(a, b) per thread
-  double s = 0.0;
-  if (a <= b)
-    for (int r = 0; r < rows; ++r) s = fma(Vx[r * QRCP_NB + a], Vx[r * QRCP_NB + b], s);
-  Gs[a][b] = s;
-  Ts[a][b] = 0.0;
-  __syncthreads();
-  for (int j = 0; j < nb; ++j) {
-    const double tj = tau[j];
-    if (tid < j) col[tid] = -tj * Gs[tid][j];
-    __syncthreads();
-    if (tid < j) {
-      double t = 0.0;
-      for (int k = tid; k < j; ++k) t = fma(Ts[tid][k], col[k], t);
-      Ts[tid][j] = t;
-    }
-    if (tid == 0) Ts[j][j] = tj;
-    __syncthreads();
+  __shared__ double ts[QRCP_NB];
+  const int j = threadIdx.x;
+  for (int i = 0; i < QRCP_NB; ++i) Gs[i][j] = Gm[i + j * QRCP_NB];  // G(i, j), column-major
+  ts[j] = j < nb ? tau[j] : 0.0;
+  __syncwarp();
+  double t[QRCP_NB];
+#pragma unroll
+  for (int i = QRCP_NB - 1; i >= 0; --i) {
+    double s = i == j ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = i + 1; k < QRCP_NB; ++k) s = fma(-Gs[i][k], t[k], s);
+    t[i] = i <= j ? ts[i] * s : 0.0;
   }
-  Tm[a * QRCP_NB + b] = Ts[a][b];
+#pragma unroll
+  for (int i = 0; i < QRCP_NB; ++i) Tm[i * QRCP_NB + j] = t[i];
 }
 
 // Zt[j' + q ldw] = sum_{s >= q} T(q, s) Wt[j' + s ldw] (Z = T W, stored transposed like W).

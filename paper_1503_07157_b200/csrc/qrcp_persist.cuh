@@ -29,6 +29,7 @@ namespace qbk {
 constexpr int QP_THREADS = 512;
 constexpr int QP_WARPS = QP_THREADS / 32;
 constexpr int QP_MAX_L = 12288;  // v staged in shared memory (96 KB)
+constexpr int QP_CPW = 16;       // CTAs per warp in the partial sums: gridDim.x <= QP_WARPS * QP_CPW
 
 struct QrcpPanelArgs {
   double* B;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
   extern __shared__ __align__(16) double qp_sm[];
   double* xs = qp_sm;  // v (rows >= i), l - i entries
   __shared__ double s_red[QP_WARPS][33];
-  __shared__ double s_fp[QRCP_NB], s_aux[QRCP_NB], s_ai[QRCP_NB];
+  __shared__ double s_aux[QRCP_NB], s_ai[QRCP_NB];
   __shared__ double s_scal[4];  // beta, tau, scale
   __shared__ int s_p;
   __shared__ double s_bv[QP_WARPS];
@@ -100,6 +101,18 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     const int i = i0 + kk;
     QP_MARK(0);
     // ---------------- phase A
+    // this CTA's rows [ra, rz) of rows >= i; the first two per warp prefetched before the pivot is
+    // known (their panel entries and A(r, i) do not depend on it)
+    const int rcA = (l - i + G - 1) / G;
+    const int raA = i + c * rcA, rzA = min(l, raA + rcA);
+    double vq0[2], aiv0[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = raA + warp + u * QP_WARPS;
+      const double* ar = B + static_cast<int64_t>(r < rzA ? r : i) * ldb;
+      vq0[u] = r < rzA && lane < kk ? ldcg(ar + i0 + lane) : 0.0;
+      aiv0[u] = r < rzA ? ldcg(ar + i) : 0.0;
+    }
     {
       double best = -1.0;
       int bi = n;
@@ -149,28 +162,28 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     }
     const int p = s_p;
     QP_MARK(1);
-    if (tid < kk) s_fp[tid] = ldcg(a.F + tid * ldf + p);  // F(i, :) after the swap
-    __syncthreads();
+    const double fpl = lane < kk ? ldcg(a.F + lane * ldf + p) : 0.0;  // F(i, lane) after the swap
     {
       const int rows = l - i, rc = (rows + G - 1) / G;
       const int ra = i + c * rc, rz = min(l, ra + rc);
       double ss = 0.0, ax = 0.0;  // ax: lane q's sum of V(r, q) x_r
       for (int r0 = ra + warp; r0 < rz; r0 += 2 * QP_WARPS) {  // two rows per warp in flight
         double vq[2], ap[2], aiv[2];
+        const bool pre = r0 == ra + warp;  // the prefetched pair
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int r = r0 + u * QP_WARPS;
           const double* ar = B + static_cast<int64_t>(min(r, rz - 1)) * ldb;
-          vq[u] = lane < kk ? ldcg(ar + i0 + lane) : 0.0;
+          vq[u] = pre ? vq0[u] : (lane < kk ? ldcg(ar + i0 + lane) : 0.0);
           ap[u] = ldcg(ar + p);
-          aiv[u] = ldcg(ar + i);
+          aiv[u] = pre ? aiv0[u] : ldcg(ar + i);
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int r = r0 + u * QP_WARPS;
           if (r >= rz) break;
           // lane 0's sum for every lane (the xor tree's lanes may differ in the last bit)
-          const double x = __shfl_sync(0xffffffffu, ap[u] - warp_sum(lane < kk ? vq[u] * s_fp[lane] : 0.0), 0);
+          const double x = __shfl_sync(0xffffffffu, ap[u] - warp_sum(vq[u] * fpl), 0);
           if (r > i) {
             if (lane == 0) ss = fma(x, x, ss);
             ax = fma(vq[u], x, ax);
@@ -210,6 +223,11 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
       }
     }
     QP_MARK(2);
+    if (a.trace && tid == 0 && kk == 1) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      a.trace[64 + 160 + c] = t_;
+    }
     target += G;
     qp_grid_sync(a.bar, target);
     QP_MARK(3);
@@ -225,30 +243,56 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     for (int q = 0; q < QRCP_NB; ++q) fr[q] = own && q < kk ? ldcg(a.F + q * ldf + js) : 0.0;
     const double bij_old = own ? ldcg(B + static_cast<int64_t>(i) * ldb + jt) : 0.0;
     double n1 = own ? ldcg(a.vn1 + js) : 0.0, n2 = own ? ldcg(a.vn2 + js) : 1.0;
+    // the reflector's inputs, also independent of the reductions
+    double alpha = 0.0, vi = 0.0;
+    if (tid < 32) {
+      alpha = ldcg(a.alpha);
+      if (tid < kk) vi = ldcg(B + static_cast<int64_t>(i) * ldb + i0 + tid);  // V(i, q)
+    }
     // reflector and aux, every CTA in the same order: warp w sums the partials of CTAs
-    // [w*cpw, (w+1)*cpw) (lane q: aux partial q; lane 0 also the sum of squares), then 33 threads
-    // sum the warps in order
+    // [w*cpw, (w+1)*cpw) (lane q: aux partial q; lane 0 also the sum of squares; all loads issued
+    // together), then 33 threads sum the warps in order
     {
       const int cpw = (G + QP_WARPS - 1) / QP_WARPS, ca = warp * cpw, cz = min(G, ca + cpw);
-      double t = 0.0, s2 = 0.0;
-#pragma unroll 4
-      for (int cc = ca; cc < cz; ++cc) {
-        if (lane < kk) t += ldcg(a.auxp + cc * 32 + lane);
-        if (lane == 0) s2 += ldcg(a.ssp + cc);
+      double pa_[QP_CPW];
+#pragma unroll
+      for (int u = 0; u < QP_CPW; ++u) {
+        const int cc = ca + u;
+        pa_[u] = cc < cz && lane < kk ? ldcg(a.auxp + cc * 32 + lane) : 0.0;
       }
+      const double ps_ = ca + lane < cz ? ldcg(a.ssp + ca + lane) : 0.0;  // lane u: CTA ca + u
+      // x (unscaled; 0 in row i, whose v entry is 1: w_j = A(i, j) + scale sum_{r>i} x_r A(r, j))
+      {
+        double xv[8];  // eight loads in flight per thread before the shared-memory stores
+        int r = i + tid;
+        for (; r + 7 * QP_THREADS < l; r += 8 * QP_THREADS) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) xv[u] = ldcg(a.xbuf + r + u * QP_THREADS - i);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) xs[r + u * QP_THREADS - i] = r + u * QP_THREADS == i ? 0.0 : xv[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = r + u * QP_THREADS < l ? ldcg(a.xbuf + r + u * QP_THREADS - i) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (r + u * QP_THREADS < l) xs[r + u * QP_THREADS - i] = r + u * QP_THREADS == i ? 0.0 : xv[u];
+      }
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < QP_CPW; ++u) t += pa_[u];
+      const double s2 = __shfl_sync(0xffffffffu, warp_sum(ps_), 0);
       s_red[warp][lane] = t;
       if (lane == 0) s_red[warp][32] = s2;
       __syncthreads();
       if (tid < 33) {
-        double u = 0.0;
-        for (int w = 0; w < QP_WARPS; ++w) u += s_red[w][tid];
-        s_tot[tid] = u;
+        double u2 = 0.0;
+        for (int w = 0; w < QP_WARPS; ++w) u2 += s_red[w][tid];
+        s_tot[tid] = u2;
       }
       __syncthreads();
     }
     if (tid < 32) {
       const double t = s_tot[32], aq = s_tot[tid];
-      const double alpha = ldcg(a.alpha);
       double beta, tv, scale;
       if (t == 0.0) {
         tv = 0.0;
@@ -261,7 +305,6 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
         scale = 1.0 / (alpha - beta);
       }
       if (tid < kk) {
-        const double vi = ldcg(B + static_cast<int64_t>(i) * ldb + i0 + tid);  // V(i, q)
         s_ai[tid] = vi;
         s_aux[tid] = -tv * (vi + scale * aq);
       }
@@ -283,15 +326,13 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
         rowsum = fma(s_ai[q], fr[q], rowsum);
         if (own && js != jt) a.F[q * ldf + jt] = fr[q];  // F's row follows the swap
       }
-    for (int r = i + tid; r < l; r += QP_THREADS) xs[r - i] = r == i ? 1.0 : ldcg(a.xbuf + r - i) * scale;
-    __syncthreads();
     QP_MARK(5);
     // v into column i (phase A's row partition), beta on the diagonal
     {
       const int rows = l - i, rc = (rows + G - 1) / G;
       const int ra = i + c * rc, rz = min(l, ra + rc);
       for (int r = ra + tid; r < rz; r += QP_THREADS)
-        B[static_cast<int64_t>(r) * ldb + i] = r == i ? beta : xs[r - i];
+        B[static_cast<int64_t>(r) * ldb + i] = r == i ? beta : xs[r - i] * scale;
     }
     // w over the owned columns j > i: warps over (32-column chunk, row split)
     const int nch = jn > 0 ? (jn + 31) / 32 : 0;
@@ -329,6 +370,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     if (own) {
       double w = 0.0;
       for (int sp = 0; sp < S; ++sp) w += wp[sp * (nch * 32) + tid];
+      w = fma(scale, w, bij_old);
       const double f = fma(tv, w, f0);
       a.F[kk * ldf + jt] = f;
       const double rij = bij_old - rowsum - f;
@@ -363,7 +405,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
         double f2[QRCP_NB];
 #pragma unroll
         for (int q = 0; q < QRCP_NB; ++q) f2[q] = act && q < kk ? ldcg(a.F + q * ldf + col) : 0.0;
-        const double fk = act ? ldcg(a.F + kk * ldf + col) : 0.0;
+        const double fk = act ? ldcg(a.F + kk * ldf + col) * scale : 0.0;  // v_r = scale x_r
         double sa = 0.0, sb = 0.0;
         int r = ra;
         for (; r + 1 < rz; r += 2) {  // two rows in flight
@@ -443,6 +485,11 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
       a.pidx[c] = bi;
     }
     QP_MARK(9);
+    if (a.trace && tid == 0 && kk == 1) {  // every CTA's arrival time at the second barrier of step 1
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      a.trace[64 + c] = t_;
+    }
     target += G;
     qp_grid_sync(a.bar, target);
     QP_MARK(10);
