@@ -1800,18 +1800,18 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
     // and every CTA owns at most QP_THREADS columns
     static const int no_persist = debug_env("QB_QRCP_NO_PERSIST");
     const int G = ctx->num_sms;
-    const size_t qp_smem = sizeof(double) * (size_t)std::max<int64_t>(l + 2 * QP_THREADS, 33 * G);
-    bool persist = !no_persist && l <= QP_MAX_L && (n + G - 1) / G <= QP_THREADS && G <= QP_WARPS * QP_CPW;
+    const int qp_cwp = (int)(((n + G - 1) / G + 1) | 1);  // odd stride: conflict-free F columns
+    const size_t qp_smem = sizeof(double) * (size_t)(l + 2 * QP_THREADS + QRCP_NB * qp_cwp);
+    bool persist = !no_persist && (n + G - 1) / G <= QP_THREADS && G <= QP_WARPS * QP_CPW && qp_smem <= QP_MAX_SMEM;
     if (persist) {
-      QB_SMEM_ATTR(qrcp_panel_kernel, (int)(sizeof(double) * (QP_MAX_L + 2 * QP_THREADS)));  // the largest launch
-      if (33 * G > QP_MAX_L + 2 * QP_THREADS) persist = false;
+      QB_SMEM_ATTR(qrcp_panel_kernel, (int)QP_MAX_SMEM);  // the largest launch
       int per_sm = 0;
       QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_panel_kernel, QP_THREADS, qp_smem));
       persist = per_sm >= 1;
     }
     QrcpPanelArgs pa{};
     if (persist) {
-      QB_TRY(ensure(ctx, ctx->qw2, sizeof(double) * (size_t)(l + 64 + 38 * G + 512)));
+      QB_TRY(ensure(ctx, ctx->qw2, sizeof(double) * (size_t)(QP_REP * (l + 8 + 35 * G) + 512)));
       double* pw = ctx->qw2.d();
       pa.B = R;
       pa.ldb = ldr;
@@ -1824,13 +1824,14 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
       pa.F = F;
       pa.ldf = ldf;
       pa.xbuf = pw;
-      pa.alpha = pw + l;
-      pa.bar = reinterpret_cast<unsigned*>(pw + l + 8);
-      pa.ssp = pw + l + 64;
-      pa.auxp = pa.ssp + G;
-      pa.pmax = pa.auxp + 32 * G;
-      pa.pidx = reinterpret_cast<int*>(pa.pmax + G);
+      pa.alpha = pa.xbuf + QP_REP * l;
+      pa.ssp = pa.alpha + QP_REP;
+      pa.auxp = pa.ssp + QP_REP * G;
+      pa.pmax = pa.auxp + QP_REP * 32 * G;
+      pa.pidx = reinterpret_cast<int*>(pa.pmax + QP_REP * G);
+      pa.bar = reinterpret_cast<unsigned*>(pa.pmax + 2 * QP_REP * G);
       pa.tol3z = tol3z;
+      pa.cwp = qp_cwp;
     }
     for (int i0 = 0; i0 < kmin; i0 += QRCP_NB) {
       const int nb = std::min(QRCP_NB, kmin - i0);
@@ -1852,7 +1853,7 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
         lc.numAttrs = 1;
         static const int ptr = debug_env("QB_QRCP_PTRACE");  // diagnostics: phase marks of panels 0 and mid
         const bool trace_this = ptr && (i0 == 0 || i0 == (kmin / 2 / QRCP_NB) * QRCP_NB || i0 + QRCP_NB >= kmin);
-        pa.trace = trace_this ? reinterpret_cast<unsigned long long*>(pa.pidx + 2 * G) : nullptr;
+        pa.trace = trace_this ? reinterpret_cast<unsigned long long*>(pa.pmax + 2 * QP_REP * G + 8) : nullptr;
         QB_CUDA(cudaLaunchKernelEx(&lc, qrcp_panel_kernel, pa));
         QB_TRY(check_launch(ctx, "qrcp_panel"));
         if (trace_this) {
@@ -1876,7 +1877,8 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
             std::fprintf(stderr, "qrcp panel %d step %d:", i0, s2);
             for (int k2 = 1; k2 <= 10; ++k2)
               std::fprintf(stderr, " %.2f", (double)(tr[s2 * 16 + k2] - tr[s2 * 16 + k2 - 1]) * 1e-3);
-            std::fprintf(stderr, " us\n");
+            std::fprintf(stderr, " | after barrier: loads %.2f sum %.2f us\n", (double)(tr[s2 * 16 + 11] - tr[s2 * 16 + 3]) * 1e-3,
+                         (double)(tr[s2 * 16 + 12] - tr[s2 * 16 + 11]) * 1e-3);
           }
         }
       }

@@ -28,7 +28,8 @@ namespace qbk {
 
 constexpr int QP_THREADS = 512;
 constexpr int QP_WARPS = QP_THREADS / 32;
-constexpr int QP_MAX_L = 12288;  // v staged in shared memory (96 KB)
+constexpr int QP_MAX_SMEM = 200 * 1024;  // dynamic shared memory: v (l), w partials, F block
+constexpr int QP_REP = 8;        // replicas of the data every CTA reads (spreads the L2 hot lines)
 constexpr int QP_CPW = 16;       // CTAs per warp in the partial sums: gridDim.x <= QP_WARPS * QP_CPW
 
 struct QrcpPanelArgs {
@@ -41,14 +42,16 @@ struct QrcpPanelArgs {
   double* tau;
   double* F;
   int64_t ldf;
-  double* xbuf;   // l: x of the current step
-  double* ssp;    // G: per-CTA sum of squares
-  double* auxp;   // G x 32: per-CTA V^T x partials
-  double* alpha;  // 1: x_i
-  double* pmax;   // G
-  int* pidx;      // G
+  // exchanged between the CTAs, each in QP_REP replicas
+  double* xbuf;   // QP_REP x l: x of the current step
+  double* ssp;    // QP_REP x G: per-CTA sum of squares
+  double* auxp;   // QP_REP x G x 32: per-CTA V^T x partials
+  double* alpha;  // QP_REP: x_i
+  double* pmax;   // QP_REP x G
+  int* pidx;      // QP_REP x G
   unsigned* bar;  // grid barrier counter (zeroed before the launch)
   double tol3z;
+  int cwp;        // row stride of the shared-memory F block (>= the columns a CTA owns)
   int first;      // step i0 == 0: pick the first pivot from vn1 itself
   unsigned long long* trace;  // diagnostics (QB_QRCP_PTRACE): %globaltimer marks of CTA 0, steps 0-3
 };
@@ -77,7 +80,7 @@ __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
 __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPanelArgs a) {
   extern __shared__ __align__(16) double qp_sm[];
-  double* xs = qp_sm;  // v (rows >= i), l - i entries
+  double* xs = qp_sm;  // x / v (rows >= i), l - i entries, then the w partials
   __shared__ double s_red[QP_WARPS][33];
   __shared__ double s_aux[QRCP_NB], s_ai[QRCP_NB];
   __shared__ double s_scal[4];  // beta, tau, scale
@@ -96,6 +99,13 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
   const int ncols = n - i0, cw = (ncols + G - 1) / G;
   const int cj0 = i0 + c * cw, cj1 = min(n, cj0 + cw);
   unsigned target = 0;
+  // thread tid owns column cj0 + tid for the whole panel: its norms in registers, its F row in
+  // shared memory (F also goes to global memory for the trailing GEMM and the pivot swaps)
+  const int jt = cj0 + tid;
+  double n1r = jt < cj1 ? ldcg(a.vn1 + jt) : 0.0, n2r = jt < cj1 ? ldcg(a.vn2 + jt) : 1.0;
+  double* sF = qp_sm + a.l + 2 * QP_THREADS;  // [QRCP_NB][cwp]
+  const int cwp = a.cwp;
+  const int rep = c % QP_REP;  // the replica of the exchanged data this CTA reads
 
   for (int kk = 0; kk < a.nb; ++kk) {
     const int i = i0 + kk;
@@ -113,6 +123,7 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
       vq0[u] = r < rzA && lane < kk ? ldcg(ar + i0 + lane) : 0.0;
       aiv0[u] = r < rzA ? ldcg(ar + i) : 0.0;
     }
+    int pv_;
     {
       double best = -1.0;
       int bi = n;
@@ -126,8 +137,8 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
         }
       } else {
         for (int q = tid; q < G; q += QP_THREADS) {
-          const double v = ldcg(a.pmax + q);
-          const int x = __ldcg(a.pidx + q);
+          const double v = ldcg(a.pmax + rep * G + q);
+          const int x = __ldcg(a.pidx + rep * G + q);
           if (v > best || (v == best && x < bi)) {
             best = v;
             bi = x;
@@ -159,10 +170,16 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
         s_p = x;
       }
       __syncthreads();
+      pv_ = s_p;
     }
-    const int p = s_p;
+    const int p = pv_;
     QP_MARK(1);
     const double fpl = lane < kk ? ldcg(a.F + lane * ldf + p) : 0.0;  // F(i, lane) after the swap
+    // rows < i (finished rows of R): columns i and p to be swapped, at most one row per thread
+    const int rc2 = (i + G - 1) / G, rsw = c * rc2 + tid;
+    const bool swp = p != i && rsw < min(i, (c + 1) * rc2);
+    const double sw_i = swp ? ldcg(B + static_cast<int64_t>(rsw) * ldb + i) : 0.0;
+    const double sw_p = swp ? ldcg(B + static_cast<int64_t>(rsw) * ldb + p) : 0.0;
     {
       const int rows = l - i, rc = (rows + G - 1) / G;
       const int ra = i + c * rc, rz = min(l, ra + rc);
@@ -188,23 +205,20 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
             if (lane == 0) ss = fma(x, x, ss);
             ax = fma(vq[u], x, ax);
           } else if (lane == 0) {
-            a.alpha[0] = x;
+            for (int e = 0; e < QP_REP; ++e) a.alpha[e] = x;
           }
+          if (lane < QP_REP) a.xbuf[lane * l + r - i] = x;
           if (lane == 0) {
-            a.xbuf[r - i] = x;
             if (p != i) B[static_cast<int64_t>(r) * ldb + p] = aiv[u];
           }
         }
       }
       // rows < i (finished rows of R): columns i and p swapped
+      if (swp) {
+        B[static_cast<int64_t>(rsw) * ldb + i] = sw_p;
+        B[static_cast<int64_t>(rsw) * ldb + p] = sw_i;
+      }
       if (p != i) {
-        const int rc2 = (i + G - 1) / G;
-        for (int r = c * rc2 + tid; r < min(i, (c + 1) * rc2); r += QP_THREADS) {
-          double* ar = B + static_cast<int64_t>(r) * ldb;
-          const double t0 = ldcg(ar + i), t1 = ldcg(ar + p);
-          ar[i] = t1;
-          ar[p] = t0;
-        }
         if (c == 0 && tid == 0) {
           const int t = a.perm[i];
           a.perm[i] = a.perm[p];
@@ -218,8 +232,10 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
       if (tid < 33) {
         double t = 0.0;
         for (int w = 0; w < QP_WARPS; ++w) t += s_red[w][tid];
-        if (tid < 32) a.auxp[c * 32 + tid] = t;
-        else a.ssp[c] = t;
+        for (int e = 0; e < QP_REP; ++e) {
+          if (tid < 32) a.auxp[(e * G + c) * 32 + tid] = t;
+          else a.ssp[e * G + c] = t;
+        }
       }
     }
     QP_MARK(2);
@@ -236,17 +252,17 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     // this thread's column (independent of the reflector): F's row, A(i, j) and the norms, read
     // through the swap, issued before the reductions so that their latency overlaps them
     const int ja = max(cj0, i + 1), jn = cj1 - ja;
-    const bool own = tid < jn;
-    const int jt = ja + tid, js = own && jt == p ? i : jt;
-    double fr[QRCP_NB];
-#pragma unroll
-    for (int q = 0; q < QRCP_NB; ++q) fr[q] = own && q < kk ? ldcg(a.F + q * ldf + js) : 0.0;
+    const bool own = jt < cj1 && jt > i;
     const double bij_old = own ? ldcg(B + static_cast<int64_t>(i) * ldb + jt) : 0.0;
-    double n1 = own ? ldcg(a.vn1 + js) : 0.0, n2 = own ? ldcg(a.vn2 + js) : 1.0;
+    if (own && jt == p) {  // the pivot swap: column p takes column i's F row and norms
+      n1r = ldcg(a.vn1 + i);
+      n2r = ldcg(a.vn2 + i);
+      for (int q = 0; q < kk; ++q) sF[q * cwp + tid] = ldcg(a.F + q * ldf + i);
+    }
     // the reflector's inputs, also independent of the reductions
     double alpha = 0.0, vi = 0.0;
     if (tid < 32) {
-      alpha = ldcg(a.alpha);
+      alpha = ldcg(a.alpha + rep);
       if (tid < kk) vi = ldcg(B + static_cast<int64_t>(i) * ldb + i0 + tid);  // V(i, q)
     }
     // reflector and aux, every CTA in the same order: warp w sums the partials of CTAs
@@ -258,21 +274,21 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
 #pragma unroll
       for (int u = 0; u < QP_CPW; ++u) {
         const int cc = ca + u;
-        pa_[u] = cc < cz && lane < kk ? ldcg(a.auxp + cc * 32 + lane) : 0.0;
+        pa_[u] = cc < cz && lane < kk ? ldcg(a.auxp + (rep * G + cc) * 32 + lane) : 0.0;
       }
-      const double ps_ = ca + lane < cz ? ldcg(a.ssp + ca + lane) : 0.0;  // lane u: CTA ca + u
+      const double ps_ = ca + lane < cz ? ldcg(a.ssp + rep * G + ca + lane) : 0.0;  // lane u: CTA ca + u
       // x (unscaled; 0 in row i, whose v entry is 1: w_j = A(i, j) + scale sum_{r>i} x_r A(r, j))
       {
         double xv[8];  // eight loads in flight per thread before the shared-memory stores
         int r = i + tid;
         for (; r + 7 * QP_THREADS < l; r += 8 * QP_THREADS) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) xv[u] = ldcg(a.xbuf + r + u * QP_THREADS - i);
+          for (int u = 0; u < 8; ++u) xv[u] = ldcg(a.xbuf + rep * l + r + u * QP_THREADS - i);
 #pragma unroll
           for (int u = 0; u < 8; ++u) xs[r + u * QP_THREADS - i] = r + u * QP_THREADS == i ? 0.0 : xv[u];
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = r + u * QP_THREADS < l ? ldcg(a.xbuf + r + u * QP_THREADS - i) : 0.0;
+        for (int u = 0; u < 8; ++u) xv[u] = r + u * QP_THREADS < l ? ldcg(a.xbuf + rep * l + r + u * QP_THREADS - i) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (r + u * QP_THREADS < l) xs[r + u * QP_THREADS - i] = r + u * QP_THREADS == i ? 0.0 : xv[u];
@@ -284,12 +300,14 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
       s_red[warp][lane] = t;
       if (lane == 0) s_red[warp][32] = s2;
       __syncthreads();
+      QP_MARK(11);
       if (tid < 33) {
         double u2 = 0.0;
         for (int w = 0; w < QP_WARPS; ++w) u2 += s_red[w][tid];
         s_tot[tid] = u2;
       }
       __syncthreads();
+      QP_MARK(12);
     }
     if (tid < 32) {
       const double t = s_tot[32], aq = s_tot[tid];
@@ -318,14 +336,6 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     __syncthreads();
     QP_MARK(4);
     const double beta = s_scal[0], tv = s_scal[1], scale = s_scal[2];
-    double f0 = 0.0, rowsum = 0.0;  // F(j, 0:kk) aux and A(i, i0:i) F(j, 0:kk)^T
-#pragma unroll
-    for (int q = 0; q < QRCP_NB; ++q)
-      if (q < kk) {
-        f0 = fma(fr[q], s_aux[q], f0);
-        rowsum = fma(s_ai[q], fr[q], rowsum);
-        if (own && js != jt) a.F[q * ldf + jt] = fr[q];  // F's row follows the swap
-      }
     QP_MARK(5);
     // v into column i (phase A's row partition), beta on the diagonal
     {
@@ -368,19 +378,27 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     // host): w, F, the row update, the norm downdate
     bool recompute = false;
     if (own) {
+      double f0 = 0.0, rowsum = 0.0;  // F(j, 0:kk) aux and A(i, i0:i) F(j, 0:kk)^T
+      for (int q = 0; q < kk; ++q) {
+        const double fq = sF[q * cwp + tid];
+        f0 = fma(fq, s_aux[q], f0);
+        rowsum = fma(s_ai[q], fq, rowsum);
+        if (jt == p) a.F[q * ldf + jt] = fq;  // F's row follows the swap
+      }
       double w = 0.0;
-      for (int sp = 0; sp < S; ++sp) w += wp[sp * (nch * 32) + tid];
+      for (int sp = 0; sp < S; ++sp) w += wp[sp * (nch * 32) + (jt - ja)];
       w = fma(scale, w, bij_old);
       const double f = fma(tv, w, f0);
+      sF[kk * cwp + tid] = f;
       a.F[kk * ldf + jt] = f;
       const double rij = bij_old - rowsum - f;
       B[static_cast<int64_t>(i) * ldb + jt] = rij;
-      if (n1 != 0.0) {
-        double temp = fabs(rij) / n1;
+      if (n1r != 0.0) {
+        double temp = fabs(rij) / n1r;
         temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
-        const double ratio = n1 / n2;
+        const double ratio = n1r / n2r;
         if (temp * ratio * ratio <= a.tol3z) recompute = true;
-        else n1 = n1 * sqrt(temp);
+        else n1r = n1r * sqrt(temp);
       }
     }
     QP_MARK(7);
@@ -401,11 +419,11 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
       for (int g = 0; g < total; g += 32) {
         const bool act = g + lane < total;
         const int tl = act ? s_list[g + lane] : 0;
-        const int col = act ? ja + tl : i;
+        const int col = act ? cj0 + tl : i;
         double f2[QRCP_NB];
 #pragma unroll
-        for (int q = 0; q < QRCP_NB; ++q) f2[q] = act && q < kk ? ldcg(a.F + q * ldf + col) : 0.0;
-        const double fk = act ? ldcg(a.F + kk * ldf + col) * scale : 0.0;  // v_r = scale x_r
+        for (int q = 0; q < QRCP_NB; ++q) f2[q] = act && q < kk ? sF[q * cwp + tl] : 0.0;
+        const double fk = act ? sF[kk * cwp + tl] * scale : 0.0;  // v_r = scale x_r
         double sa = 0.0, sb = 0.0;
         int r = ra;
         for (; r + 1 < rz; r += 2) {  // two rows in flight
@@ -453,12 +471,12 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
     int bi = n;
     if (own) {
       if (recompute) {
-        n1 = s_res[tid];
-        n2 = n1;
+        n1r = s_res[tid];
+        n2r = n1r;
       }
-      a.vn1[jt] = n1;
-      a.vn2[jt] = n2;
-      best = n1;
+      a.vn1[jt] = n1r;
+      a.vn2[jt] = n2r;
+      best = n1r;
       bi = jt;
     }
 #pragma unroll
@@ -481,8 +499,10 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
           best = s_bv[w];
           bi = s_bi[w];
         }
-      a.pmax[c] = best;
-      a.pidx[c] = bi;
+      for (int e = 0; e < QP_REP; ++e) {
+        a.pmax[e * G + c] = best;
+        a.pidx[e * G + c] = bi;
+      }
     }
     QP_MARK(9);
     if (a.trace && tid == 0 && kk == 1) {  // every CTA's arrival time at the second barrier of step 1
