@@ -68,3 +68,18 @@ def test_pivoted_qr_without_factorization(qbmod):
     with pytest.raises(qbmod.QBError):
         c.pivoted_qr()
     c.close()
+
+
+@pytest.mark.parametrize("env", ["QB_QRCP_NO_PERSIST", "QB_QRCP_LOOKAHEAD", "QB_QRCP_UNFUSED", "QB_QRCP_Q_UNBLOCKED"])
+def test_pivoted_qr_other_schedules(qbmod, env):
+    """The schedules the default one falls back to (multi-kernel blocked: too many columns per SM
+    or too little shared memory) and the reference ones, each against the oracle in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""), **{env: "1"})
+    for case in (["1500", "900", "poly2", "1e-4", "64"], ["800", "2000", "exp_100", "1e-3", "100"]):
+        p = subprocess.run([sys.executable, os.path.join(root, "tests", "qrcp_variant_check.py"), *case], env=e,
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stdout + p.stderr
