@@ -146,3 +146,33 @@ def test_c5_against_stored_oracle_values(qbmod):
     orth = (Q.T @ Q - torch.eye(k, dtype=torch.float64, device=Q.device)).abs().max().item()
     assert orth <= 1e-12
     ctx.close()
+
+
+def test_pivoted_qr_T_full_size_properties(qbmod):
+    """qb_pivoted_qr at T (the bench's post-processing workload, l = 2816, n = 20000): the oracle's
+    dlaqp2 loop is too slow at this size, so check what holds for any size:
+    perm is a permutation; the greedy pivot property |R(i,i)|^2 >= ||R(i:, j)||^2 for j > i (to the
+    norm-downdate accuracy, sqrt(u) relative: dlaqp2's tol3z); A P ~ Q^ R to the QB residual;
+    Q^ orthonormal."""
+    cfg = synth.CONFIGS["T"]
+    A = synth.make_matrix_torch(cfg.m, cfg.n, synth.config_sigma(cfg), cfg.seed_matrix, dtype=torch.float64)
+    c = qbmod.QB(0)
+    g = c.factor(A, cfg.eps, cfg.b, cfg.q, seed=cfg.seed_omega, copy_out=False)
+    k = g["k"]
+    r = c.pivoted_qr(copy_out=False)
+    perm = np.asarray(r["perm"])
+    assert np.array_equal(np.sort(perm), np.arange(cfg.n))
+    R, Qh = r["R"].double(), r["Qh"].double()
+    assert torch.count_nonzero(torch.tril(R[:, :k], -1)).item() == 0
+    # suffix sums over rows: S[i, j] = ||R(i:, j)||^2
+    S = torch.flip(torch.cumsum(torch.flip(R * R, [0]), 0), [0])
+    d2 = torch.diagonal(R[:, :k]) ** 2
+    jmask = torch.arange(cfg.n, device=R.device)[None, :] > torch.arange(k, device=R.device)[:, None]
+    trail = torch.where(jmask, S, torch.zeros_like(S)).max(dim=1).values
+    assert bool((d2 >= trail * (1.0 - 1e-6)).all())
+    orth = (Qh.T @ Qh - torch.eye(k, dtype=torch.float64, device=Qh.device)).abs().max().item()
+    assert orth <= 1e-12, orth
+    P = torch.as_tensor(perm, device=A.device, dtype=torch.long)
+    err = torch.linalg.norm(A[:, P] - Qh @ R).item()
+    assert err <= cfg.eps * (1 + 1e-6) + 1e-11 * torch.linalg.norm(A).item(), err
+    c.close()
