@@ -15,3 +15,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
     -k "regex:gemm_f64_kernelILi0ELi64ELi2E" -s 3 -c 1 -o gpurun_out/prof_down_$R \
     env PYTHONPATH=. python tools/quick_run.py T 1 > gpurun_out/ncu_down_$R.log 2>&1; echo down_rc=$?
+# qb_pivoted_qr at T: launch list (after an uninstrumented run) and one persistent panel launch under --set full
+PYTHONPATH=. timeout 300 python tools/qrcp_once.py T > gpurun_out/qrcp_plain_$R.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_qrcp_$R.csv \
+    env PYTHONPATH=. python tools/qrcp_once.py T > gpurun_out/ncu_launch_qrcp_$R.log 2>&1; echo qrcp_rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k "regex:qrcp_panel_kernel" -s 90 -c 1 -o gpurun_out/prof_qrcp_$R \
+    env PYTHONPATH=. python tools/qrcp_once.py T > gpurun_out/ncu_qrcp_$R.log 2>&1; echo qrcp_full_rc=$?
