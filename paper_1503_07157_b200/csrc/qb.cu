@@ -481,6 +481,12 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
                const int* gate = nullptr) {
   if (nparts) *nparts = 0;
   if (M <= 0 || N <= 0) return QB_OK;
+  // a short M wastes most of the 128-row tile (C2's B_i = Q_i^T A at w = 64: half of it): compute
+  // C^T = op(B)^T op(A)^T instead (the same operands, roles and store orientation swapped)
+  static const int no_swap = debug_env("QB_GEMM_NO_SWAP");
+  if (!no_swap && epi != EPI_SUB_COL && M < GEMM_BM && N >= 2 * GEMM_BM)
+    return gemm(ctx, layout, epi == EPI_STORE_COL ? EPI_STORE_ROW : EPI_STORE_COL, N, M, K, B, ldb, A, lda, C, ldc,
+                want_norm, nparts, allow_split, gate);
   GemmParams p{};
   p.M = M;
   p.N = N;

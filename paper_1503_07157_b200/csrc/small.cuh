@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
     const int64_t r = idx / cols, c = idx - r * cols;
     const double* src = P + r * ldp + c;
     double v = 0.0;
+#pragma unroll 8
     for (int s = 0; s < S; ++s) v += src[s * stride];
     if (subtract) v = out[r * ldo + c] - v;  // C -= sum of the split products
     out[r * ldo + c] = v;
@@ -847,3 +848,4 @@ __global__ void __launch_bounds__(SCQR_THREADS) small_cholqr_kernel(const double
 }
 
 }  // namespace qbk
+
