@@ -111,6 +111,7 @@ struct qb_ctx_s {
   int64_t col_offset = 0, n_global = 0;
   // row sharding (NEXT-2, tall-skinny A): this rank holds rows row_offset .. of an m_global-row A
   bool shard_rows = false;
+  bool tf_gram = false;  // FP32 factorization in progress: CholeskyQR Grams on 3xTF32 (reading R18d)
   int64_t row_offset = 0, m_global = 0;
   ncclComm_t comm = nullptr;  // set on NCCL-distributed contexts (any nranks >= 1)
   qb_loopback loop = nullptr; // set on loopback-distributed contexts (in-process ranks, one GPU)
@@ -848,27 +849,37 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
                       const int* gate, bool row_distributed, const float* src32 = nullptr, int64_t lds32 = 0,
                       float* dst32 = nullptr, int64_t ldd32 = 0) {
   const int64_t ldgb = round_up(kMaxB, 16);
-  QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr, true,
-              gate));
+  static const int orth64 = debug_env("QB_ORTH64");
+  static const int gram64_env = debug_env("QB_GRAM64");
+  const bool gram64 = gram64_env || !ctx->tf_gram;  // qb_orth and the small paths keep the FP64 Gram
+  const bool tf = ctx->dtype == QB_F32 && !orth64;
+  const float* X32 = src32;
+  int64_t ld_x = lds32;
+  if (tf && X32 == nullptr) {
+    const int64_t ldx = round_up(m, 16);
+    QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(ldx * w)));
+    QB_TRY(launch_convert(ctx, src, lds, m, w, static_cast<float*>(ctx->X32.p), ldx, gate));
+    X32 = static_cast<const float*>(ctx->X32.p);
+    ld_x = ldx;
+  }
+  if (tf && !gram64) {
+    // FP32 factorizations (reading R18d): the Gram of the FP32 copy on the 3xTF32 tensor cores,
+    // FP32 accumulation per 128-deep k chunk and FP64 across chunks and splits (relative error
+    // ~1e-6, which CholeskyQR2 absorbs at the FP32 tolerances; QB_GRAM64=1 keeps it FP64)
+    QB_TRY(gemm_tf(ctx, GEMM_TN, TF_STORE_COL, w, w, (int)m, X32, ld_x, X32, ld_x, ctx->G.d(), ldgb, false, nullptr,
+                   true, gate));
+  } else {
+    QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, w, w, (int)m, src, lds, src, lds, ctx->G.d(), ldgb, false, nullptr, true,
+                gate));
+  }
   if (row_distributed) QB_TRY(allreduce_sum(ctx, ctx->G.d(), (size_t)(ldgb * w)));  // G = sum_p src_p^T src_p
   // the shifted-CholeskyQR shift (reading R8) is sized for the GLOBAL row count of the panel:
   // the power step's Z on column shards has n_global rows, a row shard's Y / Q_i m_global
   const int64_t m_shift = !row_distributed ? m : (ctx->shard_rows ? ctx->m_global : ctx->n_global);
   QB_TRY(chol_inv(ctx, w, m_shift, true, gate));
-  static const int orth64 = debug_env("QB_ORTH64");
-  if (ctx->dtype == QB_F32 && !orth64) {
-    // FP32 contexts (reading R18c): X T on the 3xTF32 tensor cores from FP32 copies of X and T;
-    // the Gram stays FP64
-    const int64_t ldx = round_up(m, 16);
+  if (tf) {
+    // FP32 contexts (reading R18c): X T on the 3xTF32 tensor cores from FP32 copies of X and T
     QB_TRY(ensure(ctx, ctx->T32, sizeof(float) * (size_t)(ldgb * ldgb)));
-    const float* X32 = src32;
-    int64_t ld_x = lds32;
-    if (X32 == nullptr) {
-      QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(ldx * w)));
-      QB_TRY(launch_convert(ctx, src, lds, m, w, static_cast<float*>(ctx->X32.p), ldx, gate));
-      X32 = static_cast<const float*>(ctx->X32.p);
-      ld_x = ldx;
-    }
     float* T32 = static_cast<float*>(ctx->T32.p);
     QB_TRY(launch_convert(ctx, static_cast<const double*>(ctx->Rinv.d()), ldgb, w, w, T32, ldgb, gate));
     return gemm_tf(ctx, GEMM_NN, TF_STORE_COL, (int)m, w, w, X32, ld_x, T32, ldgb, dst, ldd, false, nullptr, true, gate,
@@ -2213,6 +2224,11 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
   if (!k_out) return fail(ctx, QB_ERR_INVALID_ARG, "k must not be NULL");
   *k_out = 0;
   const bool is_f32 = ctx->dtype == QB_F32;
+  struct TfGram {  // set for the duration of this factorization
+    qb_ctx c;
+    explicit TfGram(qb_ctx c_, bool on) : c(c_) { c->tf_gram = on; }
+    ~TfGram() { c->tf_gram = false; }
+  } tf_gram_scope(ctx, is_f32);
   // empty A (m = 0 or n = 0, single-rank contexts): ||A||_F = 0 <= eps, so k = 0 (reading R3,
   // Algorithm 1 line (2)); A may be NULL.  Arguments b, q, eps are still validated.
   if (m >= 0 && n >= 0 && (m == 0 || n == 0) && ctx->nranks <= 1 && lda >= std::max<int64_t>(m, 1)) {
