@@ -570,7 +570,8 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   p.split_stride = stride;
   QB_TRY(dispatch_gemm<64>(ctx, layout, epi, ta, tb, tc, p, splits));
   const int64_t total = rows * cols;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
+  const int rsub = splitk_sub(total, splits, ctx->num_sms);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total * rsub + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
   double* sq = nullptr;
   if (want_norm) {
     QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
@@ -578,7 +579,7 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
     if (nparts) *nparts = grid;
   }
   splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp, C, ldc, sq,
-                                                               gate, subtract ? 1 : 0);
+                                                               gate, subtract ? 1 : 0, nullptr, 0, rsub);
   return check_launch(ctx, "splitk_reduce");
 }
 
@@ -783,7 +784,8 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   p.split_stride = stride;
   QB_TRY(run(epi, splits));
   const int64_t total = rows * cols;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
+  const int rsub = splitk_sub(total, splits, ctx->num_sms);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total * rsub + RED_THREADS - 1) / RED_THREADS, 8 * ctx->num_sms));
   double* sq = nullptr;
   if (want_norm) {
     QB_TRY(ensure(ctx, ctx->parts, sizeof(double) * (size_t)grid));
@@ -792,7 +794,7 @@ qb_status gemm_tf(qb_ctx ctx, int layout, int epi, int M, int N, int K, const fl
   }
   splitk_reduce_kernel<<<grid, RED_THREADS, 0, ctx->stream>>>(ctx->P.d(), splits, stride, rows, cols, ldp,
                                                                static_cast<double*>(C), ldc, sq, gate, 0, C32,
-                                                               ldc32);
+                                                               ldc32, rsub);
   return check_launch(ctx, "splitk_reduce");
 }
 

@@ -57,29 +57,46 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_kernel(const double* __res
 
 // out[r*ldo + c] = sum_{s<S} P[s*stride + r*ldp + c] for r < rows, c < cols (any layout
 // where "r" is the strided index), or out -= that sum when `subtract`.  Optional per-block
-// sum of squares of the result.
+// sum of squares of the result.  `sub` (1, 2, 4 or 8) consecutive lanes share an output when there
+// are few outputs and many splits: lane j of the group sums splits [j S/sub, (j+1) S/sub) in order
+// and the group adds its partial sums in lane order — a fixed order either way.
 __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double* __restrict__ P, int S, int64_t stride,
                                                                     int64_t rows, int64_t cols, int64_t ldp,
                                                                     double* __restrict__ out, int64_t ldo,
                                                                     double* __restrict__ sq_partials,
                                                                     const int* __restrict__ gate, int subtract,
                                                                     float* __restrict__ out32 = nullptr,
-                                                                    int64_t ld32 = 0) {
+                                                                    int64_t ld32 = 0, int sub = 1) {
   if (gate != nullptr && __ldcg(gate) == 0) return;
   __shared__ double red[RED_THREADS / 32];
   double sq = 0.0;
-  const int64_t total = rows * cols;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(RED_THREADS) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * RED_THREADS) {
+  const int64_t total = rows * cols, nthr = total * sub;
+  const int lane = threadIdx.x & 31, part = lane % sub;
+  const int s_lo = static_cast<int>((static_cast<int64_t>(S) * part) / sub);
+  const int s_hi = static_cast<int>((static_cast<int64_t>(S) * (part + 1)) / sub);
+  // warp-uniform trip count (the group sums shuffle)
+  for (int64_t base = (blockIdx.x * static_cast<int64_t>(RED_THREADS) + threadIdx.x) - lane; base < nthr;
+       base += static_cast<int64_t>(gridDim.x) * RED_THREADS) {
+    const int64_t g = base + lane;
+    const bool live = g < nthr;
+    const int64_t idx = live ? g / sub : 0;
     const int64_t r = idx / cols, c = idx - r * cols;
     const double* src = P + r * ldp + c;
     double v = 0.0;
+    if (live) {
 #pragma unroll 8
-    for (int s = 0; s < S; ++s) v += src[s * stride];
-    if (subtract) v = out[r * ldo + c] - v;  // C -= sum of the split products
-    out[r * ldo + c] = v;
-    if (out32 != nullptr) out32[r * ld32 + c] = static_cast<float>(v);  // FP32 contexts: RN_32 copy
-    sq = fma(v, v, sq);
+      for (int s2 = s_lo; s2 < s_hi; ++s2) v += src[s2 * stride];
+    }
+    for (int k = 1; k < sub; ++k) {
+      const double o = __shfl_down_sync(0xffffffffu, v, k);
+      if (part == 0) v += o;  // ((p0 + p1) + p2) + ...
+    }
+    if (live && part == 0) {
+      if (subtract) v = out[r * ldo + c] - v;  // C -= sum of the split products
+      out[r * ldo + c] = v;
+      if (out32 != nullptr) out32[r * ld32 + c] = static_cast<float>(v);  // FP32 contexts: RN_32 copy
+      sq = fma(v, v, sq);
+    }
   }
   if (sq_partials != nullptr) {
     sq = warp_sum(sq);
@@ -91,6 +108,14 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(const double
       sq_partials[blockIdx.x] = t;
     }
   }
+}
+
+// Lanes per output for splitk_reduce_kernel: more when the outputs alone leave most of the GPU idle
+// and each lane would still sum at least 8 splits.
+inline int splitk_sub(int64_t total, int S, int num_sms) {
+  int sub = 1;
+  while (sub < 8 && total * sub * 2 <= static_cast<int64_t>(4) * num_sms * RED_THREADS && S / (sub * 2) >= 8) sub *= 2;
+  return sub;
 }
 
 // Loopback collective: out = sum_r in[r] in rank order, one kernel over the data
