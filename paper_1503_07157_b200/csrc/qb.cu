@@ -847,6 +847,19 @@ qb_status chol_inv(qb_ctx ctx, int w, int64_t m_rows, bool ns, const int* gate) 
 // One CholeskyQR pass: dst = src T, with T from chol_inv (all on the device; gated).
 // FP32 contexts: src32 (optional) is RN_32(src) already in memory (ld lds32), else src is
 // converted into ctx->X32; dst32 (optional) receives RN_32(dst) (ld ldd32); src32 != dst32.
+// CholeskyQR2 of a panel small enough for one CTA's shared memory (small_cholqr_kernel, FP64 source)
+bool small_orth(int64_t m, int w, bool row_distributed) {
+  static const int no_small = debug_env("QB_NO_SMALL_ORTH");
+  return !row_distributed && !no_small && w <= SCQR_MAX_W && m * w <= SCQR_MAX_ELEMS;
+}
+
+// FP32 factorizations (reading R18d): CholeskyQR reads only the FP32 copy of its source
+bool tf_gram_on(qb_ctx ctx) {
+  static const int gram64_env = debug_env("QB_GRAM64");
+  static const int orth64 = debug_env("QB_ORTH64");
+  return ctx->dtype == QB_F32 && ctx->tf_gram && !gram64_env && !orth64;
+}
+
 qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
                       const int* gate, bool row_distributed, const float* src32 = nullptr, int64_t lds32 = 0,
                       float* dst32 = nullptr, int64_t ldd32 = 0) {
@@ -913,8 +926,7 @@ qb_status cholqr_pass(qb_ctx ctx, const double* src, int64_t lds, double* dst, i
 qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t m, int w,
                   bool row_distributed = false, bool single = false, const float* src32 = nullptr,
                   int64_t lds32 = 0, float* dst32 = nullptr, int64_t ldd32 = 0) {
-  static const int no_small = debug_env("QB_NO_SMALL_ORTH");
-  if (!row_distributed && !no_small && w <= SCQR_MAX_W && m * w <= SCQR_MAX_ELEMS) {
+  if (small_orth(m, w, row_distributed)) {
     // the whole CholeskyQR2 (all passes, fallback included) in one CTA for a small panel
     QB_SMEM_ATTR(small_cholqr_kernel, SCQR_SMEM);
     const double ns_tol2 = ctx->dtype == QB_F32 ? 1e-8 : 1e-16;
@@ -2616,7 +2628,9 @@ static qb_status factor_impl(qb_ctx ctx, void* Ain, int64_t m, int64_t n, int64_
         // CholeskyQR2 into Q_i / Q̄32_i is not in place and its usual single pass moves no data
         QB_TRY(ensure(ctx, ctx->X32, sizeof(float) * (size_t)(std::max(ldm, ldn) * w)));
         float* X32 = static_cast<float*>(ctx->X32.p);
-        {
+        if (tf_gram_on(ctx) && !small_orth(m, (int)w, rowsh)) {  // the passes read only the FP32 copy (R18d)
+          QB_TRY(launch_convert(ctx, static_cast<const float*>(Qi32), ctx->ldq, m, w, X32, ldm));
+        } else {
           const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((m * w + 255) / 256, 8 * ctx->num_sms));
           convert_dual_kernel<<<grid, 256, 0, ctx->stream>>>(Qi32, ctx->ldq, m, w, ctx->Y.d(), ldm, X32, ldm);
           QB_TRY(check_launch(ctx, "convert_dual"));
