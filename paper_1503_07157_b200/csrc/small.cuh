@@ -358,6 +358,7 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
   __shared__ double red[2][CHOL_THREADS / 32];
   __shared__ double s_part[2], s_tot, s_shift;
   __shared__ int s_fail;
+  __shared__ double s_lb[2][CHOL_NB];  // the pivot CTA's warp 0: pivot columns, then 1/diag
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cta = static_cast<int>(cluster.block_rank());
   const int nbk = (w + CHOL_NB - 1) / CHOL_NB;
@@ -428,6 +429,11 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
       if (i == j) v += shift;
       P[i * PLD + j] = v;
     }
+    // every 32-row block of this CTA's block column of L^-1 up to the last panel's, padding rows of a
+    // narrow last block included (their zeros meet the identity padding of L_KK^-1)
+    if (active)
+      for (int idx = tid; idx < (nbk - cta) * CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
+        X[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = 0.0;
     if (tid == 0) s_fail = 0;
     CHOL_TS(1);
     cluster.sync();  // panels loaded; no peer still reads the previous attempt's panels
@@ -459,6 +465,7 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
           // right-looking with a one-column lookahead: column jj+1 gets pivot jj's update first and
           // pivot jj+1 is formed before the rest of pivot jj's updates, so the dependent
           // pivot chain overlaps the independent column updates
+#ifdef QB_CHOL_SHFL  // round-1 variant: the pivot column broadcast by shuffles (2 SHFL per FP64 value)
           double l = pivot(0);
 #pragma unroll
           for (int jj = 0; jj < CHOL_NB; ++jj) {
@@ -477,6 +484,34 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
             }
             l = lnext;
           }
+#else
+          // the pivot column goes through shared memory (one store per lane, then broadcast loads:
+          // the single warp's shuffle pipe was the bottleneck, 12 us per 32 x 32 block); two buffers,
+          // because pivot jj+1 is formed (lookahead) before pivot jj's remaining updates read theirs
+          double l = pivot(0);
+          s_lb[0][lane] = l;
+          __syncwarp();
+#pragma unroll
+          for (int jj = 0; jj < CHOL_NB; ++jj) {
+            const double* sl = s_lb[jj & 1];
+            double lnext = 0.0;
+            if (jj + 1 < CHOL_NB) {
+              const double lc = sl[jj + 1];
+              if (lane >= jj + 1) a[jj + 1] = fma(-l, lc, a[jj + 1]);
+              lnext = pivot(jj + 1);
+              s_lb[(jj + 1) & 1][lane] = lnext;
+            }
+#pragma unroll
+            for (int c = 0; c < CHOL_NB; ++c) {  // fixed bounds: a[] stays in registers
+              if (c > jj + 1) {
+                const double lc = sl[c];
+                if (lane >= c) a[c] = fma(-l, lc, a[c]);
+              }
+            }
+            __syncwarp();  // buffer jj & 1 is rewritten by pivot jj + 2
+            l = lnext;
+          }
+#endif
           bad = __any_sync(0xffffffffu, bad);
           if (p == 0) CHOL_TS(4);
           // L11^-1, column `lane`, right-looking: x_r = v_r / L(r, r), then v_r2 -= L(r2, r) x_r for
@@ -484,6 +519,7 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
           double x[CHOL_NB];
 #pragma unroll
           for (int r = 0; r < CHOL_NB; ++r) x[r] = (r == lane) ? 1.0 : 0.0;
+#ifdef QB_CHOL_SHFL
 #pragma unroll
           for (int r = 0; r < CHOL_NB; ++r) {
             x[r] *= __shfl_sync(0xffffffffu, rdiag, r);
@@ -491,6 +527,21 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
             for (int r2 = 0; r2 < CHOL_NB; ++r2)
               if (r2 > r) x[r2] = fma(-__shfl_sync(0xffffffffu, a[r], r2), x[r], x[r2]);
           }
+#else
+          // L (identity-padded) and 1/diag to shared memory (S is free on the pivot CTA during its
+          // diagonal step); L(r2, r) is the same for every lane: broadcast loads
+#pragma unroll
+          for (int c = 0; c < CHOL_NB; ++c) S[lane * PLD + c] = (c <= lane) ? a[c] : 0.0;
+          s_lb[0][lane] = rdiag;
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < CHOL_NB; ++r) {
+            x[r] *= s_lb[0][r];
+#pragma unroll
+            for (int r2 = 0; r2 < CHOL_NB; ++r2)
+              if (r2 > r) x[r2] = fma(-S[r2 * PLD + r], x[r], x[r2]);
+          }
+#endif
           if (p == 0) CHOL_TS(5);
 #pragma unroll
           for (int r = 0; r < CHOL_NB; ++r) Di[r * PLD + lane] = (r >= lane) ? x[r] : 0.0;
@@ -522,8 +573,77 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
         __syncthreads();
         chol_rows_times_bt(S, S, 0, rows, nb, [&](int i, int c, double v) { P[i * PLD + c] -= v; });
       }
+      // the block columns of L^-1 (T = R^-1 = L^-T) whose diagonal blocks are done advance by one
+      // step while the later CTAs update their panels: CTA J's step K needs only L_KK^-1 and panel K
+      if (active && cta <= p) {  // block column J = cta of L^-1: its step K = p (panel p is final)
+        const int K = p;
+        double* XK = X + (K - cta) * CHOL_NB * PLD;
+        if (K == cta) {
+          for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
+            XK[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = Di[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)];
+        } else {  // X_KJ = -L_KK^-1 acc_K
+          chol_copy_rows(Dt, cluster.map_shared_rank(Di, K), 0, CHOL_NB);
+          __syncthreads();
+          const int r = tid >> 3, c0 = (tid & 7) * 4;  // thread owns X_KJ(r, c0..c0+3)
+          double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+#pragma unroll 8
+          for (int t = 0; t < CHOL_NB / 2; ++t) {
+            const int th = t + CHOL_NB / 2;
+            const double d = Dt[r * PLD + t], dh = Dt[r * PLD + th];
+            v0 = fma(d, XK[t * PLD + c0], v0);
+            v1 = fma(d, XK[t * PLD + c0 + 1], v1);
+            v2 = fma(d, XK[t * PLD + c0 + 2], v2);
+            v3 = fma(d, XK[t * PLD + c0 + 3], v3);
+            u0 = fma(dh, XK[th * PLD + c0], u0);
+            u1 = fma(dh, XK[th * PLD + c0 + 1], u1);
+            u2 = fma(dh, XK[th * PLD + c0 + 2], u2);
+            u3 = fma(dh, XK[th * PLD + c0 + 3], u3);
+          }
+          __syncthreads();
+          XK[r * PLD + c0] = -(v0 + u0);
+          XK[r * PLD + c0 + 1] = -(v1 + u1);
+          XK[r * PLD + c0 + 2] = -(v2 + u2);
+          XK[r * PLD + c0 + 3] = -(v3 + u3);
+        }
+        const int below = w - (K + 1) * CHOL_NB;  // rows of panel K under its diagonal block
+        if (below > 0) {
+          chol_copy_rows(S, cluster.map_shared_rank(P, K), CHOL_NB, below);
+          __syncthreads();
+          // acc_I += L_IK X_KJ for the rows below block K: out(i, c) = sum_k S(i, k) XK(k, c)
+          double* acc = X + (K + 1 - cta) * CHOL_NB * PLD;
+          for (int i = 4 * warp; i < below; i += 4 * (CHOL_THREADS / 32)) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+            const bool q1 = i + 1 < below, q2 = i + 2 < below, q3 = i + 3 < below;
+#pragma unroll 8
+            for (int k = 0; k < CHOL_NB / 2; ++k) {
+              const int kh = k + CHOL_NB / 2;
+              const double xk = XK[k * PLD + lane], xh = XK[kh * PLD + lane];
+              a0 = fma(S[i * PLD + k], xk, a0);
+              e0 = fma(S[i * PLD + kh], xh, e0);
+              if (q1) {
+                a1 = fma(S[(i + 1) * PLD + k], xk, a1);
+                e1 = fma(S[(i + 1) * PLD + kh], xh, e1);
+              }
+              if (q2) {
+                a2 = fma(S[(i + 2) * PLD + k], xk, a2);
+                e2 = fma(S[(i + 2) * PLD + kh], xh, e2);
+              }
+              if (q3) {
+                a3 = fma(S[(i + 3) * PLD + k], xk, a3);
+                e3 = fma(S[(i + 3) * PLD + kh], xh, e3);
+              }
+            }
+            acc[i * PLD + lane] += a0 + e0;
+            if (q1) acc[(i + 1) * PLD + lane] += a1 + e1;
+            if (q2) acc[(i + 2) * PLD + lane] += a2 + e2;
+            if (q3) acc[(i + 3) * PLD + lane] += a3 + e3;
+          }
+        }
+        __syncthreads();
+      }
+      // no barrier here: the next step's pivot CTA reads only its own shared memory until the next
+      // step's barrier publishes its panel, and nothing a peer reads is rewritten before that barrier
       CHOL_TS(8 + 2 * p);
-      cluster.sync();
       CHOL_TS(9 + 2 * p);
     }
     if (!failed) break;
@@ -558,77 +678,8 @@ __global__ void __cluster_dims__(CHOL_CTAS, 1, 1) __launch_bounds__(CHOL_THREADS
   }
 
   CHOL_TS(30);
-  // ---- block column J = cta of L^-1, right-looking over K = J .. nbk-1 (X rows 32J..w-1)
+  // ---- L^-1 is complete (its block columns advanced inside the factor loop)
   if (active) {
-    // every 32-row block up to the last panel's, padding rows of a narrow last block included
-    // (their zeros meet the identity padding of L_KK^-1 in the finalisation)
-    for (int idx = tid; idx < (nbk - cta) * CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
-      X[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = 0.0;
-    __syncthreads();
-    const int r = tid >> 3, c0 = (tid & 7) * 4;  // thread owns X_KJ(r, c0..c0+3) when finalising
-    for (int K = cta; K < nbk; ++K) {
-      double* XK = X + (K - cta) * CHOL_NB * PLD;
-      if (K == cta) {
-        for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += CHOL_THREADS)
-          XK[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)] = Di[(idx / CHOL_NB) * PLD + (idx % CHOL_NB)];
-      } else {  // X_KJ = -L_KK^-1 acc_K
-        chol_copy_rows(Dt, cluster.map_shared_rank(Di, K), 0, CHOL_NB);
-        __syncthreads();
-        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
-#pragma unroll 8
-        for (int t = 0; t < CHOL_NB / 2; ++t) {
-          const int th = t + CHOL_NB / 2;
-          const double d = Dt[r * PLD + t], dh = Dt[r * PLD + th];
-          v0 = fma(d, XK[t * PLD + c0], v0);
-          v1 = fma(d, XK[t * PLD + c0 + 1], v1);
-          v2 = fma(d, XK[t * PLD + c0 + 2], v2);
-          v3 = fma(d, XK[t * PLD + c0 + 3], v3);
-          u0 = fma(dh, XK[th * PLD + c0], u0);
-          u1 = fma(dh, XK[th * PLD + c0 + 1], u1);
-          u2 = fma(dh, XK[th * PLD + c0 + 2], u2);
-          u3 = fma(dh, XK[th * PLD + c0 + 3], u3);
-        }
-        __syncthreads();
-        XK[r * PLD + c0] = -(v0 + u0);
-        XK[r * PLD + c0 + 1] = -(v1 + u1);
-        XK[r * PLD + c0 + 2] = -(v2 + u2);
-        XK[r * PLD + c0 + 3] = -(v3 + u3);
-      }
-      const int below = w - (K + 1) * CHOL_NB;  // rows of panel K under its diagonal block
-      if (below <= 0) break;
-      chol_copy_rows(S, cluster.map_shared_rank(P, K), CHOL_NB, below);
-      __syncthreads();
-      // acc_I += L_IK X_KJ for the rows below block K: out(i, c) = sum_k S(i, k) XK(k, c)
-      double* acc = X + (K + 1 - cta) * CHOL_NB * PLD;
-      for (int i = 4 * warp; i < below; i += 4 * (CHOL_THREADS / 32)) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-        const bool q1 = i + 1 < below, q2 = i + 2 < below, q3 = i + 3 < below;
-#pragma unroll 8
-        for (int k = 0; k < CHOL_NB / 2; ++k) {
-          const int kh = k + CHOL_NB / 2;
-          const double xk = XK[k * PLD + lane], xh = XK[kh * PLD + lane];
-          a0 = fma(S[i * PLD + k], xk, a0);
-          e0 = fma(S[i * PLD + kh], xh, e0);
-          if (q1) {
-            a1 = fma(S[(i + 1) * PLD + k], xk, a1);
-            e1 = fma(S[(i + 1) * PLD + kh], xh, e1);
-          }
-          if (q2) {
-            a2 = fma(S[(i + 2) * PLD + k], xk, a2);
-            e2 = fma(S[(i + 2) * PLD + kh], xh, e2);
-          }
-          if (q3) {
-            a3 = fma(S[(i + 3) * PLD + k], xk, a3);
-            e3 = fma(S[(i + 3) * PLD + kh], xh, e3);
-          }
-        }
-        acc[i * PLD + lane] += a0 + e0;
-        if (q1) acc[(i + 1) * PLD + lane] += a1 + e1;
-        if (q2) acc[(i + 2) * PLD + lane] += a2 + e2;
-        if (q3) acc[(i + 3) * PLD + lane] += a3 + e3;
-      }
-      __syncthreads();
-    }
     for (int idx = tid; idx < w * nb; idx += CHOL_THREADS) {
       const int row = idx % w, c = idx / w;
       Tout[row + static_cast<int64_t>(p0 + c) * ldt] = row >= p0 ? X[(row - p0) * PLD + c] : 0.0;
