@@ -1836,9 +1836,10 @@ qb_status qb_pivoted_qr(qb_ctx ctx, int64_t* perm_out, const void** Qh_out, int6
     bool persist = !no_persist && (n + G - 1) / G <= QP_THREADS && G <= QP_WARPS * QP_CPW && qp_smem <= QP_MAX_SMEM;
     if (persist) {
       QB_SMEM_ATTR(qrcp_panel_kernel, (int)QP_MAX_SMEM);  // the largest launch
-      int per_sm = 0;
+      int per_sm = 0, coop = 0;
       QB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_panel_kernel, QP_THREADS, qp_smem));
-      persist = per_sm >= 1;
+      QB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
+      persist = per_sm >= 1 && coop != 0;  // one co-resident CTA per SM, or the multi-kernel schedule
     }
     QrcpPanelArgs pa{};
     if (persist) {
