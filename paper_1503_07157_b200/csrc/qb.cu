@@ -145,6 +145,7 @@ struct qb_ctx_s {
   cudaEvent_t ev_copy = nullptr;
   DevBuf QB, R, Usv, Vsv, Ssv, Wsv, Ut, Vt, Usv32, Vsv32, Ssv32, Swork;  // rqb_svd
   DevBuf Rq, Qh, Qt, qvn1, qvn2, qperm, qtau, qv, qparts, Rq32, Qh32, qw, qw2;  // qb_pivoted_qr
+  DevBuf Xsave;  // orth_blocked with R: the projected block before its CholeskyQR2
   DevBuf X32, T32;  // FP32 contexts: FP32 copies of a CholeskyQR pass's X and T
   DevBuf X32b;      // FP32 contexts: RN_32 of CholeskyQR2's scratch (when the caller takes an FP32 copy)
   DevBuf Bsp;       // FP32 GEMM: a small B operand split into hi / lo
@@ -967,19 +968,37 @@ qb_status cholqr2(qb_ctx ctx, const double* src, int64_t lds, double* dst, int64
 // Orthonormalise the m x l column-major panel X (ld ldx) in place for any l: 256 columns at a
 // time, two block Gram-Schmidt projections against the finished columns, then CholeskyQR2.
 // Uses ctx->Wsv (l x 256 row-major coefficients).
-qb_status orth_blocked(qb_ctx ctx, double* X, int64_t ldx, int64_t m, int64_t l) {
+qb_status orth_blocked(qb_ctx ctx, double* X, int64_t ldx, int64_t m, int64_t l, double* R = nullptr,
+                       int64_t ldr = 0) {
+  // R (optional, l x l column-major, ld ldr): X_in = Q R assembled from the projections themselves
+  // (block column j: the two passes' coefficients above the diagonal block, Q_j^T of the projected
+  // block on it, zero below) instead of a separate l x l x m product Q^T X_in
   const int64_t bp = round_up(kMaxB, 16);
   QB_TRY(ensure(ctx, ctx->Wsv, sizeof(double) * (size_t)(round_up(l, 16) * bp)));
+  if (R != nullptr) {
+    QB_TRY(ensure(ctx, ctx->Xsave, sizeof(double) * (size_t)(ldx * kMaxB)));
+    QB_CUDA(cudaMemsetAsync(R, 0, sizeof(double) * (size_t)(ldr * l), ctx->stream));
+  }
   for (int64_t j0 = 0; j0 < l; j0 += kMaxB) {
     const int64_t w = std::min<int64_t>(kMaxB, l - j0);
     double* Xj = X + j0 * ldx;
     for (int pass = 0; pass < 2 && j0 > 0; ++pass) {  // Xj -= X (X^T Xj), twice
       QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_ROW, (int)j0, (int)w, (int)m, X, ldx, Xj, ldx, ctx->Wsv.d(), bp, false,
                   nullptr));
+      if (R != nullptr) {
+        add_rowmajor_kernel<<<(int)std::min<int64_t>((j0 * w + 255) / 256, 8 * ctx->num_sms), 256, 0, ctx->stream>>>(
+            R + j0 * ldr, ldr, ctx->Wsv.d(), bp, j0, w);
+        QB_TRY(check_launch(ctx, "add_rowmajor"));
+      }
       QB_TRY(gemm(ctx, GEMM_NN, EPI_SUB_COL, (int)m, (int)w, (int)j0, X, ldx, ctx->Wsv.d(), bp, Xj, ldx, false,
                   nullptr));
     }
+    if (R != nullptr)
+      QB_CUDA(cudaMemcpy2DAsync(ctx->Xsave.p, ldx * 8, Xj, ldx * 8, m * 8, w, cudaMemcpyDeviceToDevice, ctx->stream));
     QB_TRY(cholqr2(ctx, Xj, ldx, Xj, ldx, m, (int)w));
+    if (R != nullptr)  // R_jj = Q_j^T (the projected block)
+      QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)w, (int)w, (int)m, Xj, ldx, ctx->Xsave.d(), ldx,
+                  R + j0 + j0 * ldr, ldr, false, nullptr));
   }
   return QB_OK;
 }
@@ -1348,7 +1367,7 @@ void qb_destroy(qb_ctx ctx) {
                     &ctx->QB,    &ctx->R,    &ctx->Usv,    &ctx->Vsv,  &ctx->Ssv, &ctx->Wsv,    &ctx->Ut,
                     &ctx->Vt,    &ctx->Usv32, &ctx->Vsv32, &ctx->Ssv32, &ctx->Swork, &ctx->Rq,    &ctx->Qh,
                     &ctx->Qt,    &ctx->qvn1, &ctx->qvn2,   &ctx->qperm, &ctx->qtau,  &ctx->qv,    &ctx->qparts,
-                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->qw2,   &ctx->X32,   &ctx->T32,
+                    &ctx->Rq32,  &ctx->Qh32, &ctx->qw,    &ctx->qw2,   &ctx->Xsave, &ctx->X32,   &ctx->T32,
                     &ctx->Bsp,   &ctx->X32b, &ctx->Jx,    &ctx->Jj,   &ctx->Jpart, &ctx->Jw,
                     &ctx->Jint,  &ctx->Jsig, &ctx->Jpairs, &ctx->Srec, &ctx->Strace, &ctx->Jq2, &ctx->Jm2};
   for (DevBuf* b : bufs)
@@ -1549,10 +1568,16 @@ qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const 
 
   // 1. Q_B = orth(B̄^T), 256 columns at a time
   QB_CUDA(cudaMemcpy2DAsync(QBm, ldn * 8, Bbar, ctx->ldb * 8, n * 8, k, cudaMemcpyDeviceToDevice, ctx->stream));
-  QB_TRY(orth_blocked(ctx, QBm, ldn, n, k));
-  // 2. R = Q_B^T B̄^T (k x k, column-major)
-  QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)k, (int)k, (int)n, QBm, ldn, Bbar, ctx->ldb, ctx->R.d(), ldk, false,
-              nullptr));
+  // 2. R (k x k, column-major, upper triangular) with B̄^T = Q_B R, from the projections of step 1
+  //    (QB_SVD_RGEMM=1: the explicit product Q_B^T B̄^T instead)
+  static const int rgemm = debug_env("QB_SVD_RGEMM");
+  if (rgemm) {
+    QB_TRY(orth_blocked(ctx, QBm, ldn, n, k));
+    QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)k, (int)k, (int)n, QBm, ldn, Bbar, ctx->ldb, ctx->R.d(), ldk, false,
+                nullptr));
+  } else {
+    QB_TRY(orth_blocked(ctx, QBm, ldn, n, k, ctx->R.d(), ldk));
+  }
   double t_front = 0.0;
   if (debug_env("QB_JAC_TRACE")) {  // diagnostics: host time of the front end (orth of B̄^T, R)
     const double t0 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();

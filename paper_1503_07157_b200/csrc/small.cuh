@@ -925,3 +925,19 @@ __global__ void __launch_bounds__(SCQR_THREADS) small_cholqr_kernel(const double
 
 }  // namespace qbk
 
+
+namespace qbk {
+
+// R(r, c) += W(r, c) for r < rows, c < cols: R column-major (ld ldr), W row-major (ld ldw) — the
+// block Gram-Schmidt coefficients of one projection pass added into R's block column.
+__global__ void __launch_bounds__(256) add_rowmajor_kernel(double* __restrict__ R, int64_t ldr,
+                                                           const double* __restrict__ W, int64_t ldw, int64_t rows,
+                                                           int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * 256ll + threadIdx.x; idx < total; idx += static_cast<int64_t>(gridDim.x) * 256) {
+    const int64_t c = idx / rows, r = idx - c * rows;
+    R[r + c * ldr] += W[r * ldw + c];
+  }
+}
+
+}  // namespace qbk
