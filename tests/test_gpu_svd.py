@@ -168,3 +168,34 @@ def test_svd_eps_tail_rule(qbmod):
     with pytest.raises(qbmod.QBError):
         c.svd(eps=-1.0)
     c.close()
+
+
+def test_svd_preconditioned_and_plain_in_fresh_processes():
+    """rqb_svd with and without the QR preconditioning step (QB_SVD_PRECOND=1 / 0; the default depends
+    on k), each against the oracle's SVD of the same QB in a fresh process (the variable is read once
+    per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import numpy as np, torch, synth
+from oracle import qb as oqb
+import paper_1503_07157_b200 as qbp
+A = synth.make_matrix_np(1500, 1200, synth.sigma("exp_150", 1200), 77)
+c = qbp.QB(0)
+g = c.factor(torch.from_numpy(np.asfortranarray(A)).cuda(), 1e-6, 128, 0, seed=5)
+Q, B = g["Q"].cpu().numpy(), g["B"].cpu().numpy()
+s = c.svd()
+U, S, V = s["U"].cpu().numpy(), s["S"].cpu().numpy(), s["V"].cpu().numpy()
+So = np.linalg.svd(B, compute_uv=False)
+nA = np.linalg.norm(A)
+assert np.abs(S - So[:len(S)]).max() <= 1e-10 * nA
+assert np.linalg.norm(U * S @ V.T - Q @ B) <= 1e-13 * nA
+assert np.abs(U.T @ U - np.eye(len(S))).max() <= 1e-12 and np.abs(V.T @ V - np.eye(len(S))).max() <= 1e-12
+print("ok", g["k"], len(S))
+'''
+    for v in ("0", "1"):
+        e = dict(os.environ, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""), QB_SVD_PRECOND=v)
+        p = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=300, cwd=root)
+        assert p.returncode == 0, p.stdout + p.stderr
