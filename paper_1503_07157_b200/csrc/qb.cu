@@ -1595,11 +1595,8 @@ qb_status rqb_svd(qb_ctx ctx, double eps, int64_t kkeep, int64_t* kk_out, const 
     dim3 grid((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
     transpose_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->R.d(), ldk, k, k, ctx->Jq2.d(), ldk);
     QB_TRY(check_launch(ctx, "transpose"));  // Jq2 = R^T (column-major)
-    QB_CUDA(cudaMemcpy2DAsync(ctx->Ut.p, ldk * 8, ctx->Jq2.p, ldk * 8, k * 8, k, cudaMemcpyDeviceToDevice, ctx->stream));
-    QB_TRY(orth_blocked(ctx, ctx->Jq2.d(), ldk, k, k));  // Jq2 = Q2
-    // R (column-major) <- R2 = Q2^T R^T
-    QB_TRY(gemm(ctx, GEMM_TN, EPI_STORE_COL, (int)k, (int)k, (int)k, ctx->Jq2.d(), ldk, ctx->Ut.d(), ldk, ctx->R.d(),
-                ldk, false, nullptr));
+    // Jq2 = Q2 and R (column-major) <- R2, assembled from the projections (R^T = Q2 R2)
+    QB_TRY(orth_blocked(ctx, ctx->Jq2.d(), ldk, k, k, ctx->R.d(), ldk));
   }
   // 3. one-sided Jacobi on X = R^T (kp x kp, zero-padded), J = I
   double* X = ctx->Jx.d();
