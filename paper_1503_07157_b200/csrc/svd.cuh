@@ -126,12 +126,17 @@ __global__ void __launch_bounds__(JST) jac_solve_kernel(const double* __restrict
   const double* src = part + static_cast<int64_t>(p) * nchunks * JPW * JPW;
   for (int idx = t; idx < JPW * JPW; idx += JST) {
     double s0 = 0.0, s1 = 0.0;  // chunk order: even chunks, odd chunks, then the pair (fixed)
-    int c = 0;
-    for (; c + 1 < nchunks; c += 2) {
-      s0 += __ldcg(src + static_cast<int64_t>(c) * JPW * JPW + idx);
-      s1 += __ldcg(src + static_cast<int64_t>(c + 1) * JPW * JPW + idx);
+    for (int c0 = 0; c0 < nchunks; c0 += 16) {  // sixteen partials in flight, summed in that order
+      double x[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        x[u] = c0 + u < nchunks ? __ldcg(src + static_cast<int64_t>(c0 + u) * JPW * JPW + idx) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; u += 2) {
+        if (c0 + u < nchunks) s0 += x[u];
+        if (c0 + u + 1 < nchunks) s1 += x[u + 1];
+      }
     }
-    if (c < nchunks) s0 += __ldcg(src + static_cast<int64_t>(c) * JPW * JPW + idx);
     G[(idx / JPW) * JGLD + idx % JPW] = s0 + s1;
     Dl[(idx / JPW) * JGLD + idx % JPW] = 0.0;
   }
