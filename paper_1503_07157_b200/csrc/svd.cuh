@@ -259,8 +259,16 @@ __global__ void __launch_bounds__(JTHREADS) jac_update_kernel(double* __restrict
   const int r0 = blockIdx.y * JRC, rows = min(JRC, nrows - r0);
   if (rows <= 0) return;
   const double* dsrc = Dg + static_cast<int64_t>(p) * JPW * JPW;
-  for (int idx = t; idx < JPW * JPW; idx += JTHREADS) D[(idx / JPW) * JLDD + idx % JPW] = __ldcg(dsrc + idx);
+  constexpr int JDL = JPW * JPW / JTHREADS;  // Δ entries per thread, loaded with the panel (all in flight)
+  double dv[JDL];
+#pragma unroll
+  for (int u = 0; u < JDL; ++u) dv[u] = __ldcg(dsrc + t + u * JTHREADS);
   jac_load_panel(T, M, ld, pr, r0, rows, t);
+#pragma unroll
+  for (int u = 0; u < JDL; ++u) {
+    const int idx = t + u * JTHREADS;
+    D[(idx / JPW) * JLDD + idx % JPW] = dv[u];
+  }
   __syncthreads();
   const int m = lane >> 2, kk = lane & 3;
   double acc[2][JTN][2];
