@@ -27,7 +27,10 @@ namespace qbk {
 #endif
 constexpr int JNB = QB_JAC_NB;    // block width (16 or 32)
 constexpr int JPW = 2 * JNB;      // pair width
-constexpr int JRC = 128;          // rows per chunk (Gram partials, panel updates)
+#ifndef QB_JAC_RC
+#define QB_JAC_RC 128
+#endif
+constexpr int JRC = QB_JAC_RC;     // rows per chunk (Gram partials, panel updates): 128 or 256
 constexpr int JLDR = JRC + 4;     // row stride of a transposed chunk T[col][row] (= 4 mod 16 words:
                                   // conflict-free DMMA fragment loads)
 constexpr int JLDD = JPW + 4;     // row stride of Δ in shared memory (= 4 mod 16 words)
@@ -38,7 +41,9 @@ constexpr int JGRAM_SMEM = JPW * JLDR * 8;
 constexpr int JUPD_SMEM = (JPW * JLDR + JPW * JLDD) * 8;
 constexpr int JTN = JPW / 8;                  // 8 x 8 DMMA tiles per dimension of a pair
 constexpr int JTPW = JTN * JTN / (JTHREADS / 32);  // Gram tiles per warp (same row tile)
-static_assert((JPW == 32 || JPW == 64) && JTHREADS == 256 && JRC == 128, "fragment maps below assume these");
+static_assert((JPW == 32 || JPW == 64) && JTHREADS == 256 && (JRC == 128 || JRC == 256),
+              "fragment maps below assume these");
+constexpr int JRT = JRC / 64;  // 8-row tiles per warp in the panel update
 
 // Column j (0..JPW-1) of pair p's panel: block I or J of the pair, as a global column index.
 __device__ __forceinline__ int jac_col(const int2 pr, int j) {
@@ -271,29 +276,30 @@ __global__ void __launch_bounds__(JTHREADS) jac_update_kernel(double* __restrict
   }
   __syncthreads();
   const int m = lane >> 2, kk = lane & 3;
-  double acc[2][JTN][2];
+  double acc[JRT][JTN][2];
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < JRT; ++h)
 #pragma unroll
     for (int cb = 0; cb < JTN; ++cb) acc[h][cb][0] = acc[h][cb][1] = 0.0;
 #pragma unroll
   for (int ks = 0; ks < JPW; ks += 4) {
     // A(m, kk) = chunk(8 rb + m, ks + kk) = T[ks + kk][8 rb + m];  B(kk, n) = Δ(ks + kk, 8 cb + n), n = lane >> 2
-    const double a0 = T[(ks + kk) * JLDR + 16 * w + m];
-    const double a1 = T[(ks + kk) * JLDR + 16 * w + 8 + m];
+    double a[JRT];
+#pragma unroll
+    for (int h = 0; h < JRT; ++h) a[h] = T[(ks + kk) * JLDR + 8 * JRT * w + 8 * h + m];
 #pragma unroll
     for (int cb = 0; cb < JTN; ++cb) {
       const double b = D[(ks + kk) * JLDD + 8 * cb + m];
-      dmma_8x8x4(acc[0][cb][0], acc[0][cb][1], a0, b);
-      dmma_8x8x4(acc[1][cb][0], acc[1][cb][1], a1, b);
+#pragma unroll
+      for (int h = 0; h < JRT; ++h) dmma_8x8x4(acc[h][cb][0], acc[h][cb][1], a[h], b);
     }
   }
   __syncthreads();  // every warp has read its A fragments: update T in place
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < JRT; ++h)
 #pragma unroll
     for (int cb = 0; cb < JTN; ++cb) {
-      const int row = 16 * w + 8 * h + m, col = 8 * cb + 2 * kk;
+      const int row = 8 * JRT * w + 8 * h + m, col = 8 * cb + 2 * kk;
       T[col * JLDR + row] += acc[h][cb][0];
       T[(col + 1) * JLDR + row] += acc[h][cb][1];
     }
