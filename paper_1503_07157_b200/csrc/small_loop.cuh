@@ -153,10 +153,19 @@ __device__ __forceinline__ void gather_rows(cg::cluster_group& cl, double* Qf, c
                                             int w) {
   const unsigned ncta = cl.num_blocks();
   #pragma unroll 1
-  for (int e = threadIdx.x; e < m * w; e += SL_THREADS) {
-    const int tt = e / m, i = e % m;
-    const unsigned r = static_cast<unsigned>(i / mr);
-    if (r < ncta) Qf[e] = cl.map_shared_rank(Ys, r)[tt * mr + (i - static_cast<int>(r) * mr)];
+  for (int e0 = threadIdx.x; e0 < m * w; e0 += 8 * SL_THREADS) {  // eight DSMEM loads in flight
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * SL_THREADS, tt = e / m, i = e % m;
+      const unsigned r = static_cast<unsigned>(i / mr);
+      v[u] = (e < m * w && r < ncta) ? cl.map_shared_rank(Ys, r)[tt * mr + (i - static_cast<int>(r) * mr)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * SL_THREADS, i = e % m;
+      if (e < m * w && static_cast<unsigned>(i / mr) < ncta) Qf[e] = v[u];
+    }
   }
   __syncthreads();
 }
