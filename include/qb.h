@@ -275,7 +275,9 @@ int qb_svd_sweeps(qb_ctx ctx);
 /* Partial pivoted QR from the context's last factorization (NEXT-4):
  * B P = Q~ R by Householder QR with column pivoting of the k x n factor B (LAPACK dlaqp2
  * order: first column of largest partial norm, norms downdated and recomputed on cancellation),
- * Q^ = Q Q~, so that A P ~ Q^ R.  FP64 internally.
+ * Q^ = Q Q~, so that A P ~ Q^ R.  FP64 internally; computed by panels of 32 pivots (LAPACK
+ * dlaqps: the trailing update deferred to one GEMM per panel), which leaves the pivots of the
+ * unblocked order unchanged.
  * Outputs: perm (HOST, n entries, caller-owned): column j of A P is column perm[j] of A;
  * Q^ device column-major m x k (*ldqh); R device ROW-major k x n upper trapezoidal (*ldr);
  * both context-owned, in the context's dtype, valid until the next call.  k = 0 gives the
