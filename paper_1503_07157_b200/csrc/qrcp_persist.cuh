@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
   __shared__ int s_cnt[QP_WARPS], s_list[QP_THREADS];
   __shared__ double s_res[QP_THREADS];
   __shared__ double s_tot[33];
+  __shared__ double s_fg[QRCP_NB + 1][32];  // flagged group: F rows (and scale F(j, kk)) per column
+  __shared__ int s_col[32];
 
   double* __restrict__ B = a.B;
   const int64_t ldb = a.ldb, ldf = a.ldf;
@@ -414,54 +416,59 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qrcp_panel_kernel(const QrcpPan
       }
       if (recompute) s_list[base + __popc(ballot & ((1u << lane) - 1u))] = tid;
       __syncthreads();
-      const int rows = l - i - 1, slice = (rows + QP_WARPS - 1) / QP_WARPS;
-      const int ra = i + 1 + warp * slice, rz = min(l, ra + slice);
+      // lanes over rows (each lane's V row in registers, loaded once per pass), the group's columns
+      // in passes of 8 (their F rows broadcast from shared memory, 8 loads in flight per lane);
+      // per column: lane partials over the lane's rows, xor-tree warp sums, then warps in order
       for (int g = 0; g < total; g += 32) {
-        const bool act = g + lane < total;
-        const int tl = act ? s_list[g + lane] : 0;
-        const int col = act ? cj0 + tl : i;
-        double f2[QRCP_NB];
+        const int gn = min(32, total - g);
+        if (tid < 32) {
+          const int tl = tid < gn ? s_list[g + tid] : 0;
+          s_col[tid] = tid < gn ? cj0 + tl : i;
 #pragma unroll
-        for (int q = 0; q < QRCP_NB; ++q) f2[q] = act && q < kk ? sF[q * cwp + tl] : 0.0;
-        const double fk = act ? sF[kk * cwp + tl] * scale : 0.0;  // v_r = scale x_r
-        double sa = 0.0, sb = 0.0;
-        int r = ra;
-        for (; r + 1 < rz; r += 2) {  // two rows in flight
-          const double* a0 = B + static_cast<int64_t>(r) * ldb;
-          const double* a1 = a0 + ldb;
-          double x0 = fma(-xs[r - i], fk, ldcg(a0 + col)), x1 = fma(-xs[r + 1 - i], fk, ldcg(a1 + col));
-#pragma unroll
-          for (int q = 0; q < QRCP_NB; q += 2)
-            if (q < kk) {
-              const double2 u0 = __ldcg(reinterpret_cast<const double2*>(a0 + i0 + q));
-              const double2 u1 = __ldcg(reinterpret_cast<const double2*>(a1 + i0 + q));
-              x0 = fma(-u0.x, f2[q], x0);
-              x1 = fma(-u1.x, f2[q], x1);
-              x0 = fma(-u0.y, f2[q + 1], x0);
-              x1 = fma(-u1.y, f2[q + 1], x1);
-            }
-          sa = fma(x0, x0, sa);
-          sb = fma(x1, x1, sb);
+          for (int q = 0; q < QRCP_NB; ++q) s_fg[q][tid] = tid < gn && q < kk ? sF[q * cwp + tl] : 0.0;
+          s_fg[QRCP_NB][tid] = tid < gn ? sF[kk * cwp + tl] * scale : 0.0;  // v_r = scale x_r
         }
-        if (r < rz) {
-          const double* a0 = B + static_cast<int64_t>(r) * ldb;
-          double x0 = fma(-xs[r - i], fk, ldcg(a0 + col));
-#pragma unroll
-          for (int q = 0; q < QRCP_NB; q += 2)
-            if (q < kk) {
-              const double2 u0 = __ldcg(reinterpret_cast<const double2*>(a0 + i0 + q));
-              x0 = fma(-u0.x, f2[q], x0);
-              x0 = fma(-u0.y, f2[q + 1], x0);
-            }
-          sa = fma(x0, x0, sa);
-        }
-        sa += sb;
-        s_red[warp][lane] = sa;
         __syncthreads();
-        if (warp == 0 && act) {
+        for (int c0 = 0; c0 < gn; c0 += 8) {
+          double acc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+          for (int rb = i + 1 + warp * 32; rb < l; rb += QP_WARPS * 32) {
+            const int r = rb + lane;
+            const bool rv = r < l;
+            const double* ar = B + static_cast<int64_t>(rv ? r : i) * ldb;
+            double v[QRCP_NB];
+#pragma unroll
+            for (int q = 0; q < QRCP_NB; q += 2) {
+              double2 u2 = make_double2(0.0, 0.0);
+              if (rv && q < kk) u2 = __ldcg(reinterpret_cast<const double2*>(ar + i0 + q));
+              v[q] = u2.x;
+              v[q + 1] = q + 1 < kk ? u2.y : 0.0;
+            }
+            const double xv = rv ? xs[r - i] : 0.0;
+            double x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = rv && c0 + u < gn ? ldcg(ar + s_col[c0 + u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              double y = fma(-xv, s_fg[QRCP_NB][c0 + u], x[u]);
+#pragma unroll
+              for (int q = 0; q < QRCP_NB; ++q)
+                if (q < kk) y = fma(-v[q], s_fg[q][c0 + u], y);
+              acc[u] = fma(y, y, acc[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double t2 = __shfl_sync(0xffffffffu, warp_sum(acc[u]), 0);
+            if (lane == 0) s_red[warp][c0 + u] = t2;
+          }
+        }
+        __syncthreads();
+        if (tid < gn) {
           double t2 = 0.0;
-          for (int w = 0; w < QP_WARPS; ++w) t2 += s_red[w][lane];
-          s_res[tl] = sqrt(t2);
+          for (int w = 0; w < QP_WARPS; ++w) t2 += s_red[w][tid];
+          s_res[s_list[g + tid]] = sqrt(t2);
         }
         __syncthreads();
       }
