@@ -436,7 +436,12 @@ qb_status launch_gemm_t(qb_ctx ctx, const CUtensorMap& ta, const CUtensorMap& tb
 
 constexpr int kBN = 64;
 
-int choose_splits(int tiles, int nkt, int slots, int max_splits) {
+// out_elems > 0 (FP64 products): the split-K reduction's cost counts too for large outputs — it
+// reads s partials of the output and writes it once (≈ 3 TB/s; ≈ 2 us per unit of the model's
+// wave x k-tile time), which outweighs the wave-quantisation gain of splitting a short-K product with
+// a large output (T's X T and re-projection updates: 55-100 us reductions on 100-340 us products).
+int choose_splits(int tiles, int nkt, int slots, int max_splits, double out_elems = 0.0) {
+  static const int no_rcost = debug_env("QB_SPLIT_NO_RCOST");
   int best = 1;
   double best_t = 1e300;
   for (int s = 1; s <= max_splits; ++s) {
@@ -444,7 +449,11 @@ int choose_splits(int tiles, int nkt, int slots, int max_splits) {
     if (s > 1 && per < 4) break;
     const int units = tiles * s;
     const int waves = (units + slots - 1) / slots;
-    const double t = waves * (per + 3.0) * (s > 1 ? 1.0 + 0.003 * s : 1.0);
+    // counted for large outputs only (>= 4M entries, 32 MB per partial: T, T1, C5); at C3's 10 MB
+    // partials the model overestimates the reduction and its choice measured slower (45.7 -> 47.7 ms)
+    const double rbytes = (s + 1) * out_elems * 8.0;
+    const double reduce_units = (s > 1 && !no_rcost && out_elems >= 4e6) ? rbytes / 3e12 * 1e6 / 2.0 : 0.0;
+    const double t = waves * (per + 3.0) * (s > 1 ? 1.0 + 0.003 * s : 1.0) + reduce_units;
     if (t < best_t * 0.995) {
       best_t = t;
       best = s;
@@ -499,7 +508,9 @@ qb_status gemm(qb_ctx ctx, int layout, int epi, int M, int N, int K, const doubl
   int bn = 64;
   p.tiles_n = (N + bn - 1) / bn;
   int splits = 1;
-  if (allow_split) splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 296);
+  if (allow_split)
+    splits = choose_splits(p.tiles_m * p.tiles_n, p.nkt, ctx->num_sms * GemmCfg<64>::MIN_BLOCKS, 296,
+                           static_cast<double>(M) * N);
   const bool subtract = epi == EPI_SUB_COL;
   static const int wide_env = debug_env("QB_WIDE_DOWNDATE");  // experiment: 1 = 128-wide tiles
   if (subtract && splits == 1 && wide_env > 0 && N >= 2048) {
